@@ -1,0 +1,416 @@
+"""bench.py -- the driver's benchmark contract for the B200 iPregel superstep.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg4] [--apps pagerank,cc,sssp]
+
+One STEP = one pass of the whole hot path over the synthetic input: PageRank (10 gather
+supersteps, fp64), Hash-Min CC to convergence and SSSP from vertex 0 to convergence, each run
+through the C ABI (ipregel_run) on BASELINE.json configs[4] (R-MAT scale 26, edgefactor 28,
+seed 5: 67,108,864 vertices, 1.879e9 edges, int32 CSR + CSC, u32 weights in [1,64]).
+
+metric: GTEPS = messages delivered (the method's edge work: every superstep s >= 1 delivers the
+messages of superstep s-1) per second of device time, whole job (all ranks).  The inputs
+(7.5 GB per adjacency array) are larger than L2, so no flush is needed between steps.
+
+Extra keys: roofline (dominant kernel: the PageRank pull gather, algorithmic bytes per launch
+12E + 16N over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs), cpu_baseline
+(the oracle on a bounded sample, rank 0, N=1), e2e (host buffers through the C ABI, copies
+inside the timed region), clocks (nvidia-smi sampled during the timed region), gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GTEPS per superstep and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "GTEPS"
+APP_CODES = {"pagerank": 0, "cc": 1, "sssp": 2}
+# bounded sample of the cfg4 workload for the oracle: same generator and parameters
+# (a, b, c, d, edgefactor 28, seed 5), 1/64 of the vertices
+SAMPLE_SCALE = 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ helpers
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the PageRank pull kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "pr_pull_ncu_summary.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def delivered_messages(stats):
+    """Messages delivered by supersteps 1..S-1 = messages sent in supersteps 0..S-2."""
+    m = stats["messages"].astype(np.int64)
+    return int(m[:-1].sum()) if len(m) > 1 else 0
+
+
+def build_graph_device(cfg_name, rank, world):
+    import torch
+
+    import inputs
+    import paper_2010_08781_b200 as ipr
+    from inputs.gpu import config_graph_device
+    cfg = inputs.CONFIGS[cfg_name]
+    t = time.time()
+    g = config_graph_device(cfg, weighted=True)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] graph {cfg_name}: N={g['n']} E={g['e']} built in {time.time() - t:.1f}s")
+    if world == 1:
+        part = ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
+                                  g["csr_idx"], g["csc_w"], g["csr_w"])
+        return g, part, np.array([0, g["n"]])
+    bounds = ipr.edge_balanced_bounds(g["csc_off"].cpu().numpy(), world, g["csr_off"].cpu().numpy())
+    parts = ipr.split_partitions(g["n"], g["e"], bounds, g["csc_off"], g["csc_idx"], g["csr_off"],
+                                 g["csr_idx"], g["csc_w"], g["csr_w"])
+    # keep only this rank's slices alive (copies, so the full graph can be freed)
+    p = parts[rank]
+    own = ipr.Partition(p.num_vertices, p.num_edges, p.vertex_begin, p.vertex_end,
+                        p.csc_offsets.clone(), p.csc_indices.clone(), p.csr_offsets.clone(),
+                        p.csr_indices.clone(), p.csc_weights.clone(), p.csr_weights.clone())
+    del parts
+    for k in list(g.keys()):
+        if k not in ("n", "e"):
+            g[k] = None
+    torch.cuda.empty_cache()
+    return g, own, bounds
+
+
+def run_step(G, apps, iterations=10):
+    out = {}
+    for app in apps:
+        G.run(app, mode="pull" if app == "pagerank" else "auto", iterations=iterations)
+        out[app] = G.stats()
+    return out
+
+
+# ------------------------------------------------------------------------------ cpu baseline
+def cpu_baseline(apps, scale=SAMPLE_SCALE, repeats=1):
+    """The oracle (single-threaded C Pregel interpreter) on a bounded sample of cfg4."""
+    import inputs
+    import oracle
+    cfg = inputs.CONFIGS["cfg4"]
+    src, dst, w = inputs.rmat_coo(scale, cfg.edgefactor, cfg.seed, weighted=True)
+    n = 1 << scale
+    msgs = 0
+    secs = 0.0
+    per_app = {}
+    for _ in range(repeats):
+        for app in apps:
+            r = oracle.run(APP_CODES[app], n, src, dst, w if app == "sssp" else None,
+                           k=cfg.iterations, source=0)
+            d = int(r["messages"][:-1].sum()) if r["supersteps"] > 1 else 0
+            s = float(r["seconds"].sum())
+            msgs += d
+            secs += s
+            per_app[app] = {"gteps": d / s / 1e9 if s > 0 else None, "seconds": s,
+                            "supersteps": int(r["supersteps"])}
+    return {"value": msgs / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"R-MAT scale {scale}, edgefactor {cfg.edgefactor}, seed {cfg.seed} "
+                       f"(cfg4's generator at 1/{1 << (cfg.scale - scale)} of the vertices, "
+                       f"E={len(src)}); {'+'.join(apps)} to termination; superstep loop only "
+                       f"(adjacency build excluded, PAPER.md:428)"),
+            "seconds": secs, "apps": per_app}
+
+
+def reference_arm(args):
+    """--impl reference: the oracle as it stands, on the host cores, same metric/unit."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    apps = args.apps
+    for _ in range(args.warmup):
+        cpu_baseline(apps, scale=args.sample_scale)
+    t_steps = []
+    res = None
+    for _ in range(args.steps):
+        res = cpu_baseline(apps, scale=args.sample_scale)
+        t_steps.append(res["seconds"])
+    value = res["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(t_steps) / len(t_steps), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+        "config": {"workload": f"{args.config} sample: R-MAT scale {args.sample_scale}, ef 28, seed 5",
+                   "apps": apps},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": res["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--apps", default="pagerank,cc,sssp")
+    ap.add_argument("--sample-scale", type=int, default=SAMPLE_SCALE)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.apps = [a for a in args.apps.split(",") if a]
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_08781_b200 as ipr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    ipr.device_check(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    g, part, bounds = build_graph_device(args.config, rank, world)
+    comm = ipr.Comm.from_process_group(local) if world > 1 else None
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        G = ipr.Graph(part, comm=comm, stream=stream)
+    n, e = g["n"], g["e"]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            run_step(G, args.apps)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, events on the library's stream, barrier + sync on both sides
+    launches0 = ipr.kernel_launches()
+    per_step = []
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                per_step.append(run_step(G, args.apps))
+        stop.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = ipr.kernel_launches() - launches0
+    ms_total = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+
+    # work per step (identical every step; counters are global, so rank-independent)
+    msgs = sum(delivered_messages(st) for st in per_step[0].values())
+    value = msgs / (ms_per_step * 1e-3) / 1e9
+
+    # dominant kernel: the PageRank pull gather (+ its fixup), timed by the library's events
+    peak, peak_src = measured_peak()
+    apps_out = {}
+    for app in args.apps:
+        sts = [step[app] for step in per_step]
+        t_app = float(np.mean([s["time_ms"].sum() for s in sts]))
+        d = delivered_messages(sts[0])
+        apps_out[app] = {"gteps": d / (t_app * 1e-3) / 1e9, "ms": t_app,
+                         "supersteps": int(sts[0]["supersteps"]),
+                         "modes": "".join("ilp"[m] for m in sts[0]["mode"])}
+    roof = None
+    if "pagerank" in args.apps:
+        sts = [step["pagerank"] for step in per_step]
+        k_ms = np.concatenate([s["kernel_ms"][1:] for s in sts])
+        mb = np.concatenate([s["model_bytes"][1:] for s in sts]).astype(np.float64)
+        achieved = float(np.mean(mb) / (np.mean(k_ms) * 1e-3) / 1e9)
+        if world > 1:
+            t = torch.tensor([float(np.mean(k_ms))], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            achieved = float(np.mean(mb) / (float(t.item()) * 1e-3) / 1e9)  # per-rank bytes
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(),
+                "kernel": "k_pull_tiles<PageRankPull> + k_pull_fixup",
+                "bytes_per_launch": float(np.mean(mb)),
+                "model": "12 B/edge (4 B index + 8 B gathered f64 outbox) + 16 B/vertex",
+                "avg_launch_ms": float(np.mean(k_ms)), "peak_source": peak_src,
+                "frac_of_8TBps": achieved / 8000.0}
+        apps_out["pagerank"]["superstep_ms_median"] = float(np.median(
+            np.concatenate([s["time_ms"][1:] for s in sts])))
+        apps_out["pagerank"]["gteps_per_gather_superstep"] = float(
+            e / (apps_out["pagerank"]["superstep_ms_median"] * 1e-3) / 1e9)
+
+    # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = e2e_measure(g, args, msgs, stream)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: R-MAT scale 26 ef 28 seed 5, "
+                               f"{'+'.join(args.apps)} per step",
+                   "n": n, "e": e, "parallelism": f"1D destination partition x{world}",
+                   "l2": "inputs larger than L2 (7.5 GB per adjacency array), no flush",
+                   "apps": apps_out},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.apps)
+        line["cpu_baseline"].pop("apps", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    G.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(g, args, msgs_per_step, stream):
+    """Same work through ipregel_graph_create(MEMORY_HOST) from pinned host arrays."""
+    import torch
+
+    import paper_2010_08781_b200 as ipr
+    host = {}
+    h2d = 0
+    for k in ("csc_off", "csc_idx", "csc_w", "csr_off", "csr_idx", "csr_w"):
+        t = g[k]
+        if t is None:
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        host[k] = h.numpy()
+        h2d += h.numel() * h.element_size()
+    part = ipr.full_partition(g["n"], g["e"], host["csc_off"], host["csc_idx"], host["csr_off"],
+                              host["csr_idx"], host["csc_w"], host["csr_w"])
+    out_pr = torch.empty(g["n"], dtype=torch.float64, pin_memory=True)
+    out_u = torch.empty(g["n"], dtype=torch.int32, pin_memory=True)
+    d2h = 0
+    steps = max(1, min(args.steps, 3))
+
+    def one():
+        nonlocal d2h
+        d2h = 0
+        G = ipr.Graph(part, stream=stream)
+        for app in args.apps:
+            G.run(app, mode="pull" if app == "pagerank" else "auto")
+            o = out_pr if app == "pagerank" else out_u
+            ipr.load().ipregel_get_values(G.handle, o.data_ptr(), o.numel() * o.element_size(), 0)
+            d2h += o.numel() * o.element_size()
+        G.close()
+
+    one()  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        one()
+    stop.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    ms = start.elapsed_time(stop) / steps
+    return {"value": msgs_per_step / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "wall_ms_per_step": wall * 1e3,
+            "steps": steps,
+            "path": "ipregel_graph_create(IPREGEL_MEMORY_HOST, pinned) + ipregel_run x apps + "
+                    "ipregel_get_values(host) + destroy"}
+
+
+if __name__ == "__main__":
+    main()

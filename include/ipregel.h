@@ -1,0 +1,226 @@
+/*
+ * include/ipregel.h -- C ABI of the B200-native iPregel superstep library
+ * (libipregel.so, built from paper_2010_08781_b200/csrc/).
+ *
+ * What it computes.  iPregel's synchronous vertex-centric superstep
+ * (Sec. 4.2, Fig. 3): every active vertex runs compute(),
+ * sends one message per out-edge (a broadcast), messages are
+ * folded at the recipient by the program's combiner into a single-slot
+ * mailbox (Sec. 4.3.3), and vertices that voted to halt are
+ * skipped via selection bypass (Sec. 4.3.1).  The vertex
+ * programs are the paper's three benchmarks (Sec. 6): PageRank (Fig. 8,
+ * PAPER.md:276-298), Hash-Min connected components (Fig. 9, :332-350) and
+ * single-source shortest paths (Fig. 10, :372-396, generalised to uint32
+ * edge weights; weights == NULL is exactly Fig. 10's "+1").
+ *
+ * A user program is the pair (compute, combine) of Fig. 1 (PAPER.md:94-100,
+ * :131).  Device code cannot cross a C ABI at run time, so compute is chosen
+ * by `ipregel_app` and the combiner is passed and validated against it
+ * (PageRank: SUM; CC and SSSP: MIN).  The paper's compile-time optimisation
+ * flags (push/pull) become `ipregel_mode`.
+ *
+ * Conventions for every entry point:
+ *   - Returns an ipregel_status.  Nothing aborts, throws or exits.  A
+ *     thread-local message describing the last failure is available from
+ *     ipregel_last_error().
+ *   - Pointers are plain host or device pointers as stated per argument.
+ *     Device pointers must be addresses in the current CUDA device's memory
+ *     (any allocator: cudaMalloc, PyTorch's caching allocator, ...).
+ *   - `stream` arguments are a cudaStream_t passed as void* (NULL = the
+ *     legacy default stream).  All device work of a graph handle runs on the
+ *     stream it was created with.
+ *   - A CUDA or NCCL failure poisons the handle: later calls on it return
+ *     IPREGEL_ERR_STATE.  Only ipregel_graph_destroy remains valid.
+ *   - One host thread at a time per handle.
+ */
+#ifndef IPREGEL_H
+#define IPREGEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IPREGEL_ABI_VERSION 1
+
+typedef enum {
+    IPREGEL_OK = 0,
+    IPREGEL_ERR_INVALID_ARGUMENT = 1, /* NULL required pointer, sizes out of range, app/combiner
+                                         mismatch, source >= N, out_bytes mismatch,
+                                         max_supersteps == 0, unknown enum                      */
+    IPREGEL_ERR_INVALID_GRAPH = 2,    /* validate != 0 and: offsets[0] != 0, offsets not
+                                         monotone, offsets[rows] != edge count, an index
+                                         outside [0, N)                                         */
+    IPREGEL_ERR_OUT_OF_MEMORY = 3,    /* device or host allocation failed; nothing leaked      */
+    IPREGEL_ERR_CUDA = 4,             /* a CUDA call failed; the handle is poisoned             */
+    IPREGEL_ERR_NCCL = 5,             /* an NCCL call failed; the handle is poisoned            */
+    IPREGEL_ERR_MAX_SUPERSTEPS = 6,   /* the superstep guard stopped a run that had more work;
+                                         values/stats hold the state after the last executed
+                                         superstep                            */
+    IPREGEL_ERR_STATE = 7,            /* call order violated (get_values before a run,
+                                         use after poison, comm/graph mismatch)                 */
+    IPREGEL_ERR_UNSUPPORTED = 8       /* device is not sm_100, size beyond int32 indexing,
+                                         NCCL unavailable, mode not available for the app       */
+} ipregel_status;
+
+/* The vertex programs of PAPER.md Sec. 6 (Figs. 8, 9, 10). */
+typedef enum {
+    IPREGEL_APP_PAGERANK = 0,   /* values: double[N]   -- ranks after superstep k              */
+    IPREGEL_APP_HASHMIN_CC = 1, /* values: uint32_t[N] -- min vertex id of the component in the
+                                   symmetrised graph (every edge taken in both directions)     */
+    IPREGEL_APP_SSSP = 2        /* values: uint32_t[N] -- distance from the source,
+                                   IPREGEL_INF (0xFFFFFFFF) if unreachable; sums saturate      */
+} ipregel_app;
+
+/* Fig. 1's combine: Fig. 8 sums; Fig. 5 keeps the minimum (:213-221). */
+typedef enum { IPREGEL_COMBINE_SUM = 0, IPREGEL_COMBINE_MIN = 1 } ipregel_combiner;
+
+/* Message delivery (Sec. 4.3.2).  PULL: every recipient gathers from its
+ * in-neighbours' outboxes (CSC gather-combine).  PUSH: every sender in the frontier folds its
+ * message into the recipient's slot with a lock-free atomic combine (the optimisation the paper
+ * leaves as future work).  AUTO: per superstep, push when the previous
+ * superstep sent few messages, else pull (Ligra's switch the paper names). */
+typedef enum { IPREGEL_MODE_AUTO = 0, IPREGEL_MODE_PULL = 1, IPREGEL_MODE_PUSH = 2 } ipregel_mode;
+
+/* Where the arrays of an ipregel_graph_desc live. */
+typedef enum {
+    IPREGEL_MEMORY_DEVICE = 0, /* device pointers, BORROWED: must stay valid and unmodified until
+                                  ipregel_graph_destroy; no copy is made                         */
+    IPREGEL_MEMORY_HOST = 1    /* host pointers (pinned or pageable): copied into library-owned
+                                  device memory during ipregel_graph_create                       */
+} ipregel_memory;
+
+#define IPREGEL_INF 0xFFFFFFFFu
+
+typedef struct ipregel_graph ipregel_graph; /* opaque */
+typedef struct ipregel_comm ipregel_comm;   /* opaque; NULL means a single GPU */
+
+/*
+ * One partition of a directed graph with N vertices and E edges (self-loops are allowed but the
+ * fixtures remove them; duplicate edges are kept and count with multiplicity).  A partition owns
+ * the destination range [vertex_begin, vertex_end) (1D destination partition; on one GPU the
+ * whole range [0, N)).  All offsets are int32 and REBASED to the partition: offsets[0] == 0,
+ * offsets[rows] == number of stored edges, rows = vertex_end - vertex_begin.  All indices are
+ * GLOBAL vertex ids in [0, N).
+ *
+ *   csc_*: in-edges of the owned vertices ("CSC", the in-adjacency of PAPER.md:123).  Row r
+ *          lists the sources u of edges (u -> vertex_begin + r).  Required.
+ *   csr_*: out-edges of the owned vertices (the out-adjacency).  Row r lists the destinations v
+ *          of edges (vertex_begin + r -> v).  Required: out-degrees come from it (PageRank's
+ *          r/outdeg, messages counters), Hash-Min CC gathers over it (the reverse direction of
+ *          the symmetrised graph) and push mode expands over it.
+ *   *_weights: uint32 weight per stored edge, aligned with *_indices, used by SSSP only; NULL
+ *          means every weight is 1.  csc_weights and csr_weights must both be NULL or both set.
+ */
+typedef struct {
+    int64_t num_vertices;       /* N, 1 <= N <= 2^31 - 1                                        */
+    int64_t num_edges;          /* E, global                                                    */
+    int64_t vertex_begin;       /* owned destination range                                      */
+    int64_t vertex_end;
+    int64_t csc_edges;          /* edges stored in this partition's csc_* arrays                */
+    int64_t csr_edges;          /* edges stored in this partition's csr_* arrays                */
+    const int32_t* csc_offsets; /* [rows + 1]                                                   */
+    const int32_t* csc_indices; /* [csc_edges]                                                  */
+    const uint32_t* csc_weights;/* [csc_edges] or NULL                                          */
+    const int32_t* csr_offsets; /* [rows + 1]                                                   */
+    const int32_t* csr_indices; /* [csr_edges]                                                  */
+    const uint32_t* csr_weights;/* [csr_edges] or NULL                                          */
+    int32_t memory;             /* ipregel_memory                                               */
+    int32_t validate;           /* 1: O(E) device validation during create (INVALID_GRAPH)      */
+} ipregel_graph_desc;
+
+typedef struct {
+    int32_t mode;                  /* ipregel_mode, default AUTO                                */
+    uint32_t pagerank_iterations;  /* k: supersteps that broadcast (Fig. 8's 10); default 10    */
+    uint32_t sssp_source;          /* SSSP_SOURCE of Fig. 10; default 0                         */
+    float push_fraction;           /* AUTO: push when messages(s-1) < push_fraction * scanned
+                                      edges of a pull superstep; default 0.04                  */
+    uint32_t flags;                /* reserved, must be 0                                       */
+} ipregel_run_params;
+
+/* Per-superstep record of the last run (index = superstep, 0 = initialisation). */
+typedef struct {
+    uint32_t capacity;        /* in: length of every non-NULL array below                       */
+    uint32_t supersteps;      /* out: supersteps executed (including superstep 0)               */
+    int32_t status;           /* out: status of the last run                                    */
+    float* time_ms;           /* superstep wall time on the stream (kernels + exchange + counters) */
+    float* kernel_ms;         /* time of the superstep's main delivery kernel(s) only           */
+    uint8_t* mode;            /* 0 init, 1 pull, 2 push                                         */
+    uint64_t* changed;        /* vertices that broadcast in the superstep                       */
+    uint64_t* messages;       /* messages sent in the superstep (sum of broadcasters' degrees)  */
+    uint64_t* edges_scanned;  /* edges the superstep's delivery touched                         */
+    uint64_t* model_bytes;    /* algorithmic DRAM bytes of the superstep (DESIGN.md roofline)   */
+} ipregel_stats;
+
+/* ---- errors / device ---------------------------------------------------------------------- */
+const char* ipregel_status_string(ipregel_status status);
+const char* ipregel_last_error(void);     /* thread-local, never NULL                          */
+int ipregel_abi_version(void);
+/* Number of CUDA kernels this library has launched in the process so far (diagnostic). */
+uint64_t ipregel_kernel_launches(void);
+/* IPREGEL_OK if `device` is an sm_100 (B200-class) GPU, else UNSUPPORTED / CUDA. */
+ipregel_status ipregel_device_check(int device);
+
+/* ---- run parameters ----------------------------------------------------------------------- */
+/* Writes the defaults listed in ipregel_run_params into *out. */
+ipregel_status ipregel_run_params_default(ipregel_run_params* out);
+
+/* ---- multi-GPU (one process per GPU, 1D destination partition) --------------------------- */
+/* Rank 0 creates the 128-byte NCCL unique id; the caller ships it to every rank (e.g. a
+ * torch.distributed broadcast) -- PyTorch is plumbing, the library owns the communicator. */
+ipregel_status ipregel_nccl_unique_id(uint8_t out[128]);
+/* Collective over `world` ranks; `device` is this rank's CUDA ordinal. */
+ipregel_status ipregel_comm_create(int rank, int world, const uint8_t id[128], int device,
+                                   ipregel_comm** out);
+void ipregel_comm_destroy(ipregel_comm* comm);
+
+/* Host, deterministic.  cost_prefix[0..n] is a non-decreasing prefix sum of per-vertex cost
+ * (cost_prefix[0] == 0).  Writes bounds_out[0..world] with bounds_out[0] = 0,
+ * bounds_out[world] = n, non-decreasing, each range's cost as close as possible to
+ * cost_prefix[n] * g / world at its left end (binary search, lower bound). */
+ipregel_status ipregel_partition(const int64_t* cost_prefix, int64_t n, int world,
+                                 int64_t* bounds_out);
+
+/* ---- graph ---------------------------------------------------------------------------------- */
+/* Single GPU (comm == NULL, the desc must own [0, N)) or one rank of a multi-GPU run (collective:
+ * every rank calls it with its own partition; the ranges must tile [0, N) in rank order). */
+ipregel_status ipregel_graph_create(const ipregel_graph_desc* desc, ipregel_comm* comm,
+                                    void* stream, ipregel_graph** out);
+/* Loopback: `num_partitions` partitions of one graph, all on the current device, exchanging
+ * through device copies instead of NCCL (tests the partitioned path on one GPU).  descs[p] must
+ * tile [0, N) in order. */
+ipregel_status ipregel_graph_create_partitioned(const ipregel_graph_desc* descs,
+                                                int num_partitions, void* stream,
+                                                ipregel_graph** out);
+void ipregel_graph_destroy(ipregel_graph* graph);
+
+/* Device bytes held by the handle: graph-side (copies, tile plans) and vertex state (values,
+ * mailboxes/outboxes, frontier).  The vertex state is Theta(N), independent of E
+ * (PAPER.md:205-211, :476-480). */
+ipregel_status ipregel_memory_footprint(ipregel_graph* graph, uint64_t* graph_bytes,
+                                        uint64_t* state_bytes);
+
+/* ---- run ------------------------------------------------------------------------------------ */
+/* Runs supersteps 0, 1, ... of `app` until no vertex is active and no message is in flight
+ * (PageRank: superstep k is the last; CC/SSSP: until a superstep sends no message), or until
+ * `max_supersteps` supersteps (counting superstep 0) have executed while work remains
+ * (IPREGEL_ERR_MAX_SUPERSTEPS, state kept).  Host-synchronous.  params may be NULL (defaults).
+ * Collective across ranks of a comm. */
+ipregel_status ipregel_run(ipregel_graph* graph, ipregel_app app, ipregel_combiner combiner,
+                           uint32_t max_supersteps, const ipregel_run_params* params);
+
+/* Copies the full N-vertex result of the last run into `out` (host or device memory per
+ * out_is_device).  out_bytes must be N * 8 (PageRank) or N * 4 (CC, SSSP).  Multi-GPU: every
+ * rank receives all N values (collective). */
+ipregel_status ipregel_get_values(ipregel_graph* graph, void* out, size_t out_bytes,
+                                  int out_is_device);
+
+/* Fills the caller-owned arrays of *inout (up to capacity entries) for the last run. */
+ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IPREGEL_H */

@@ -1,0 +1,1299 @@
+// paper_2010_08781_b200/csrc/ipregel.cu -- the C ABI (include/ipregel.h) and the host superstep
+// driver.  One translation unit; kernels live in pull.cuh / push.cuh / setup.cuh.
+//
+// BSP loop (Sec. 4.2, Fig. 3): superstep 0 initialises every vertex and its
+// first broadcast; superstep s >= 1 delivers the messages of s-1 (pull: CSC gather-combine;
+// push: frontier expansion with atomic combine), runs the recipients' compute fused into the
+// same kernels, counts broadcasters and messages on the device, exchanges owned values between
+// partitions, and the host reads the counters to decide termination ("every active vertex has
+// been processed and every outgoing message delivered").
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ipregel.h"
+#include "common.cuh"
+#include "pull.cuh"
+#include "push.cuh"
+#include "setup.cuh"
+
+using namespace ipr;
+
+// =============================================================================================
+// errors
+// =============================================================================================
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure {
+    ipregel_status status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(ipregel_status s, const char* fmt, ...) {
+    char buf[640];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw Failure{s, buf};
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            ipregel_status st_ = e_ == cudaErrorMemoryAllocation ? IPREGEL_ERR_OUT_OF_MEMORY  \
+                                                                 : IPREGEL_ERR_CUDA;          \
+            fail(st_, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);   \
+        }                                                                                     \
+    } while (0)
+
+#define NC(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            fail(IPREGEL_ERR_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, \
+                 __LINE__);                                                                   \
+    } while (0)
+
+std::atomic<unsigned long long> g_launches{0};
+#define LAUNCH_CHECK()                                   \
+    do {                                                 \
+        g_launches.fetch_add(1, std::memory_order_relaxed); \
+        CU(cudaGetLastError());                          \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline unsigned grid_for(int64_t n, int threads) {
+    int64_t g = ceil_div(std::max<int64_t>(n, 1), threads);
+    return (unsigned)std::min<int64_t>(g, 0x7FFFFFFF);
+}
+
+}  // namespace
+
+// =============================================================================================
+// handles
+// =============================================================================================
+struct ipregel_comm {
+    ncclComm_t nccl = nullptr;
+    int rank = 0, world = 1, device = 0;
+};
+
+namespace {
+
+struct DeviceBuffers {
+    std::vector<void*> ptrs;
+    uint64_t bytes = 0;
+    template <class T>
+    T* alloc(int64_t count, cudaStream_t s, bool zero = false) {
+        void* p = nullptr;
+        size_t b = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
+        CU(cudaMalloc(&p, b));
+        ptrs.push_back(p);
+        bytes += b;
+        if (zero) CU(cudaMemsetAsync(p, 0, b, s));
+        return static_cast<T*>(p);
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+        bytes = 0;
+    }
+};
+
+// Vertex state of one app on one partition: Theta(N), never a function of E
+// (single-slot mailboxes).
+struct AppState {
+    bool ready = false;
+    double* rank = nullptr;                    // PageRank: owned ranks
+    double* contrib[2] = {nullptr, nullptr};   // PageRank outbox replicas [N] (s / s+1)
+    double* acc = nullptr;                     // PageRank push accumulator (owned)
+    uint32_t* val[2] = {nullptr, nullptr};     // CC/SSSP value replicas [N] (current / next)
+    uint32_t* bits = nullptr;                  // owned bitmap of broadcasters
+    int32_t* f_id = nullptr;                   // owned frontier (ascending ids) + snapshots
+    uint32_t* f_val = nullptr;
+    int32_t* g_id = nullptr;                   // global frontier (== f_* on one partition)
+    uint32_t* g_val = nullptr;
+    unsigned long long* g_len = nullptr;       // device scalar
+    int32_t* e_id = nullptr;                   // expand list: push-view degree > 0
+    uint32_t* e_val = nullptr;
+    long long* e_pre = nullptr;
+    unsigned long long* blk_a = nullptr;       // scan scratch
+    unsigned long long* blk_b = nullptr;
+    int32_t* iota = nullptr;                   // PageRank push: every vertex as a source
+    unsigned long long* iota_len = nullptr;
+    DeviceBuffers mem;
+};
+
+struct Partition {
+    int64_t vb = 0, ve = 0, rows = 0;
+    int64_t csc_edges = 0, csr_edges = 0;
+    int64_t csc_ebase = 0, csr_ebase = 0;   // global edge offset of this partition's first row
+    const int32_t* csc_off = nullptr;
+    const int32_t* csc_idx = nullptr;
+    const uint32_t* csc_w = nullptr;
+    const int32_t* csr_off = nullptr;
+    const int32_t* csr_idx = nullptr;
+    const uint32_t* csr_w = nullptr;
+    TilePlan plan_csc, plan_csr;
+    PushAdj push_sssp, push_cc;   // out-edges of every source that land in the owned range
+    bool push_view_ready = false;
+    int64_t nondangling = 0;
+    DeviceBuffers graph_mem;      // host copies, tile plans, push view
+    AppState st[3];
+    PullCounters* pull_cnt = nullptr;         // device
+    FrontierCounters* front_cnt = nullptr;    // device
+    unsigned long long* host_cnt = nullptr;   // pinned [16]
+    unsigned long long* dscratch = nullptr;   // device [64] (NCCL counter buffers)
+};
+
+struct StepRecord {
+    float time_ms = 0, kernel_ms = 0;
+    uint8_t mode = 0;
+    uint64_t changed = 0, messages = 0, edges_scanned = 0, model_bytes = 0;
+};
+
+}  // namespace
+
+struct ipregel_graph {
+    int64_t n = 0, e = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    ipregel_comm* comm = nullptr;
+    std::vector<Partition> parts;
+    std::vector<int64_t> rank_vb, rank_rows;  // multi-GPU: every rank's owned range
+    bool poisoned = false;
+    int last_app = -1;
+    int last_status = -1;
+    int cur = 0;
+    std::vector<StepRecord> steps;
+    std::vector<cudaEvent_t> events;
+    double* gather_tmp = nullptr;  // multi-GPU get_values scratch
+};
+
+// =============================================================================================
+// internals
+// =============================================================================================
+namespace {
+
+bool multi_rank(const ipregel_graph* g) { return g->comm && g->comm->world > 1; }
+
+void check_device(int device) {
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        fail(IPREGEL_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+             device, prop.major, prop.minor);
+}
+
+void build_plan(TilePlan& P, const int32_t* off, int64_t rows, int64_t edges, int64_t diag0,
+                DeviceBuffers& mem, cudaStream_t s) {
+    P.rows = (int32_t)rows;
+    P.edges = edges;
+    P.phase = diag0 % kPullItems;
+    const int64_t total = rows + edges;
+    P.num_tiles = rows > 0 ? (int32_t)ceil_div(total + P.phase, kPullItems) : 0;
+    if (P.num_tiles == 0) return;
+    P.cx = mem.alloc<int32_t>(P.num_tiles + 1, s);
+    P.cy = mem.alloc<int32_t>(P.num_tiles + 1, s);
+    P.carry = mem.alloc<double>(P.num_tiles, s);   // 8-byte slots hold f64 or u32
+    P.head = mem.alloc<double>(P.num_tiles, s);
+    k_plan_boundaries<<<grid_for(P.num_tiles + 1, 256), 256, 0, s>>>(off, P.rows, edges, P.phase,
+                                                                      P.num_tiles, P.cx, P.cy);
+    LAUNCH_CHECK();
+    // Spanning rows: boundary b in [1, T-1] carries row cx[b]; consecutive boundaries with the
+    // same row form one group (row, a, b).  Host pass at create time (not timed).
+    std::vector<int32_t> cx(P.num_tiles + 1);
+    CU(cudaMemcpyAsync(cx.data(), P.cx, cx.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    std::vector<int4> groups;
+    for (int32_t b = 1; b < P.num_tiles; ++b) {
+        if (cx[b] >= rows) continue;
+        if (!groups.empty() && groups.back().x == cx[b] && groups.back().z == b - 1)
+            groups.back().z = b;
+        else
+            groups.push_back(make_int4(cx[b], b, b, 0));
+    }
+    P.num_groups = (int32_t)groups.size();
+    if (P.num_groups) {
+        P.groups = mem.alloc<int4>(P.num_groups, s);
+        CU(cudaMemcpyAsync(P.groups, groups.data(), groups.size() * sizeof(int4),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));
+    }
+}
+
+template <class Op>
+void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
+                 PullCounters* cnt, cudaStream_t s) {
+    using T = typename Op::T;
+    if (P.num_tiles == 0) return;
+    k_pull_tiles<Op><<<P.num_tiles, kPullThreads, 0, s>>>(op, off, idx, P.cx, P.cy, P.rows,
+                                                          P.phase, static_cast<T*>(P.carry),
+                                                          static_cast<T*>(P.head), cnt);
+    LAUNCH_CHECK();
+    if (P.num_groups) {
+        k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
+            op, P.groups, P.num_groups, static_cast<const T*>(P.carry),
+            static_cast<const T*>(P.head), cnt);
+        LAUNCH_CHECK();
+    }
+}
+
+template <class T>
+ncclDataType_t nccl_type();
+template <>
+ncclDataType_t nccl_type<double>() { return ncclFloat64; }
+template <>
+ncclDataType_t nccl_type<uint32_t>() { return ncclUint32; }
+
+// Replicate every partition's owned slice of a replica array into every other replica
+// (multi-GPU: in-place AllGatherv as grouped ncclBroadcast, one root per rank range).
+template <class T, class Get>
+void exchange_owned(ipregel_graph* g, Get get) {
+    if (multi_rank(g)) {
+        T* rep = get(g->parts[0]);
+        NC(ncclGroupStart());
+        for (int r = 0; r < g->comm->world; ++r) {
+            if (g->rank_rows[r] == 0) continue;
+            NC(ncclBroadcast(rep + g->rank_vb[r], rep + g->rank_vb[r], (size_t)g->rank_rows[r],
+                             nccl_type<T>(), r, g->comm->nccl, g->stream));
+        }
+        NC(ncclGroupEnd());
+        return;
+    }
+    const int np = (int)g->parts.size();
+    for (int a = 0; a < np; ++a) {
+        Partition& pa = g->parts[a];
+        if (pa.rows == 0) continue;
+        for (int b = 0; b < np; ++b) {
+            if (a == b) continue;
+            CU(cudaMemcpyAsync(get(g->parts[b]) + pa.vb, get(pa) + pa.vb,
+                               (size_t)pa.rows * sizeof(T), cudaMemcpyDeviceToDevice, g->stream));
+        }
+    }
+}
+
+// Sum u64 device counters over partitions / ranks into out[0..count).
+void reduce_counters(ipregel_graph* g, bool frontier, unsigned long long* out, int count) {
+    for (int i = 0; i < count; ++i) out[i] = 0;
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        void* src = frontier ? (void*)p.front_cnt : (void*)p.pull_cnt;
+        NC(ncclAllReduce(src, p.dscratch, (size_t)count, ncclUint64, ncclSum, g->comm->nccl,
+                         g->stream));
+        CU(cudaMemcpyAsync(p.host_cnt, p.dscratch, count * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, g->stream));
+        CU(cudaStreamSynchronize(g->stream));
+        for (int i = 0; i < count; ++i) out[i] = p.host_cnt[i];
+        return;
+    }
+    for (auto& p : g->parts) {
+        void* src = frontier ? (void*)p.front_cnt : (void*)p.pull_cnt;
+        CU(cudaMemcpyAsync(p.host_cnt, src, count * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, g->stream));
+    }
+    CU(cudaStreamSynchronize(g->stream));
+    for (auto& p : g->parts)
+        for (int i = 0; i < count; ++i) out[i] += p.host_cnt[i];
+}
+
+int64_t words_of(int64_t rows) { return (rows + 31) >> 5; }
+
+void ensure_state(ipregel_graph* g, int app) {
+    for (auto& p : g->parts) {
+        AppState& S = p.st[app];
+        if (S.ready) continue;
+        cudaStream_t s = g->stream;
+        const int64_t n = g->n;
+        if (app == IPREGEL_APP_PAGERANK) {
+            S.rank = S.mem.alloc<double>(p.rows, s);
+            S.contrib[0] = S.mem.alloc<double>(n, s, true);
+            S.contrib[1] = S.mem.alloc<double>(n, s, true);
+        } else {
+            S.val[0] = S.mem.alloc<uint32_t>(n, s);
+            S.val[1] = S.mem.alloc<uint32_t>(n, s);
+            S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
+            S.f_id = S.mem.alloc<int32_t>(p.rows, s);
+            S.f_val = S.mem.alloc<uint32_t>(p.rows, s);
+            if (g->parts.size() > 1 || multi_rank(g)) {
+                S.g_id = S.mem.alloc<int32_t>(n, s);
+                S.g_val = S.mem.alloc<uint32_t>(n, s);
+                S.g_len = S.mem.alloc<unsigned long long>(1, s, true);
+            } else {
+                S.g_id = S.f_id;
+                S.g_val = S.f_val;
+                S.g_len = &p.front_cnt->changed;
+            }
+        }
+        // expand list + scan scratch (PageRank needs them for push mode only; allocated lazily)
+        const int64_t blk = std::max<int64_t>(ceil_div(words_of(p.rows), kWordsPerBlock),
+                                              ceil_div(n, kListPerBlock)) + 1;
+        S.blk_a = S.mem.alloc<unsigned long long>(blk, s);
+        S.blk_b = S.mem.alloc<unsigned long long>(blk, s);
+        S.ready = true;
+    }
+}
+
+void ensure_expand_list(Partition& p, AppState& S, int64_t n, cudaStream_t s) {
+    if (S.e_id) return;
+    S.e_id = S.mem.alloc<int32_t>(n, s);
+    S.e_val = S.mem.alloc<uint32_t>(n, s);
+    S.e_pre = S.mem.alloc<long long>(n, s);
+    (void)p;
+}
+
+// Device-wide exclusive scan of int32 counts in place (create-time helper).
+void exscan_i32(int32_t* a, int64_t n, DeviceBuffers& tmp, cudaStream_t s) {
+    const int64_t nb = ceil_div(n, kScanChunk);
+    unsigned long long* sums = tmp.alloc<unsigned long long>(nb, s);
+    k_chunk_sums<<<grid_for(nb, 1), 256, 0, s>>>(a, n, sums);
+    LAUNCH_CHECK();
+    k_scan_blocks<<<1, 1024, 0, s>>>(sums, nullptr, nb, nullptr, nullptr);
+    LAUNCH_CHECK();
+    k_chunk_apply<<<grid_for(nb, 1), 256, 0, s>>>(a, n, sums);
+    LAUNCH_CHECK();
+}
+
+// Push adjacency of one partition.  One partition: the graph's own CSR (+ CSC for CC).  Several:
+// transposes of the owned CSC (and, for CC, owned CSR) rows, over all N sources.
+void ensure_push_view(ipregel_graph* g, Partition& p) {
+    if (p.push_view_ready) return;
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    if (g->parts.size() == 1 && !multi_rank(g)) {
+        p.push_sssp = PushAdj{p.csr_off, p.csr_idx, p.csr_w, nullptr, nullptr, 0, n};
+        p.push_cc = PushAdj{p.csr_off, p.csr_idx, nullptr, p.csc_off, p.csc_idx, 0, n};
+        p.push_view_ready = true;
+        return;
+    }
+    auto transpose = [&](const int32_t* off, const int32_t* idx, const uint32_t* w, int64_t edges,
+                         bool want_w, int32_t** out_off, int32_t** out_idx, uint32_t** out_w) {
+        int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+        int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
+        uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
+        if (edges > 0) {
+            k_hist_sources<<<grid_for(edges, 256) > 4096 ? 4096 : grid_for(edges, 256), 256, 0, s>>>(
+                idx, edges, o);
+            LAUNCH_CHECK();
+        }
+        DeviceBuffers tmp;
+        exscan_i32(o, n + 1, tmp, s);
+        int32_t* cursor = tmp.alloc<int32_t>(n + 1, s);
+        CU(cudaMemcpyAsync(cursor, o, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        if (p.rows > 0) {
+            k_transpose_rows<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, idx, w, p.rows, p.vb,
+                                                                       cursor, ix, wx);
+            LAUNCH_CHECK();
+        }
+        CU(cudaStreamSynchronize(s));
+        tmp.release();
+        *out_off = o;
+        *out_idx = ix;
+        if (out_w) *out_w = wx;
+    };
+    int32_t *o1, *i1, *o2, *i2;
+    uint32_t* w1 = nullptr;
+    transpose(p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, &o1, &i1, &w1);
+    transpose(p.csr_off, p.csr_idx, nullptr, p.csr_edges, false, &o2, &i2, nullptr);
+    p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, 0, n};
+    p.push_cc = PushAdj{o1, i1, nullptr, o2, i2, 0, n};
+    p.push_view_ready = true;
+}
+
+// ---- frontier machinery ------------------------------------------------------------------
+// Compact the owned bitmap into (ids, snapshots) and count broadcasters / messages.
+void compact_bitmap(ipregel_graph* g, Partition& p, AppState& S, const uint32_t* vals, bool cc) {
+    cudaStream_t s = g->stream;
+    const int64_t nw = words_of(p.rows);
+    const int64_t nb = std::max<int64_t>(ceil_div(nw, kWordsPerBlock), 1);
+    OwnedDegree deg{p.csr_off, cc ? p.csc_off : nullptr};
+    k_bitmap_count<<<(unsigned)nb, kScanThreads, 0, s>>>(S.bits, nw, deg, S.blk_a, S.blk_b);
+    LAUNCH_CHECK();
+    k_scan_blocks<<<1, 1024, 0, s>>>(S.blk_a, S.blk_b, nb, &p.front_cnt->changed,
+                                     &p.front_cnt->messages);
+    LAUNCH_CHECK();
+    k_bitmap_write<<<(unsigned)nb, kScanThreads, 0, s>>>(S.bits, nw, p.vb, vals, S.blk_a, S.f_id,
+                                                        S.f_val);
+    LAUNCH_CHECK();
+}
+
+// Multi-partition: concatenate every partition's owned frontier (rank order = ascending ids)
+// into every partition's global frontier and scatter the snapshots into its replica.
+void exchange_frontier(ipregel_graph* g, int app, const std::vector<unsigned long long>& counts,
+                       int cur) {
+    auto replica = [app](Partition& p, int w) { return p.st[app].val[w]; };
+    cudaStream_t s = g->stream;
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        AppState& S = p.st[app];
+        unsigned long long total = 0;
+        std::vector<unsigned long long> off(counts.size());
+        for (size_t r = 0; r < counts.size(); ++r) { off[r] = total; total += counts[r]; }
+        NC(ncclGroupStart());
+        for (int r = 0; r < g->comm->world; ++r) {
+            if (counts[r] == 0) continue;
+            const void* sid = r == g->comm->rank ? (const void*)S.f_id : nullptr;
+            const void* sval = r == g->comm->rank ? (const void*)S.f_val : nullptr;
+            NC(ncclBroadcast(sid, S.g_id + off[r], counts[r], ncclInt32, r, g->comm->nccl, s));
+            NC(ncclBroadcast(sval, S.g_val + off[r], counts[r], ncclUint32, r, g->comm->nccl, s));
+        }
+        NC(ncclGroupEnd());
+        CU(cudaMemcpyAsync(S.g_len, &total, sizeof(total), cudaMemcpyHostToDevice, s));
+        k_scatter_frontier<<<grid_for(std::max<unsigned long long>(total, 1ull), 256) > 2048
+                                 ? 2048 : grid_for(std::max<unsigned long long>(total, 1ull), 256),
+                             256, 0, s>>>(S.g_id, S.g_val, S.g_len, replica(p, cur));
+        LAUNCH_CHECK();
+        CU(cudaStreamSynchronize(s));  // `total` lives on the host stack
+        return;
+    }
+    const int np = (int)g->parts.size();
+    if (np <= 1) return;
+    unsigned long long total = 0;
+    std::vector<unsigned long long> off(np);
+    for (int a = 0; a < np; ++a) { off[a] = total; total += counts[a]; }
+    for (int b = 0; b < np; ++b) {
+        AppState& Sb = g->parts[b].st[app];
+        for (int a = 0; a < np; ++a) {
+            if (counts[a] == 0) continue;
+            AppState& Sa = g->parts[a].st[app];
+            CU(cudaMemcpyAsync(Sb.g_id + off[a], Sa.f_id, counts[a] * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, s));
+            CU(cudaMemcpyAsync(Sb.g_val + off[a], Sa.f_val, counts[a] * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, s));
+        }
+        CU(cudaMemcpyAsync(Sb.g_len, &total, sizeof(total), cudaMemcpyHostToDevice, s));
+        unsigned gr = grid_for(std::max<unsigned long long>(total, 1ull), 256);
+        k_scatter_frontier<<<gr > 2048 ? 2048 : gr, 256, 0, s>>>(Sb.g_id, Sb.g_val, Sb.g_len,
+                                                                replica(g->parts[b], cur));
+        LAUNCH_CHECK();
+    }
+    CU(cudaStreamSynchronize(s));  // `total` lives on the host stack
+}
+
+// Build the expand list (entries of the global frontier with push-view degree > 0, with the
+// exclusive degree prefix) for one partition.
+void build_expand_list(ipregel_graph* g, Partition& p, AppState& S, const PushAdj& adj,
+                       const int32_t* ids, const uint32_t* vals, const unsigned long long* len,
+                       int64_t len_host) {
+    cudaStream_t s = g->stream;
+    ensure_expand_list(p, S, g->n, s);
+    const int64_t nb = std::max<int64_t>(ceil_div(len_host, kListPerBlock), 1);
+    k_list_count<<<(unsigned)nb, kScanThreads, 0, s>>>(ids, len, adj, S.blk_a, S.blk_b);
+    LAUNCH_CHECK();
+    k_scan_blocks<<<1, 1024, 0, s>>>(S.blk_a, S.blk_b, nb, &p.front_cnt->list_len,
+                                     &p.front_cnt->list_edges);
+    LAUNCH_CHECK();
+    k_list_write<<<(unsigned)nb, kScanThreads, 0, s>>>(ids, vals, len, adj, S.blk_a, S.blk_b,
+                                                      S.e_id, S.e_val, S.e_pre);
+    LAUNCH_CHECK();
+}
+
+// Per-partition owned-frontier sizes, in partition / rank order.
+std::vector<unsigned long long> frontier_counts(ipregel_graph* g) {
+    cudaStream_t s = g->stream;
+    std::vector<unsigned long long> counts;
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        NC(ncclAllGather(&p.front_cnt->changed, p.dscratch, 1, ncclUint64, g->comm->nccl, s));
+        counts.assign(g->comm->world, 0);
+        CU(cudaMemcpyAsync(counts.data(), p.dscratch, g->comm->world * 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        return counts;
+    }
+    for (auto& p : g->parts)
+        CU(cudaMemcpyAsync(p.host_cnt + 2, &p.front_cnt->changed, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (auto& p : g->parts) counts.push_back(p.host_cnt[2]);
+    return counts;
+}
+
+// ---- timing -------------------------------------------------------------------------------
+cudaEvent_t ev(ipregel_graph* g, size_t i) {
+    while (g->events.size() <= i) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        g->events.push_back(e);
+    }
+    return g->events[i];
+}
+
+struct StepTimer {
+    ipregel_graph* g;
+    size_t step;
+    void begin() { CU(cudaEventRecord(ev(g, 4 * step + 0), g->stream)); }
+    void kbegin() { CU(cudaEventRecord(ev(g, 4 * step + 1), g->stream)); }
+    void kend() { CU(cudaEventRecord(ev(g, 4 * step + 2), g->stream)); }
+    void end() { CU(cudaEventRecord(ev(g, 4 * step + 3), g->stream)); }
+};
+
+void finalize_times(ipregel_graph* g) {
+    CU(cudaStreamSynchronize(g->stream));
+    for (size_t s = 0; s < g->steps.size(); ++s) {
+        float a = 0, b = 0;
+        CU(cudaEventElapsedTime(&a, ev(g, 4 * s + 0), ev(g, 4 * s + 3)));
+        CU(cudaEventElapsedTime(&b, ev(g, 4 * s + 1), ev(g, 4 * s + 2)));
+        g->steps[s].time_ms = a;
+        g->steps[s].kernel_ms = b;
+    }
+}
+
+// =============================================================================================
+// PageRank (Fig. 8)
+// =============================================================================================
+ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_run_params& P) {
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    const uint32_t k = P.pagerank_iterations;
+    const double ratio = 0.15 / (double)n;   // Pregel's 0.15 / NumVertices()
+    const double inv_n = 1.0 / (double)n;    // initial_value
+    const uint32_t last = std::min<uint32_t>(k, max_steps - 1);
+    const bool push = P.mode == IPREGEL_MODE_PUSH;
+    // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
+    int64_t nondangling = 0;
+    for (auto& p : g->parts) nondangling += p.nondangling;
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        p.host_cnt[0] = (unsigned long long)p.nondangling;
+        CU(cudaMemcpyAsync(p.dscratch, p.host_cnt, 8, cudaMemcpyHostToDevice, s));
+        NC(ncclAllReduce(p.dscratch, p.dscratch + 1, 1, ncclUint64, ncclSum, g->comm->nccl, s));
+        CU(cudaMemcpyAsync(p.host_cnt + 1, p.dscratch + 1, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        nondangling = (int64_t)p.host_cnt[1];
+    }
+
+    // superstep 0
+    g->steps.assign(1, StepRecord{});
+    StepTimer T0{g, 0};
+    T0.begin();
+    T0.kbegin();
+    for (auto& p : g->parts) {
+        AppState& S = p.st[IPREGEL_APP_PAGERANK];
+        if (p.rows == 0) continue;
+        k_init_pagerank<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, p.vb, inv_n,
+                                                              k > 0, last == 0, S.rank,
+                                                              S.contrib[0]);
+        LAUNCH_CHECK();
+    }
+    T0.kend();
+    if (k > 0) exchange_owned<double>(g, [](Partition& p) { return p.st[0].contrib[0]; });
+    T0.end();
+    g->steps[0].mode = 0;
+    g->steps[0].changed = k > 0 ? (uint64_t)nondangling : 0;
+    g->steps[0].messages = k > 0 ? (uint64_t)g->e : 0;
+    g->steps[0].model_bytes = 12ull * (uint64_t)n;
+    int cur = 0;
+
+    // push mode: static expand list of every source with push-view degree > 0
+    if (push && k > 0) {
+        for (auto& p : g->parts) {
+            ensure_push_view(g, p);
+            AppState& S = p.st[IPREGEL_APP_PAGERANK];
+            if (!S.acc) S.acc = S.mem.alloc<double>(p.rows, s, true);
+            if (!S.iota) {
+                S.iota = S.mem.alloc<int32_t>(n, s);
+                S.iota_len = S.mem.alloc<unsigned long long>(1, s);
+                unsigned long long nn = (unsigned long long)n;
+                CU(cudaMemcpyAsync(S.iota_len, &nn, sizeof(nn), cudaMemcpyHostToDevice, s));
+                k_iota<<<grid_for(n, 256), 256, 0, s>>>(S.iota, n);
+                LAUNCH_CHECK();
+                CU(cudaStreamSynchronize(s));
+            }
+            build_expand_list(g, p, S, p.push_sssp, S.iota, nullptr, S.iota_len, n);
+        }
+    }
+
+    ipregel_status status = IPREGEL_OK;
+    for (uint32_t step = 1; step <= k; ++step) {
+        if (step == max_steps) { status = IPREGEL_ERR_MAX_SUPERSTEPS; break; }
+        const int broadcast = step < k;
+        const int write_rank = step == last;
+        g->steps.push_back(StepRecord{});
+        StepTimer T{g, step};
+        T.begin();
+        T.kbegin();
+        for (auto& p : g->parts) {
+            AppState& S = p.st[IPREGEL_APP_PAGERANK];
+            if (p.rows == 0) continue;
+            if (!push) {
+                PageRankPull op;
+                op.contrib_cur = S.contrib[cur];
+                op.contrib_next = S.contrib[1 - cur];
+                op.rank = S.rank;
+                op.out_off = p.csr_off;
+                op.vbase = p.vb;
+                op.ratio = ratio;
+                op.broadcast = broadcast;
+                op.write_rank = write_rank;
+                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, s);
+            } else {
+                k_expand<0><<<1184, kExpandThreads, 0, s>>>(
+                    p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
+                    &p.front_cnt->list_edges, p.vb, nullptr, nullptr, S.contrib[cur], S.acc);
+                LAUNCH_CHECK();
+                k_pr_push_apply<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                    S.acc, p.csr_off, p.rows, p.vb, ratio, broadcast, write_rank, S.rank,
+                    S.contrib[1 - cur]);
+                LAUNCH_CHECK();
+            }
+        }
+        T.kend();
+        if (broadcast) {
+            const int nx = 1 - cur;
+            exchange_owned<double>(g, [nx](Partition& p) { return p.st[0].contrib[nx]; });
+        }
+        T.end();
+        StepRecord& R = g->steps.back();
+        R.mode = push ? 2 : 1;
+        R.changed = broadcast ? (uint64_t)nondangling : 0;
+        R.messages = broadcast ? (uint64_t)g->e : 0;
+        R.edges_scanned = (uint64_t)g->e;
+        R.model_bytes = push ? 12ull * g->e + 24ull * n : 12ull * g->e + 16ull * n;
+        cur = 1 - cur;
+    }
+    g->cur = cur;
+    finalize_times(g);
+    return status;
+}
+
+// =============================================================================================
+// Hash-Min CC (Fig. 9) and SSSP (Fig. 10)
+// =============================================================================================
+ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipregel_run_params& P) {
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    const bool cc = app == IPREGEL_APP_HASHMIN_CC;
+    const int np = (int)g->parts.size();
+    const bool multi = np > 1 || multi_rank(g);
+    // edges a pull superstep scans (CC gathers over CSC and CSR rows: the symmetrised graph)
+    const uint64_t pull_edges = cc ? 2ull * (uint64_t)g->e : (uint64_t)g->e;
+
+    for (auto& p : g->parts) ensure_push_view(g, p);
+
+    // ---------------- superstep 0
+    g->steps.assign(1, StepRecord{});
+    StepTimer T0{g, 0};
+    T0.begin();
+    T0.kbegin();
+    for (auto& p : g->parts) {
+        AppState& S = p.st[app];
+        if (cc) k_init_cc<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n);
+        else k_init_sssp<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, (int64_t)P.sssp_source);
+        LAUNCH_CHECK();
+    }
+    T0.kend();
+    uint64_t changed = 0, messages = 0;
+    bool lists_ready = false;
+    if (cc) {
+        changed = (uint64_t)n;
+        messages = 2ull * (uint64_t)g->e;
+    } else {
+        // the source's broadcast: its frontier entry and out-degree come from the compaction
+        for (auto& p : g->parts) {
+            AppState& S = p.st[app];
+            if ((int64_t)P.sssp_source >= p.vb && (int64_t)P.sssp_source < p.ve) {
+                k_set_bit<<<1, 1, 0, s>>>(S.bits, (int64_t)P.sssp_source - p.vb);
+                LAUNCH_CHECK();
+            }
+            compact_bitmap(g, p, S, S.val[0], false);
+        }
+        if (multi) exchange_frontier(g, app, frontier_counts(g), 0);
+        unsigned long long c[2];
+        reduce_counters(g, true, c, 2);
+        changed = c[0];
+        messages = c[1];
+        lists_ready = true;
+    }
+    T0.end();
+    g->steps[0].mode = 0;
+    g->steps[0].changed = changed;
+    g->steps[0].messages = messages;
+    g->steps[0].model_bytes = 4ull * (uint64_t)n;
+    int cur = 0;
+    int prev_mode = 0;
+    ipregel_status status = IPREGEL_OK;
+
+    for (uint32_t step = 1; messages > 0; ++step) {
+        if (step == max_steps) { status = IPREGEL_ERR_MAX_SUPERSTEPS; break; }
+        // delivery mode for this superstep (Ligra-style switch)
+        int mode;
+        if (P.mode == IPREGEL_MODE_PULL) mode = 1;
+        else if (P.mode == IPREGEL_MODE_PUSH) mode = 2;
+        else mode = (double)messages < (double)P.push_fraction * (double)pull_edges ? 2 : 1;
+
+        g->steps.push_back(StepRecord{});
+        StepTimer T{g, step};
+        T.begin();
+        uint64_t frontier_len = changed;
+
+        if (mode == 2) {
+            // ---- push: make the frontier list of the previous superstep's broadcasters
+            if (!lists_ready) {
+                for (auto& p : g->parts) {
+                    AppState& S = p.st[app];
+                    if (prev_mode == 0) {
+                        k_fill_bits<<<grid_for(words_of(p.rows), 256), 256, 0, s>>>(S.bits, p.rows);
+                    } else {
+                        // pull -> push: broadcasters = vertices whose value decreased
+                        k_bitmap_from_diff<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                            S.val[1 - cur], S.val[cur], p.vb, p.rows, S.bits);
+                    }
+                    LAUNCH_CHECK();
+                    compact_bitmap(g, p, S, S.val[cur], cc);
+                }
+                if (multi) exchange_frontier(g, app, frontier_counts(g), cur);
+            }
+            T.kbegin();
+            for (auto& p : g->parts) {
+                AppState& S = p.st[app];
+                const PushAdj& adj = cc ? p.push_cc : p.push_sssp;
+                build_expand_list(g, p, S, adj, S.g_id, S.g_val, S.g_len, (int64_t)frontier_len);
+                const unsigned grid = (unsigned)std::min<int64_t>(
+                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), 148 * 8);
+                if (cc)
+                    k_expand<1><<<grid, kExpandThreads, 0, s>>>(
+                        adj, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
+                        &p.front_cnt->list_edges, p.vb, S.val[cur], S.bits, nullptr, nullptr);
+                else
+                    k_expand<2><<<grid, kExpandThreads, 0, s>>>(
+                        adj, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
+                        &p.front_cnt->list_edges, p.vb, S.val[cur], S.bits, nullptr, nullptr);
+                LAUNCH_CHECK();
+            }
+            T.kend();
+            // broadcasters of this superstep -> next frontier (+ counters)
+            for (auto& p : g->parts) compact_bitmap(g, p, p.st[app], p.st[app].val[cur], cc);
+            if (multi) exchange_frontier(g, app, frontier_counts(g), cur);
+            unsigned long long c[2];
+            reduce_counters(g, true, c, 2);
+            T.end();
+            StepRecord& R = g->steps.back();
+            R.mode = 2;
+            R.edges_scanned = messages;
+            R.model_bytes = (cc ? 8ull : 12ull) * messages + 16ull * frontier_len +
+                            (uint64_t)n / 8;
+            changed = c[0];
+            messages = c[1];
+            lists_ready = true;
+        } else {
+            // ---- pull: gather over CSC (and CSR for CC), value[next] = min(value, gathered)
+            for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
+            T.kbegin();
+            for (auto& p : g->parts) {
+                AppState& S = p.st[app];
+                if (p.rows == 0) continue;
+                if (cc) {
+                    CCPullIn a;
+                    a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, s);
+                    CCPullOut b;
+                    b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
+                    b.out_off = p.csr_off; b.vbase = p.vb;
+                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, p.pull_cnt, s);
+                } else {
+                    SSSPPull a;
+                    a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.in_w = p.csc_w;
+                    a.out_off = p.csr_off; a.vbase = p.vb;
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.pull_cnt, s);
+                }
+            }
+            T.kend();
+            const int nx = 1 - cur;
+            exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
+            unsigned long long c[2];
+            reduce_counters(g, false, c, 2);
+            T.end();
+            StepRecord& R = g->steps.back();
+            R.mode = 1;
+            R.edges_scanned = pull_edges;
+            R.model_bytes = cc ? 8ull * pull_edges + 16ull * n : 12ull * pull_edges + 12ull * n;
+            changed = c[0];
+            messages = c[1];
+            cur = 1 - cur;
+            lists_ready = false;
+        }
+        prev_mode = mode;
+        StepRecord& R = g->steps.back();
+        R.changed = changed;
+        R.messages = messages;
+    }
+    g->cur = cur;
+    finalize_times(g);
+    return status;
+}
+
+void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
+    if (!d) fail(IPREGEL_ERR_INVALID_ARGUMENT, "desc is NULL");
+    if (d->num_vertices < 1 || d->num_vertices > 2147483647LL)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "num_vertices %lld outside [1, 2^31-1]",
+             (long long)d->num_vertices);
+    if (d->num_edges < 0 || d->num_edges > 2147483647LL)
+        fail(IPREGEL_ERR_UNSUPPORTED, "num_edges %lld beyond int32 indexing",
+             (long long)d->num_edges);
+    if (d->vertex_begin < 0 || d->vertex_end < d->vertex_begin || d->vertex_end > d->num_vertices)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "owned range [%lld, %lld) invalid",
+             (long long)d->vertex_begin, (long long)d->vertex_end);
+    if (d->csc_edges < 0 || d->csr_edges < 0 || d->csc_edges > d->num_edges ||
+        d->csr_edges > d->num_edges)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "csc_edges/csr_edges out of range");
+    if (!d->csc_offsets || !d->csr_offsets || (d->csc_edges > 0 && !d->csc_indices) ||
+        (d->csr_edges > 0 && !d->csr_indices))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "required CSC/CSR array is NULL");
+    if ((d->csc_weights == nullptr) != (d->csr_weights == nullptr))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "csc_weights and csr_weights must both be set or NULL");
+    if (d->memory != IPREGEL_MEMORY_DEVICE && d->memory != IPREGEL_MEMORY_HOST)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown memory kind %d", d->memory);
+    if ((d->vertex_end - d->vertex_begin) + std::max(d->csc_edges, d->csr_edges) > 2147483647LL)
+        fail(IPREGEL_ERR_UNSUPPORTED, "rows + edges of a partition beyond int32 merge coordinates");
+    *n_out = d->num_vertices;
+}
+
+void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
+    cudaStream_t s = g->stream;
+    p.vb = d.vertex_begin;
+    p.ve = d.vertex_end;
+    p.rows = p.ve - p.vb;
+    p.csc_edges = d.csc_edges;
+    p.csr_edges = d.csr_edges;
+    if (d.memory == IPREGEL_MEMORY_HOST) {
+        auto up = [&](const void* src, size_t bytes) -> void* {
+            if (!src) return nullptr;
+            void* dst = p.graph_mem.alloc<uint8_t>((int64_t)bytes, s);
+            CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+            return dst;
+        };
+        p.csc_off = (const int32_t*)up(d.csc_offsets, (p.rows + 1) * 4);
+        p.csc_idx = (const int32_t*)up(d.csc_indices, d.csc_edges * 4);
+        p.csc_w = (const uint32_t*)up(d.csc_weights, d.csc_edges * 4);
+        p.csr_off = (const int32_t*)up(d.csr_offsets, (p.rows + 1) * 4);
+        p.csr_idx = (const int32_t*)up(d.csr_indices, d.csr_edges * 4);
+        p.csr_w = (const uint32_t*)up(d.csr_weights, d.csr_edges * 4);
+    } else {
+        p.csc_off = d.csc_offsets; p.csc_idx = d.csc_indices; p.csc_w = d.csc_weights;
+        p.csr_off = d.csr_offsets; p.csr_idx = d.csr_indices; p.csr_w = d.csr_weights;
+    }
+    if (d.validate) {
+        unsigned* flags = p.graph_mem.alloc<unsigned>(1, s, true);
+        k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csc_off, p.rows, p.csc_edges, flags);
+        k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csr_off, p.rows, p.csr_edges, flags);
+        LAUNCH_CHECK();
+        unsigned h = 0;
+        CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (h == 0) {
+            if (p.csc_edges)
+                k_validate_indices<<<std::min<unsigned>(grid_for(p.csc_edges, 256), 4096), 256, 0, s>>>(
+                    p.csc_idx, p.csc_edges, g->n, flags);
+            if (p.csr_edges)
+                k_validate_indices<<<std::min<unsigned>(grid_for(p.csr_edges, 256), 4096), 256, 0, s>>>(
+                    p.csr_idx, p.csr_edges, g->n, flags);
+            LAUNCH_CHECK();
+            CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+        }
+        if (h)
+            fail(IPREGEL_ERR_INVALID_GRAPH, "graph validation failed (flags 0x%x: %s%s%s)", h,
+                 (h & 1) ? "offsets[0]/offsets[rows] " : "", (h & 2) ? "non-monotone offsets " : "",
+                 (h & 4) ? "index out of range" : "");
+    }
+    p.pull_cnt = p.graph_mem.alloc<PullCounters>(1, s, true);
+    p.dscratch = p.graph_mem.alloc<unsigned long long>(64, s, true);
+    p.front_cnt = p.graph_mem.alloc<FrontierCounters>(1, s, true);
+    CU(cudaMallocHost(&p.host_cnt, 16 * sizeof(unsigned long long)));
+    // PageRank broadcasters (out-degree > 0)
+    unsigned long long* cnt = p.graph_mem.alloc<unsigned long long>(1, s, true);
+    if (p.rows) {
+        k_count_nondangling<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, cnt);
+        LAUNCH_CHECK();
+    }
+    unsigned long long h = 0;
+    CU(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    p.nondangling = (int64_t)h;
+}
+
+void build_plans(ipregel_graph* g) {
+    for (auto& p : g->parts) {
+        build_plan(p.plan_csc, p.csc_off, p.rows, p.csc_edges, p.vb + p.csc_ebase, p.graph_mem,
+                   g->stream);
+        build_plan(p.plan_csr, p.csr_off, p.rows, p.csr_edges, p.vb + p.csr_ebase, p.graph_mem,
+                   g->stream);
+    }
+    CU(cudaStreamSynchronize(g->stream));
+}
+
+void destroy_graph(ipregel_graph* g) {
+    if (!g) return;
+    cudaStreamSynchronize(g->stream);
+    for (auto& p : g->parts) {
+        for (auto& S : p.st) S.mem.release();
+        p.graph_mem.release();
+        if (p.host_cnt) cudaFreeHost(p.host_cnt);
+        p.host_cnt = nullptr;
+    }
+    for (auto e : g->events) cudaEventDestroy(e);
+    if (g->gather_tmp) cudaFree(g->gather_tmp);
+    delete g;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+#define ABI_BEGIN try {
+#define ABI_END                                                   \
+    }                                                             \
+    catch (const Failure& f_) {                                   \
+        g_last_error = f_.msg;                                    \
+        return f_.status;                                         \
+    }                                                             \
+    catch (const std::bad_alloc&) {                               \
+        g_last_error = "host allocation failed";                  \
+        return IPREGEL_ERR_OUT_OF_MEMORY;                         \
+    }                                                             \
+    catch (...) {                                                 \
+        g_last_error = "unexpected C++ exception";                \
+        return IPREGEL_ERR_CUDA;                                  \
+    }
+
+extern "C" {
+
+const char* ipregel_status_string(ipregel_status s) {
+    switch (s) {
+        case IPREGEL_OK: return "IPREGEL_OK";
+        case IPREGEL_ERR_INVALID_ARGUMENT: return "IPREGEL_ERR_INVALID_ARGUMENT";
+        case IPREGEL_ERR_INVALID_GRAPH: return "IPREGEL_ERR_INVALID_GRAPH";
+        case IPREGEL_ERR_OUT_OF_MEMORY: return "IPREGEL_ERR_OUT_OF_MEMORY";
+        case IPREGEL_ERR_CUDA: return "IPREGEL_ERR_CUDA";
+        case IPREGEL_ERR_NCCL: return "IPREGEL_ERR_NCCL";
+        case IPREGEL_ERR_MAX_SUPERSTEPS: return "IPREGEL_ERR_MAX_SUPERSTEPS";
+        case IPREGEL_ERR_STATE: return "IPREGEL_ERR_STATE";
+        case IPREGEL_ERR_UNSUPPORTED: return "IPREGEL_ERR_UNSUPPORTED";
+    }
+    return "IPREGEL_UNKNOWN_STATUS";
+}
+
+const char* ipregel_last_error(void) { return g_last_error.c_str(); }
+
+int ipregel_abi_version(void) { return IPREGEL_ABI_VERSION; }
+
+uint64_t ipregel_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+ipregel_status ipregel_device_check(int device) {
+    ABI_BEGIN
+    check_device(device);
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_run_params_default(ipregel_run_params* out) {
+    if (!out) { g_last_error = "out is NULL"; return IPREGEL_ERR_INVALID_ARGUMENT; }
+    out->mode = IPREGEL_MODE_AUTO;
+    out->pagerank_iterations = 10;
+    out->sssp_source = 0;
+    out->push_fraction = 0.04f;
+    out->flags = 0;
+    return IPREGEL_OK;
+}
+
+ipregel_status ipregel_partition(const int64_t* cost_prefix, int64_t n, int world,
+                                 int64_t* bounds_out) {
+    ABI_BEGIN
+    if (!cost_prefix || !bounds_out || n < 0 || world < 1)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "bad partition arguments");
+    if (cost_prefix[0] != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "cost_prefix[0] must be 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (cost_prefix[i + 1] < cost_prefix[i])
+            fail(IPREGEL_ERR_INVALID_ARGUMENT, "cost_prefix decreases at %lld", (long long)i);
+    const int64_t total = cost_prefix[n];
+    bounds_out[0] = 0;
+    for (int r = 1; r < world; ++r) {
+        // first vertex whose prefix reaches the r-th equal share (lower bound)
+        const long double target = (long double)total * r / world;
+        int64_t lo = bounds_out[r - 1], hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((long double)cost_prefix[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        bounds_out[r] = lo;
+    }
+    bounds_out[world] = n;
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_nccl_unique_id(uint8_t out[128]) {
+    ABI_BEGIN
+    if (!out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "out is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    memcpy(out, &id, 128);
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_comm_create(int rank, int world, const uint8_t id[128], int device,
+                                   ipregel_comm** out) {
+    ABI_BEGIN
+    if (!out || !id || world < 1 || rank < 0 || rank >= world)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "bad comm arguments");
+    *out = nullptr;
+    CU(cudaSetDevice(device));
+    check_device(device);
+    ncclUniqueId uid;
+    memcpy(&uid, id, 128);
+    ipregel_comm* c = new ipregel_comm;
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        fail(IPREGEL_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    *out = c;
+    return IPREGEL_OK;
+    ABI_END
+}
+
+void ipregel_comm_destroy(ipregel_comm* comm) {
+    if (!comm) return;
+    if (comm->nccl) ncclCommDestroy(comm->nccl);
+    delete comm;
+}
+
+static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipregel_comm* comm,
+                                    void* stream, ipregel_graph** out) {
+    ABI_BEGIN
+    if (!out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!descs || np < 1) fail(IPREGEL_ERR_INVALID_ARGUMENT, "no partition descriptors");
+    int64_t n = 0;
+    for (int i = 0; i < np; ++i) {
+        int64_t ni;
+        validate_desc(&descs[i], &ni);
+        if (i == 0) n = ni;
+        else if (ni != n || descs[i].num_edges != descs[0].num_edges)
+            fail(IPREGEL_ERR_INVALID_ARGUMENT, "partitions disagree on N or E");
+    }
+    if (!comm || comm->world == 1) {
+        int64_t expect = 0;
+        for (int i = 0; i < np; ++i) {
+            if (descs[i].vertex_begin != expect)
+                fail(IPREGEL_ERR_INVALID_ARGUMENT, "partition %d starts at %lld, expected %lld", i,
+                     (long long)descs[i].vertex_begin, (long long)expect);
+            expect = descs[i].vertex_end;
+        }
+        if (expect != n) fail(IPREGEL_ERR_INVALID_ARGUMENT, "partitions do not cover [0, N)");
+    }
+    int device = 0;
+    CU(cudaGetDevice(&device));
+    check_device(device);
+    ipregel_graph* g = new ipregel_graph;
+    g->n = n;
+    g->e = descs[0].num_edges;
+    g->device = device;
+    g->stream = static_cast<cudaStream_t>(stream);
+    g->comm = comm;
+    g->parts.resize(np);
+    try {
+        int64_t csc_base = 0, csr_base = 0;
+        for (int i = 0; i < np; ++i) {
+            g->parts[i].csc_ebase = csc_base;
+            g->parts[i].csr_ebase = csr_base;
+            csc_base += descs[i].csc_edges;
+            csr_base += descs[i].csr_edges;
+        }
+        if (comm && comm->world > 1) {
+            // every rank's (vb, rows, csc_edges, csr_edges) -> ranges and global edge bases
+            int64_t mine[4] = {descs[0].vertex_begin, descs[0].vertex_end - descs[0].vertex_begin,
+                               descs[0].csc_edges, descs[0].csr_edges};
+            int64_t* dmine = nullptr;
+            int64_t* dall = nullptr;
+            CU(cudaMalloc(&dmine, 4 * sizeof(int64_t)));
+            CU(cudaMalloc(&dall, 4 * sizeof(int64_t) * comm->world));
+            CU(cudaMemcpyAsync(dmine, mine, sizeof(mine), cudaMemcpyHostToDevice, g->stream));
+            NC(ncclAllGather(dmine, dall, 4, ncclInt64, comm->nccl, g->stream));
+            std::vector<int64_t> all(4 * comm->world);
+            CU(cudaMemcpyAsync(all.data(), dall, all.size() * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, g->stream));
+            CU(cudaStreamSynchronize(g->stream));
+            cudaFree(dmine);
+            cudaFree(dall);
+            int64_t expect = 0, cb = 0, rb = 0;
+            for (int r = 0; r < comm->world; ++r) {
+                if (all[4 * r] != expect)
+                    fail(IPREGEL_ERR_INVALID_ARGUMENT, "rank ranges do not tile [0, N)");
+                g->rank_vb.push_back(all[4 * r]);
+                g->rank_rows.push_back(all[4 * r + 1]);
+                if (r == comm->rank) {
+                    g->parts[0].csc_ebase = cb;
+                    g->parts[0].csr_ebase = rb;
+                }
+                expect += all[4 * r + 1];
+                cb += all[4 * r + 2];
+                rb += all[4 * r + 3];
+            }
+            if (expect != n) fail(IPREGEL_ERR_INVALID_ARGUMENT, "rank ranges do not cover [0, N)");
+        }
+        for (int i = 0; i < np; ++i) init_partition(g, g->parts[i], descs[i]);
+        build_plans(g);
+    } catch (...) {
+        destroy_graph(g);
+        throw;
+    }
+    *out = g;
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_graph_create(const ipregel_graph_desc* desc, ipregel_comm* comm,
+                                    void* stream, ipregel_graph** out) {
+    return create_common(desc, 1, comm, stream, out);
+}
+
+ipregel_status ipregel_graph_create_partitioned(const ipregel_graph_desc* descs,
+                                                int num_partitions, void* stream,
+                                                ipregel_graph** out) {
+    return create_common(descs, num_partitions, nullptr, stream, out);
+}
+
+void ipregel_graph_destroy(ipregel_graph* graph) { destroy_graph(graph); }
+
+ipregel_status ipregel_memory_footprint(ipregel_graph* g, uint64_t* graph_bytes,
+                                        uint64_t* state_bytes) {
+    ABI_BEGIN
+    if (!g) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph is NULL");
+    uint64_t gb = 0, sb = 0;
+    for (auto& p : g->parts) {
+        gb += p.graph_mem.bytes;
+        for (auto& S : p.st) sb += S.mem.bytes;
+    }
+    if (graph_bytes) *graph_bytes = gb;
+    if (state_bytes) *state_bytes = sb;
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner combiner,
+                           uint32_t max_supersteps, const ipregel_run_params* params) {
+    ABI_BEGIN
+    if (!g) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph is NULL");
+    if (g->poisoned) fail(IPREGEL_ERR_STATE, "graph handle was poisoned by an earlier failure");
+    ipregel_run_params P;
+    ipregel_run_params_default(&P);
+    if (params) P = *params;
+    if (app < IPREGEL_APP_PAGERANK || app > IPREGEL_APP_SSSP)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown app %d", (int)app);
+    const ipregel_combiner want =
+        app == IPREGEL_APP_PAGERANK ? IPREGEL_COMBINE_SUM : IPREGEL_COMBINE_MIN;
+    if (combiner != want)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT,
+             "combiner %d does not match the app (PageRank sums, Fig. 8; CC/SSSP take the min, "
+             "Fig. 5)", (int)combiner);
+    if (max_supersteps == 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "max_supersteps must be >= 1");
+    if (P.mode < IPREGEL_MODE_AUTO || P.mode > IPREGEL_MODE_PUSH)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown mode %d", P.mode);
+    if (P.flags != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "flags must be 0");
+    if (app == IPREGEL_APP_SSSP && (int64_t)P.sssp_source >= g->n)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "sssp_source %u >= N", P.sssp_source);
+    if (!(P.push_fraction >= 0.0f)) fail(IPREGEL_ERR_INVALID_ARGUMENT, "push_fraction < 0");
+    if (app == IPREGEL_APP_SSSP && g->parts[0].csc_w == nullptr) {
+        // unit weights (Fig. 10) -- fine
+    }
+    g->last_status = -1;
+    g->last_app = -1;
+    ipregel_status st;
+    try {
+        ensure_state(g, app);
+        st = app == IPREGEL_APP_PAGERANK ? run_pagerank(g, max_supersteps, P)
+                                         : run_min(g, app, max_supersteps, P);
+    } catch (const Failure& f) {
+        if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
+        throw;
+    }
+    g->last_app = app;
+    g->last_status = st;
+    if (st != IPREGEL_OK) g_last_error = "superstep guard reached with work remaining";
+    return st;
+    ABI_END
+}
+
+ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
+                                  int out_is_device) {
+    ABI_BEGIN
+    if (!g || !out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or out is NULL");
+    if (g->poisoned) fail(IPREGEL_ERR_STATE, "graph handle was poisoned");
+    if (g->last_app < 0) fail(IPREGEL_ERR_STATE, "no completed run");
+    const bool pr = g->last_app == IPREGEL_APP_PAGERANK;
+    const size_t esz = pr ? 8 : 4;
+    if (out_bytes != (size_t)g->n * esz)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "out_bytes %zu != N * %zu", out_bytes, esz);
+    cudaStream_t s = g->stream;
+    const cudaMemcpyKind kind = out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    try {
+        if (pr) {
+            if (multi_rank(g)) {
+                if (!g->gather_tmp) CU(cudaMalloc(&g->gather_tmp, g->n * sizeof(double)));
+                Partition& p = g->parts[0];
+                if (p.rows)
+                    CU(cudaMemcpyAsync(g->gather_tmp + p.vb, p.st[0].rank, p.rows * 8,
+                                       cudaMemcpyDeviceToDevice, s));
+                NC(ncclGroupStart());
+                for (int r = 0; r < g->comm->world; ++r)
+                    if (g->rank_rows[r])
+                        NC(ncclBroadcast(g->gather_tmp + g->rank_vb[r], g->gather_tmp + g->rank_vb[r],
+                                         (size_t)g->rank_rows[r], ncclFloat64, r, g->comm->nccl, s));
+                NC(ncclGroupEnd());
+                CU(cudaMemcpyAsync(out, g->gather_tmp, g->n * 8, kind, s));
+            } else {
+                for (auto& p : g->parts)
+                    if (p.rows)
+                        CU(cudaMemcpyAsync((double*)out + p.vb, p.st[0].rank, p.rows * 8, kind, s));
+            }
+        } else {
+            Partition& p = g->parts[0];
+            CU(cudaMemcpyAsync(out, p.st[g->last_app].val[g->cur], g->n * 4, kind, s));
+        }
+        CU(cudaStreamSynchronize(s));
+    } catch (const Failure& f) {
+        if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
+        throw;
+    }
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_get_stats(ipregel_graph* g, ipregel_stats* st) {
+    ABI_BEGIN
+    if (!g || !st) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or stats is NULL");
+    st->supersteps = (uint32_t)g->steps.size();
+    st->status = g->last_status;
+    const size_t m = std::min<size_t>(st->capacity, g->steps.size());
+    for (size_t i = 0; i < m; ++i) {
+        const StepRecord& R = g->steps[i];
+        if (st->time_ms) st->time_ms[i] = R.time_ms;
+        if (st->kernel_ms) st->kernel_ms[i] = R.kernel_ms;
+        if (st->mode) st->mode[i] = R.mode;
+        if (st->changed) st->changed[i] = R.changed;
+        if (st->messages) st->messages[i] = R.messages;
+        if (st->edges_scanned) st->edges_scanned[i] = R.edges_scanned;
+        if (st->model_bytes) st->model_bytes[i] = R.model_bytes;
+    }
+    return IPREGEL_OK;
+    ABI_END
+}
+
+}  // extern "C"

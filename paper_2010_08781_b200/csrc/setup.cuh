@@ -1,0 +1,164 @@
+// paper_2010_08781_b200/csrc/setup.cuh -- superstep 0, validation, push-view construction and
+// small utility kernels.
+#pragma once
+#include "common.cuh"
+
+namespace ipr {
+
+// ---- superstep 0 (the `ip_is_first_superstep()` branches of Figs. 8-10) --------------------
+// PageRank, Fig. 8 / PAPER.md:322: value = 1/N and, if superstep 0 < k, broadcast value/outdeg
+// (a vertex without out-neighbours does not broadcast, reading R4).
+__global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t rows, int64_t vbase,
+                                double inv_n, int broadcast, int write_rank,
+                                double* __restrict__ rank, double* __restrict__ contrib) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    if (write_rank) rank[i] = inv_n;
+    if (broadcast) {
+        const int32_t deg = out_off[i + 1] - out_off[i];
+        contrib[vbase + i] = deg > 0 ? __ddiv_rn(inv_n, (double)deg) : 0.0;
+    }
+}
+
+// Hash-Min CC, Fig. 9: value = id (every replica initialises all N locally -- no exchange).
+__global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) val[i] = (uint32_t)i;
+}
+
+// SSSP, Fig. 10: source = 0, everyone else INF.
+__global__ void k_init_sssp(uint32_t* __restrict__ val, int64_t n, int64_t source) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) val[i] = i == source ? 0u : kInf;
+}
+
+__global__ void k_fill_bits(uint32_t* __restrict__ bits, int64_t rows) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nwords = (rows + 31) >> 5;
+    if (w >= nwords) return;
+    const int64_t rem = rows - w * 32;
+    bits[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+}
+
+__global__ void k_set_bit(uint32_t* __restrict__ bits, int64_t row) {
+    bits[row >> 5] |= 1u << (row & 31);
+}
+
+// Scatter a global frontier's (id, value) snapshots into a replica (multi-partition push).
+__global__ void k_scatter_frontier(const int32_t* __restrict__ id, const uint32_t* __restrict__ v,
+                                   const unsigned long long* __restrict__ len,
+                                   uint32_t* __restrict__ val) {
+    const int64_t n = (int64_t)*len;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        val[id[i]] = v[i];
+}
+
+__global__ void k_iota(int32_t* __restrict__ a, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+
+// Owned vertices with out-degree > 0 (PageRank broadcasters).
+__global__ void k_count_nondangling(const int32_t* __restrict__ out_off, int64_t rows,
+                                    unsigned long long* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool p = i < rows && out_off[i + 1] > out_off[i];
+    const unsigned b = __ballot_sync(kFull, p);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
+// ---- validation (ipregel_graph_desc.validate) ------------------------------------------------
+// flags bit 0: offsets[0] != 0 or offsets[rows] != edges; bit 1: offsets decrease; bit 2: index
+// outside [0, N).
+__global__ void k_validate_offsets(const int32_t* __restrict__ off, int64_t rows, int64_t edges,
+                                   unsigned* __restrict__ flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && (off[0] != 0 || (int64_t)off[rows] != edges)) atomicOr(flags, 1u);
+    if (i < rows && off[i + 1] < off[i]) atomicOr(flags, 2u);
+}
+__global__ void k_validate_indices(const int32_t* __restrict__ idx, int64_t edges, int64_t n,
+                                   unsigned* __restrict__ flags) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = idx[i];
+        if (v < 0 || (int64_t)v >= n) { atomicOr(flags, 4u); return; }
+    }
+}
+
+// ---- push view for a destination partition (multi-GPU push mode) ---------------------------
+// Source-major list of the edges whose destination is owned: built by transposing the owned
+// CSC rows (u -> v) and, for CC, the owned CSR rows reversed (u <- v taken as u -> v).
+__global__ void k_hist_sources(const int32_t* __restrict__ idx, int64_t edges,
+                               int32_t* __restrict__ cnt /* [n+1]; exclusive-scanned after */) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + idx[i], 1);
+}
+
+__global__ void k_transpose_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                 const uint32_t* __restrict__ w, int64_t rows, int64_t vbase,
+                                 int32_t* __restrict__ cursor, int32_t* __restrict__ out_idx,
+                                 uint32_t* __restrict__ out_w) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32) {
+        const int32_t u = idx[e];
+        const int32_t pos = atomicAdd(cursor + u, 1);
+        out_idx[pos] = (int32_t)(vbase + r);
+        if (out_w) out_w[pos] = w ? w[e] : 1u;
+    }
+}
+
+// Device-wide exclusive scan of int32 counts (in place), 3 passes with a u64 block scratch.
+constexpr int kScanChunk = 2048;
+__global__ void __launch_bounds__(256)
+k_chunk_sums(const int32_t* __restrict__ a, int64_t n, unsigned long long* __restrict__ sums) {
+    __shared__ unsigned long long s[8];
+    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
+    unsigned long long t = 0;
+    for (int64_t i = base + threadIdx.x; i < base + kScanChunk && i < n; i += 256) t += (unsigned)a[i];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long x = 0;
+        for (int w = 0; w < 8; ++w) x += s[w];
+        sums[blockIdx.x] = x;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_chunk_apply(int32_t* __restrict__ a, int64_t n, const unsigned long long* __restrict__ offs) {
+    __shared__ unsigned long long s_w[8];
+    constexpr int kPer = kScanChunk / 256;
+    const int64_t i0 = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kPer;
+    int32_t v[kPer];
+    unsigned long long t = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        v[k] = i0 + k < n ? a[i0 + k] : 0;
+        t += (unsigned)v[k];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long inc = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long o = __shfl_up_sync(kFull, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    unsigned long long pre = offs[blockIdx.x];
+    for (int w = 0; w < warp; ++w) pre += s_w[w];
+    pre += inc - t;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        if (i0 + k < n) a[i0 + k] = (int32_t)pre;
+        pre += (unsigned)v[k];
+    }
+}
+
+}  // namespace ipr

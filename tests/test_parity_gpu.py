@@ -1,0 +1,315 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  - CC labels and SSSP distances: bit-exact; superstep count and per-superstep changed /
+    messages counters equal to the oracle's.
+  - PageRank: max |gpu - oracle| <= 1e-9 (the gate), plus the internal diagnostic
+    max relative error <= 1e-11.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import checkers
+from tests.graphs import csr_csc, make_graph
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")
+with open(GOLDEN) as f:
+    WORKED = json.load(f)
+
+MODES = ["pull", "push", "auto"]
+PR_ABS = 1e-9
+PR_REL = 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2010_08781_b200 as ipr
+    ipr.device_check(0)
+
+
+def run_gpu(app, n, src, dst, w=None, mode="auto", k=10, source=0, partitions=1,
+            max_supersteps=1 << 30, host=False, allow_guard=False):
+    g = csr_csc(n, src, dst, w)
+    G = make_graph(g, partitions=partitions, host=host, weighted=w is not None)
+    st = G.run(app, max_supersteps=max_supersteps, mode=mode, iterations=k, source=source,
+               allow_guard=allow_guard)
+    vals = G.values(host=True)
+    stats = G.stats()
+    G.close()
+    return st, vals, stats
+
+
+def check_min(app, n, src, dst, w=None, source=0, mode="auto", partitions=1):
+    o = oracle.run(oracle.APP_HASHMIN_CC if app == "cc" else oracle.APP_SSSP, n, src, dst, w,
+                   source=source)
+    st, v, s = run_gpu(app, n, src, dst, w, mode=mode, source=source, partitions=partitions)
+    np.testing.assert_array_equal(v, o["values"])
+    assert s["supersteps"] == o["supersteps"]
+    np.testing.assert_array_equal(s["changed"], o["changed"])
+    np.testing.assert_array_equal(s["messages"], o["messages"])
+    return s
+
+
+def check_pr(n, src, dst, k=10, mode="pull", partitions=1):
+    o = oracle.pagerank(n, src, dst, k=k)
+    st, v, s = run_gpu("pagerank", n, src, dst, mode=mode, k=k, partitions=partitions)
+    err = np.abs(v - o["values"])
+    assert err.max() <= PR_ABS
+    rel = err / np.maximum(np.abs(o["values"]), 1e-300)
+    assert rel.max() <= PR_REL, rel.max()
+    assert s["supersteps"] == o["supersteps"]
+    np.testing.assert_array_equal(s["changed"], o["changed"])
+    np.testing.assert_array_equal(s["messages"], o["messages"])
+    return v
+
+
+# ------------------------------------------------------------------ worked examples
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", WORKED["pagerank"], ids=lambda c: c["name"])
+def test_pagerank_worked(case, mode):
+    from fractions import Fraction
+    e = np.array(case["edges"], np.int64).reshape(-1, 2)
+    _, v, s = run_gpu("pagerank", case["n"], e[:, 0], e[:, 1], k=case["k"],
+                      mode="push" if mode == "push" else "pull")
+    want = np.array([float(Fraction(x)) for x in case["values"]])
+    np.testing.assert_allclose(v, want, rtol=1e-14, atol=0)
+    assert s["supersteps"] == case["supersteps"]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", WORKED["cc"], ids=lambda c: c["name"])
+def test_cc_worked(case, mode):
+    e = np.array(case["edges"], np.int64).reshape(-1, 2)
+    _, v, s = run_gpu("cc", case["n"], e[:, 0], e[:, 1], mode=mode)
+    want = case["trajectory"][-1] if "trajectory" in case else case["values"]
+    assert list(v) == want
+    if "supersteps" in case:
+        assert s["supersteps"] == case["supersteps"]
+    if "changed" in case:
+        assert list(s["changed"]) == case["changed"]
+        assert list(s["messages"]) == case["messages"]
+    if "trajectory" in case:
+        for step, traj in enumerate(case["trajectory"][:-1]):
+            st, vv, _ = run_gpu("cc", case["n"], e[:, 0], e[:, 1], mode=mode,
+                                max_supersteps=step + 1, allow_guard=True)
+            assert list(vv) == traj, step
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", WORKED["sssp"], ids=lambda c: c["name"])
+def test_sssp_worked(case, mode):
+    e = np.array(case["edges"], np.int64).reshape(-1, 3)
+    _, v, s = run_gpu("sssp", case["n"], e[:, 0], e[:, 1], e[:, 2], mode=mode,
+                      source=case["source"])
+    final = case["trajectory"][-1] if "trajectory" in case else case["values"]
+    assert list(v) == [oracle.INF if x == "INF" else int(x) for x in final]
+    assert s["supersteps"] == case["supersteps"]
+    if "changed" in case:
+        assert list(s["changed"]) == case["changed"]
+        assert list(s["messages"]) == case["messages"]
+
+
+# ------------------------------------------------------------------ random graphs
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("mode", MODES)
+def test_random_cc(seed, mode):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 3000))
+    m = int(rng.integers(0, 6 * n))
+    src, dst, _ = checkers.random_graph(rng, n, m)
+    check_min("cc", n, src, dst, mode=mode)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("mode", MODES)
+def test_random_sssp(seed, mode):
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.integers(1, 3000))
+    m = int(rng.integers(0, 6 * n))
+    src, dst, w = checkers.random_graph(rng, n, m, weighted=True)
+    check_min("sssp", n, src, dst, w if seed % 3 else None, source=int(rng.integers(0, n)),
+              mode=mode)
+
+
+@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("mode", ["pull", "push"])
+def test_random_pagerank(seed, mode):
+    rng = np.random.default_rng(3000 + seed)
+    n = int(rng.integers(1, 5000))
+    m = int(rng.integers(0, 8 * n))
+    src, dst, _ = checkers.random_graph(rng, n, m)
+    check_pr(n, src, dst, k=[0, 1, 3, 10][seed % 4], mode=mode)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_hub_spanning_many_tiles():
+    # in-star with 300k leaves: one row spans ~150 tiles (pull_fixup path); closed form too
+    n = 300_001
+    leaves = np.arange(1, n)
+    hub = np.zeros(n - 1, np.int64)
+    v = check_pr(n, leaves, hub, k=3)
+    want = (0.15 / n) * (1 + 0.85 * (n - 1))
+    assert v[0] == pytest.approx(want, rel=1e-12)
+    check_min("cc", n, leaves, hub)
+    check_min("sssp", n, hub, leaves, np.full(n - 1, 7, np.uint32))
+
+
+def test_long_chain_many_supersteps():
+    n = 3000
+    src = np.arange(n - 1)
+    for mode in MODES:
+        s = check_min("sssp", n, src, src + 1, mode=mode)
+        assert s["supersteps"] == n
+    check_min("cc", n, src, src + 1)
+
+
+def test_single_vertex_and_empty_graph():
+    for app in ("cc", "sssp"):
+        check_min(app, 1, np.zeros(0, np.int64), np.zeros(0, np.int64))
+        check_min(app, 17, np.zeros(0, np.int64), np.zeros(0, np.int64))
+    check_pr(1, np.zeros(0, np.int64), np.zeros(0, np.int64))
+    check_pr(9, np.zeros(0, np.int64), np.zeros(0, np.int64))
+
+
+def test_duplicates_and_saturation():
+    src = np.array([0, 0, 0, 1, 1, 2])
+    dst = np.array([1, 1, 1, 2, 2, 3])
+    w = np.array([9, 3, 5, 0xFFFFFFF0, 2, 60], np.uint32)
+    check_min("sssp", 4, src, dst, w)
+    check_pr(4, src, dst, k=4)
+
+
+def test_guard_partial_state():
+    n = 50
+    src = np.arange(n - 1)
+    o = oracle.sssp(n, src, src + 1, None, source=0, max_supersteps=7)
+    st, v, s = run_gpu("sssp", n, src, src + 1, max_supersteps=7, allow_guard=True)
+    import paper_2010_08781_b200 as ipr
+    assert st == ipr.ERR_MAX_SUPERSTEPS and o["status"] == oracle.GUARD
+    np.testing.assert_array_equal(v, o["values"])
+    assert s["supersteps"] == 7
+    o = oracle.pagerank(n, src, src + 1, k=10, max_supersteps=4)
+    st, v, s = run_gpu("pagerank", n, src, src + 1, k=10, max_supersteps=4, allow_guard=True)
+    assert st == ipr.ERR_MAX_SUPERSTEPS
+    assert np.abs(v - o["values"]).max() <= 1e-15
+
+
+def test_combiner_mismatch_and_bad_args():
+    import paper_2010_08781_b200 as ipr
+    g = make_graph(csr_csc(3, [0, 1], [1, 2]), weighted=False)
+    with pytest.raises(ipr.IpregelError) as e:
+        g.run("pagerank", combiner=ipr.COMBINE_MIN)
+    assert e.value.status == ipr.ERR_INVALID_ARGUMENT
+    with pytest.raises(ipr.IpregelError):
+        g.run("sssp", source=3)
+    with pytest.raises(ipr.IpregelError):
+        g.run("cc", max_supersteps=0)
+    with pytest.raises(ipr.IpregelError) as e:
+        g.values()
+    assert e.value.status == ipr.ERR_STATE
+
+
+def test_validate_rejects_bad_graph():
+    import paper_2010_08781_b200 as ipr
+    g = csr_csc(4, [0, 1, 2], [1, 2, 3])
+    g["csc_idx"] = g["csc_idx"].copy()
+    g["csc_idx"][1] = 9
+    with pytest.raises(ipr.IpregelError) as e:
+        make_graph(g, validate=True, weighted=False)
+    assert e.value.status == ipr.ERR_INVALID_GRAPH
+    g = csr_csc(4, [0, 1, 2], [1, 2, 3])
+    g["csr_off"] = g["csr_off"].copy()
+    g["csr_off"][2] = 0
+    with pytest.raises(ipr.IpregelError) as e:
+        make_graph(g, validate=True, weighted=False)
+    assert e.value.status == ipr.ERR_INVALID_GRAPH
+
+
+def test_host_memory_descriptor_matches_device():
+    rng = np.random.default_rng(5)
+    n = 2000
+    src, dst, w = checkers.random_graph(rng, n, 9000, weighted=True)
+    g = csr_csc(n, src, dst, w)
+    a = make_graph(g)
+    b = make_graph(g, host=True)
+    for app in ("pagerank", "cc", "sssp"):
+        a.run(app)
+        b.run(app)
+        np.testing.assert_array_equal(a.values(host=True), b.values(host=True))
+
+
+def test_message_storage_is_theta_n():
+    # single-slot mailboxes -- state bytes do not grow with E
+    import paper_2010_08781_b200 as ipr  # noqa: F401
+    n = 4096
+    small = csr_csc(n, np.arange(n - 1), np.arange(1, n))
+    rng = np.random.default_rng(9)
+    s2, d2, _ = checkers.random_graph(rng, n, 400_000)
+    big = csr_csc(n, s2, d2)
+    out = []
+    for g in (small, big):
+        G = make_graph(g, weighted=False)
+        for app in ("pagerank", "cc", "sssp"):
+            for mode in ("pull", "push"):
+                G.run(app, mode=mode)
+        out.append(G.memory_footprint()[1])
+    assert out[0] == out[1]
+    assert out[0] < 200 * n + (1 << 20)
+
+
+# ------------------------------------------------------------------ partitions (loopback)
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_loopback_partitions_bit_identical(parts):
+    rng = np.random.default_rng(77)
+    import inputs
+    src, dst, w = inputs.rmat_coo(13, 16, 11, weighted=True)
+    n = 1 << 13
+    g = csr_csc(n, src, dst, w)
+    ref = {}
+    G1 = make_graph(g)
+    for app in ("pagerank", "cc", "sssp"):
+        for mode in ("pull", "push", "auto"):
+            if app == "pagerank" and mode == "auto":
+                continue
+            G1.run(app, mode=mode)
+            ref[(app, mode)] = (G1.values(host=True), G1.stats())
+    Gp = make_graph(g, partitions=parts)
+    for (app, mode), (v1, s1) in ref.items():
+        Gp.run(app, mode=mode)
+        vp = Gp.values(host=True)
+        sp = Gp.stats()
+        if app == "pagerank" and mode == "push":
+            assert np.abs(vp - v1).max() <= 1e-15  # atomicAdd order
+        else:
+            np.testing.assert_array_equal(vp, v1)  # bit-identical, PageRank pull included
+        assert sp["supersteps"] == s1["supersteps"]
+        np.testing.assert_array_equal(sp["changed"], s1["changed"])
+        np.testing.assert_array_equal(sp["messages"], s1["messages"])
+    o = oracle.sssp(n, src, dst, w, source=0)
+    Gp.run("sssp")
+    np.testing.assert_array_equal(Gp.values(host=True), o["values"])
+    del rng
+
+
+def test_loopback_with_empty_partition():
+    n = 100
+    src = np.arange(n - 1)
+    g = csr_csc(n, src, src + 1)
+    G = make_graph(g, partitions=3, weighted=False, bounds=np.array([0, 0, 60, 100]))
+    for app in ("pagerank", "cc", "sssp"):
+        G.run(app)
+    o = oracle.sssp(n, src, src + 1, None)
+    np.testing.assert_array_equal(G.values(host=True), o["values"])
