@@ -64,13 +64,14 @@ constexpr int kSlotsPerBlock = 8192;
 
 // degree histograms (counts at index + 1) and number of kept edges
 __global__ void k_count(Gen g, uint64_t slots, int32_t* deg_row_by_dst, int32_t* deg_row_by_src,
-                        unsigned long long* kept) {
+                        unsigned long long* kept, const int32_t* remap) {
     unsigned long long local = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s, d;
         g.edge(i, s, d);
         if (s == d) continue;
+        if (remap) { s = (uint32_t)remap[s]; d = (uint32_t)remap[d]; }
         ++local;
         if (deg_row_by_dst) atomicAdd(deg_row_by_dst + d + 1, 1);
         if (deg_row_by_src) atomicAdd(deg_row_by_src + s + 1, 1);
@@ -81,12 +82,13 @@ __global__ void k_count(Gen g, uint64_t slots, int32_t* deg_row_by_dst, int32_t*
 
 // scatter keys (neighbour << 6 | (w - 1)) into rows via an atomic cursor
 __global__ void k_scatter(Gen g, uint64_t slots, int by_dst, int weighted, int32_t* cursor,
-                          uint64_t* keys) {
+                          uint64_t* keys, const int32_t* remap) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s, d;
         g.edge(i, s, d);
         if (s == d) continue;
+        if (remap) { s = (uint32_t)remap[s]; d = (uint32_t)remap[d]; }
         const uint32_t row = by_dst ? d : s, nbr = by_dst ? s : d;
         const uint32_t w = weighted ? g.weight(i) : 1u;
         const int32_t pos = atomicAdd(cursor + row, 1);
@@ -180,7 +182,7 @@ int64_t rmat_gpu_count(uint64_t seed, int scale, uint64_t slots, uint32_t ta, ui
     unsigned long long* d_kept = nullptr;
     CK(cudaMallocAsync(&d_kept, 8, s));
     CK(cudaMemsetAsync(d_kept, 0, 8, s));
-    k_count<<<148 * 16, kThreads, 0, s>>>(g, slots, deg_by_dst, deg_by_src, d_kept);
+    k_count<<<148 * 16, kThreads, 0, s>>>(g, slots, deg_by_dst, deg_by_src, d_kept, nullptr);
     CK(cudaGetLastError());
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, d_kept, 8, cudaMemcpyDeviceToHost, s));
@@ -223,7 +225,7 @@ int64_t rmat_gpu_coo(uint64_t seed, int scale, uint64_t slots, uint32_t ta, uint
 // Returns kept, or -1 on error.
 int64_t rmat_gpu_adjacency(uint64_t seed, int scale, uint64_t slots, uint32_t ta, uint32_t tab,
                            uint32_t tabc, int by_dst, int32_t* off, int32_t* idx, uint32_t* w,
-                           void* stream) {
+                           const int32_t* remap, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = (int64_t)1 << scale;
     Gen g = make_gen(seed, scale, ta, tab, tabc);
@@ -231,7 +233,7 @@ int64_t rmat_gpu_adjacency(uint64_t seed, int scale, uint64_t slots, uint32_t ta
     CK(cudaMallocAsync(&d_kept, 8, s));
     CK(cudaMemsetAsync(d_kept, 0, 8, s));
     k_count<<<148 * 16, kThreads, 0, s>>>(g, slots, by_dst ? off : nullptr,
-                                          by_dst ? nullptr : off, d_kept);
+                                          by_dst ? nullptr : off, d_kept, remap);
     CK(cudaGetLastError());
     unsigned long long kept = 0;
     CK(cudaMemcpyAsync(&kept, d_kept, 8, cudaMemcpyDeviceToHost, s));
@@ -251,7 +253,7 @@ int64_t rmat_gpu_adjacency(uint64_t seed, int scale, uint64_t slots, uint32_t ta
     CK(cudaMemcpyAsync(cursor, off, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaMallocAsync(&keys, (kept + 1) * 8, s));
     CK(cudaMallocAsync(&keys2, (kept + 1) * 8, s));
-    k_scatter<<<148 * 16, kThreads, 0, s>>>(g, slots, by_dst, w != nullptr, cursor, keys);
+    k_scatter<<<148 * 16, kThreads, 0, s>>>(g, slots, by_dst, w != nullptr, cursor, keys, remap);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(cursor, s));
     // sort each row by (neighbour, weight): deterministic arrays
@@ -267,6 +269,58 @@ int64_t rmat_gpu_adjacency(uint64_t seed, int scale, uint64_t slots, uint32_t ta
     CK(cudaFreeAsync(keys2, s));
     CK(cudaStreamSynchronize(s));
     return (int64_t)kept;
+}
+
+__global__ void k_iota_u32(uint32_t* a, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (uint32_t)i;
+}
+__global__ void k_invert(const uint32_t* old_of_new, int64_t n, int32_t* new_of_old) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) new_of_old[old_of_new[i]] = (int32_t)i;
+}
+
+// Degree-descending vertex order (ties: ascending original id): a layout choice for the device
+// graph, not part of the method.  old_of_new[k] = original id of internal vertex k;
+// new_of_old = its inverse.  `deg_src` / `deg_dst` select which degrees are summed.
+int64_t rmat_gpu_degree_order(uint64_t seed, int scale, uint64_t slots, uint32_t ta, uint32_t tab,
+                              uint32_t tabc, int use_out, int use_in, int32_t* old_of_new,
+                              int32_t* new_of_old, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = (int64_t)1 << scale;
+    Gen g = make_gen(seed, scale, ta, tab, tabc);
+    int32_t* deg = nullptr;
+    unsigned long long* d_kept = nullptr;
+    CK(cudaMallocAsync(&deg, (n + 1) * 4, s));
+    CK(cudaMemsetAsync(deg, 0, (n + 1) * 4, s));
+    CK(cudaMallocAsync(&d_kept, 8, s));
+    CK(cudaMemsetAsync(d_kept, 0, 8, s));
+    // both histograms land in the same array (counts at index + 1)
+    k_count<<<148 * 16, kThreads, 0, s>>>(g, slots, use_in ? deg : nullptr,
+                                          use_out ? deg : nullptr, d_kept, nullptr);
+    CK(cudaGetLastError());
+    uint32_t *keys_out = nullptr, *vals_in = nullptr;
+    CK(cudaMallocAsync(&keys_out, n * 4, s));
+    CK(cudaMallocAsync(&vals_in, n * 4, s));
+    k_iota_u32<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vals_in, n);
+    void* tmp = nullptr;
+    size_t tb = 0;
+    const uint32_t* keys_in = reinterpret_cast<const uint32_t*>(deg + 1);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys_in, keys_out, vals_in,
+                                              (uint32_t*)old_of_new, (int)n, 0, 32, s);
+    CK(cudaMallocAsync(&tmp, tb, s));
+    cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys_in, keys_out, vals_in,
+                                              (uint32_t*)old_of_new, (int)n, 0, 32, s);
+    CK(cudaGetLastError());
+    k_invert<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const uint32_t*)old_of_new, n, new_of_old);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, s));
+    CK(cudaFreeAsync(keys_out, s));
+    CK(cudaFreeAsync(vals_in, s));
+    CK(cudaFreeAsync(deg, s));
+    CK(cudaFreeAsync(d_kept, s));
+    CK(cudaStreamSynchronize(s));
+    return n;
 }
 
 }  // extern "C"

@@ -22,22 +22,43 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Address-range policy: the first `hot` bytes of [base, base + total) evict-last, the rest
+// evict-first (vertex arrays whose ids are sorted by descending degree keep their hot prefix).
+__device__ __forceinline__ uint64_t policy_range(const void* base, uint32_t hot, uint32_t total) {
+    uint64_t p;
+    asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+                 : "=l"(p) : "l"(base), "r"(hot), "r"(total));
+    return p;
+}
+// Gather policy selector (tuning knob, IPREGEL_GATHER_POLICY): 0 evict_normal, 1 evict_last,
+// 2 evict_first, 3 range (hot prefix evict_last).
+__device__ __forceinline__ uint64_t policy_for(int mode, const void* base = nullptr,
+                                               uint32_t hot = 0, uint32_t total = 0) {
+    if (mode == 3 && base) return policy_range(base, hot < total ? hot : total, total);
+    return mode == 1 ? policy_evict_last() : (mode == 2 ? policy_evict_first() : policy_evict_normal());
+}
+
 // Streamed (read-once) loads: non-coherent path, no L1 allocation, L2 evict-first.
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
     int32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
                  : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
     uint32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
                  : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {
     int4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
     return r;
 }
@@ -46,12 +67,12 @@ __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {
 // explicit L2 policy.
 __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
     double r;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ uint32_t ld_gather(const uint32_t* p, uint64_t pol) {
     uint32_t r;
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 
@@ -65,5 +86,7 @@ template <class T>
 __device__ __forceinline__ T shfl_up(T v, int d) { return __shfl_up_sync(kFull, v, d); }
 template <class T>
 __device__ __forceinline__ T shfl_xor(T v, int d) { return __shfl_xor_sync(kFull, v, d); }
+template <class T>
+__device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(kFull, v, src); }
 
 }  // namespace ipr

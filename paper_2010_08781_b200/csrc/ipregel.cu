@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -72,6 +73,19 @@ std::atomic<unsigned long long> g_launches{0};
         g_launches.fetch_add(1, std::memory_order_relaxed); \
         CU(cudaGetLastError());                          \
     } while (0)
+
+// Tuning knob read once per process: L2 policy of the pull gathers (default evict_last).
+int read_gather_policy() {
+    const char* e = getenv("IPREGEL_GATHER_POLICY");
+    return e ? atoi(e) : 1;
+}
+int g_gather_policy = read_gather_policy();
+// Hot-prefix bytes kept evict-last under policy 3 (IPREGEL_HOT_BYTES, default 64 MiB).
+uint64_t read_hot_bytes() {
+    const char* e = getenv("IPREGEL_HOT_BYTES");
+    return e ? strtoull(e, nullptr, 10) : (64ull << 20);
+}
+uint64_t g_hot_bytes = read_hot_bytes();
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline unsigned grid_for(int64_t n, int threads) {
@@ -196,33 +210,47 @@ void check_device(int device) {
              device, prop.major, prop.minor);
 }
 
-void build_plan(TilePlan& P, const int32_t* off, int64_t rows, int64_t edges, int64_t diag0,
+void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint32_t* w,
+                int64_t rows, int64_t edges, int64_t vertex_base, int64_t edge_base,
                 DeviceBuffers& mem, cudaStream_t s) {
     P.rows = (int32_t)rows;
     P.edges = edges;
-    P.phase = diag0 % kPullItems;
-    const int64_t total = rows + edges;
-    P.num_tiles = rows > 0 ? (int32_t)ceil_div(total + P.phase, kPullItems) : 0;
+    // ranges on the global merge grid (diagonal = global row + global edge index), chunks on the
+    // global 128-edge grid
+    P.phase = (vertex_base + edge_base) % kRangeItems;
+    P.cphase = edge_base % kChunk;
+    P.num_tiles = rows > 0 ? (int32_t)ceil_div(rows + edges + P.phase, kRangeItems) : 0;
+    // 16-byte chunk loads need (pointer - 4 * edge_base) 16-byte aligned
+    auto al = [&](const void* ptr) {
+        return ptr == nullptr || ((uintptr_t)ptr - 4 * (uintptr_t)edge_base) % 16 == 0;
+    };
+    P.aligned = al(idx) && al(w);
     if (P.num_tiles == 0) return;
-    P.cx = mem.alloc<int32_t>(P.num_tiles + 1, s);
-    P.cy = mem.alloc<int32_t>(P.num_tiles + 1, s);
-    P.carry = mem.alloc<double>(P.num_tiles, s);   // 8-byte slots hold f64 or u32
-    P.head = mem.alloc<double>(P.num_tiles, s);
-    k_plan_boundaries<<<grid_for(P.num_tiles + 1, 256), 256, 0, s>>>(off, P.rows, edges, P.phase,
-                                                                      P.num_tiles, P.cx, P.cy);
+    const int32_t Q = P.num_tiles;
+    P.cx = mem.alloc<int32_t>(Q + 1, s);
+    P.cy = mem.alloc<int32_t>(Q + 1, s);
+    P.carry = mem.alloc<double>(Q, s);   // 8-byte slots hold f64 or u32
+    P.head = mem.alloc<double>(Q, s);
+    k_plan_boundaries<<<grid_for(Q + 1, 256), 256, 0, s>>>(off, P.rows, edges, P.phase, Q, P.cx,
+                                                           P.cy);
     LAUNCH_CHECK();
-    // Spanning rows: boundary b in [1, T-1] carries row cx[b]; consecutive boundaries with the
-    // same row form one group (row, a, b).  Host pass at create time (not timed).
-    std::vector<int32_t> cx(P.num_tiles + 1);
-    CU(cudaMemcpyAsync(cx.data(), P.cx, cx.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    // Rows cut by range boundaries: consecutive boundaries carrying the same row form one group
+    // (row, a, b).  Host pass at create time (not timed).
+    DeviceBuffers tmp;
+    int32_t* infl = tmp.alloc<int32_t>(Q, s);
+    k_plan_inflight<<<grid_for(Q, 256), 256, 0, s>>>(off, P.cx, P.cy, P.rows, Q, infl);
+    LAUNCH_CHECK();
+    std::vector<int32_t> h(Q);
+    CU(cudaMemcpyAsync(h.data(), infl, Q * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    tmp.release();
     std::vector<int4> groups;
-    for (int32_t b = 1; b < P.num_tiles; ++b) {
-        if (cx[b] >= rows) continue;
-        if (!groups.empty() && groups.back().x == cx[b] && groups.back().z == b - 1)
+    for (int32_t b = 1; b < Q; ++b) {
+        if (h[b] < 0) continue;
+        if (!groups.empty() && groups.back().x == h[b] && groups.back().z == b - 1)
             groups.back().z = b;
         else
-            groups.push_back(make_int4(cx[b], b, b, 0));
+            groups.push_back(make_int4(h[b], b, b, 0));
     }
     P.num_groups = (int32_t)groups.size();
     if (P.num_groups) {
@@ -235,12 +263,22 @@ void build_plan(TilePlan& P, const int32_t* off, int64_t rows, int64_t edges, in
 
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
-                 PullCounters* cnt, cudaStream_t s) {
+                 const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
-    k_pull_tiles<Op><<<P.num_tiles, kPullThreads, 0, s>>>(op, off, idx, P.cx, P.cy, P.rows,
-                                                          P.phase, static_cast<T*>(P.carry),
-                                                          static_cast<T*>(P.head), cnt);
+    const unsigned grid = (unsigned)ceil_div(P.num_tiles, kWarpsPerCta);
+    const uint64_t total = std::min<uint64_t>((uint64_t)n_global * sizeof(T), 0xFFFFFFFFull);
+    const uint32_t hot = (uint32_t)std::min<uint64_t>(g_hot_bytes, total);
+    if (P.aligned)
+        k_pull_ranges<Op, true><<<grid, kPullThreads, 0, s>>>(
+            op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
+            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, g_gather_policy,
+            op.gather_base(), hot, (uint32_t)total);
+    else
+        k_pull_ranges<Op, false><<<grid, kPullThreads, 0, s>>>(
+            op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
+            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, g_gather_policy,
+            op.gather_base(), hot, (uint32_t)total);
     LAUNCH_CHECK();
     if (P.num_groups) {
         k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
@@ -635,7 +673,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.ratio = ratio;
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
-                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, s);
+                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n);
             } else {
                 k_expand<0><<<1184, kExpandThreads, 0, s>>>(
                     p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -795,16 +833,16 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 if (cc) {
                     CCPullIn a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, s);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n);
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
-                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, p.pull_cnt, s);
+                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n);
                 } else {
                     SSSPPull a;
-                    a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.in_w = p.csc_w;
+                    a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.pull_cnt, s);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n);
                 }
             }
             T.kend();
@@ -924,10 +962,10 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
 
 void build_plans(ipregel_graph* g) {
     for (auto& p : g->parts) {
-        build_plan(p.plan_csc, p.csc_off, p.rows, p.csc_edges, p.vb + p.csc_ebase, p.graph_mem,
-                   g->stream);
-        build_plan(p.plan_csr, p.csr_off, p.rows, p.csr_edges, p.vb + p.csr_ebase, p.graph_mem,
-                   g->stream);
+        build_plan(p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.rows, p.csc_edges, p.vb,
+                   p.csc_ebase, p.graph_mem, g->stream);
+        build_plan(p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.rows, p.csr_edges, p.vb,
+                   p.csr_ebase, p.graph_mem, g->stream);
     }
     CU(cudaStreamSynchronize(g->stream));
 }

@@ -5,66 +5,87 @@
 // previous superstep's value array (double-buffered, BSP isolation PAPER.md:151, :239), and one
 // superstep's gather + combine + compute of all recipients is ONE kernel over the in-adjacency.
 //
-// Work decomposition (B200-first, not the paper's OpenMP static schedule PAPER.md:155-157):
-// an edge-balanced "merge path" over the two sorted lists {row ends} and {edges}.  Every CTA
-// consumes exactly kItems = rows + edges merge items, so hub rows (in-degree ~1.5M at scale 26)
-// and the ~40% of rows with tiny or zero in-degree are balanced alike, with no degree binning
-// pass.  Per tile:
-//   1. coalesced, vectorised, L2-evict-first loads of the tile's column indices; the gathered
-//      outbox values are issued in one burst (8 independent loads per thread) and staged in
-//      shared memory with the tile's row ends;
-//   2. every thread walks kIPT consecutive merge items out of shared memory, combining edges
-//      and finishing rows;
-//   3. rows cut by thread boundaries are joined by a block-wide segmented scan (fixed tree);
-//      rows cut by tile boundaries are joined by pull_fixup in a fixed order.
-// The combine order therefore depends only on global merge coordinates: tile boundaries are
-// multiples of kItems in GLOBAL diagonal space, so PageRank is bit-identical for any
-// destination partition.
+// Work decomposition (B200-first; the paper's OpenMP static vertex split, is
+// prior art): the merge of the two sorted lists {row ends} and {in-edges} is cut into fixed
+// RANGES of kRangeItems items (merge path), one warp each, so every warp gets the same number of
+// edges + rows whatever the degree distribution (hub rows of in-degree ~1.5M at scale 26, long
+// runs of rows without in-edges) -- no degree binning pass, no shared-memory staging, no block
+// barrier.  A warp walks the edges of its range in CHUNKS of 128 (4 per lane):
+//   1. column indices arrive with 16-byte L2-evict-first loads two chunks ahead and the outbox
+//      values are gathered one chunk ahead (software pipeline, 8 gathers in flight per lane);
+//   2. a chunk inside one row (most edges: long rows) only adds into lane-private accumulators;
+//   3. a chunk where rows end builds a 128-bit head-flag mask from the CSC offsets
+//      (__reduce_or_sync), folds with a segmented scan (4 sequential adds per lane + a 5-step
+//      shuffle scan across lanes), and each row ending there reads its sum from a per-warp slot
+//      array and runs the recipient compute (fused epilogue);
+//   4. a row cut by a range boundary is joined by k_pull_fixup in a fixed order.
+// Range boundaries sit at multiples of kRangeItems in GLOBAL merge coordinates and chunks at
+// multiples of 128 GLOBAL edge positions, so every row's combine tree depends on global positions
+// only: PageRank is bit-identical for any destination partition.
 #pragma once
+#include <climits>
 #include "common.cuh"
 
 namespace ipr {
 
-constexpr int kPullThreads = 256;
-constexpr int kPullIPT = 8;
-constexpr int kPullItems = kPullThreads * kPullIPT;
+constexpr int kPullThreads = 256;                 // 8 warps per CTA
+constexpr int kWarpsPerCta = kPullThreads / 32;
+constexpr int kChunk = 128;                       // edges per warp step
+constexpr int kRangeItems = 4096;                 // merge items (edges + rows) per warp range
 
 struct PullCounters {
     unsigned long long changed;
     unsigned long long messages;
 };
 
-// Tile plan for one adjacency of one partition: merge coordinates of every tile boundary.
+// Range plan for one adjacency of one partition.
 struct TilePlan {
     int32_t rows = 0;
     int64_t edges = 0;
-    int64_t phase = 0;       // (global diagonal of local diagonal 0) mod kPullItems
-    int32_t num_tiles = 0;
-    int32_t* cx = nullptr;   // [num_tiles + 1] rows consumed at each boundary (local)
-    int32_t* cy = nullptr;   // [num_tiles + 1] edges consumed at each boundary (local)
+    int64_t phase = 0;        // (global merge diagonal of local diagonal 0) mod kRangeItems
+    int64_t cphase = 0;       // (global edge index of local edge 0) mod kChunk
+    int32_t num_tiles = 0;    // ranges
+    int32_t* cx = nullptr;    // [num_tiles + 1] rows finished before each range boundary
+    int32_t* cy = nullptr;    // [num_tiles + 1] edges consumed before each range boundary
     int32_t num_groups = 0;
-    int4* groups = nullptr;  // spanning rows: (row, first boundary a, last boundary b, 0)
-    void* carry = nullptr;   // [num_tiles] partial of the row leaving the tile (8-byte slots)
-    void* head = nullptr;    // [num_tiles] partial of the row entering and ending in the tile
+    int4* groups = nullptr;   // rows cut by range boundaries: (row, first boundary a, last b, 0)
+    void* carry = nullptr;    // [num_tiles] partial of the row leaving the range (8-byte slots)
+    void* head = nullptr;     // [num_tiles] partial of the row entering and ending in the range
+    bool aligned = false;     // 16-byte chunk loads possible
 };
 
-// Boundary b of the plan: local diagonal clamp(b * kItems - phase, 0, rows + edges), and its
-// merge coordinate via binary search (A[i] = end offset of row i, B[j] = j).
+// Range boundary b: local diagonal clamp(b * kRangeItems - phase, 0, rows + edges) and its merge
+// coordinate (rows finished, edges consumed) by binary search (A[i] = end of row i, B[j] = j).
 __global__ void k_plan_boundaries(const int32_t* __restrict__ off, int32_t rows, int64_t edges,
-                                  int64_t phase, int32_t num_tiles, int32_t* cx, int32_t* cy) {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b > num_tiles) return;
-    int64_t total = (int64_t)rows + edges;
-    int64_t d = b * (int64_t)kPullItems - phase;
+                                  int64_t phase, int32_t num_ranges, int32_t* __restrict__ cx,
+                                  int32_t* __restrict__ cy) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > num_ranges) return;
+    const int64_t total = (int64_t)rows + edges;
+    int64_t d = b * (int64_t)kRangeItems - phase;
     d = d < 0 ? 0 : (d > total ? total : d);
     int64_t lo = d - edges > 0 ? d - edges : 0;
     int64_t hi = d < rows ? d : rows;
     while (lo < hi) {
-        int64_t p = (lo + hi) >> 1;
-        if ((int64_t)off[p + 1] <= d - p - 1) lo = p + 1; else hi = p;
+        const int64_t m = (lo + hi) >> 1;
+        if ((int64_t)off[m + 1] <= d - m - 1) lo = m + 1; else hi = m;
     }
     cx[b] = (int32_t)lo;
     cy[b] = (int32_t)(d - lo);
+}
+
+// Row in flight at range boundary b (has edges on both sides' merge order), or -1.
+__global__ void k_plan_inflight(const int32_t* __restrict__ off, const int32_t* __restrict__ cx,
+                                const int32_t* __restrict__ cy, int32_t rows, int32_t num_ranges,
+                                int32_t* __restrict__ infl) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= num_ranges) return;
+    int32_t v = -1;
+    if (b >= 1) {
+        const int32_t r = cx[b];
+        if (r < rows && off[r] < cy[b]) v = r;
+    }
+    infl[b] = v;
 }
 
 // ---- combine policies -------------------------------------------------------------------------
@@ -79,10 +100,12 @@ struct MinU32 {
     __device__ static T combine(T a, T b) { return a > b ? b : a; }   // Fig. 5 ip_combine
 };
 
-// ---- vertex programs (gather = message on an in-edge, finish = recipient compute) ----------
+// ---- vertex programs: gather = outbox value of the sender, message = value on the edge,
+// finish = recipient compute --------------------------------------------------------------------
 // PageRank, Fig. 8: the message of u is contrib[u] = r_u / outdeg(u); recipient compute is
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
 struct PageRankPull : SumF64 {
+    static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
     double* __restrict__ rank;                // owned, local ids (written when write_rank)
@@ -91,14 +114,14 @@ struct PageRankPull : SumF64 {
     double ratio;
     int broadcast;                            // s < k
     int write_rank;
-    __device__ T gather(int64_t /*e*/, int32_t u, uint64_t /*ps*/, uint64_t pol) const {
-        return ld_gather(contrib_cur + u, pol);
-    }
-    __device__ void finish(int32_t row, T sum, PullCounters& /*c*/) const {
-        double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
+    const void* gather_base() const { return contrib_cur; }
+    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(contrib_cur + u, pol); }
+    __device__ static T message(T g, uint32_t) { return g; }
+    __device__ void finish(int32_t row, T sum, PullCounters&) const {
+        const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
         if (write_rank) rank[row] = r;
         if (broadcast) {
-            int32_t deg = out_off[row + 1] - out_off[row];
+            const int32_t deg = out_off[row + 1] - out_off[row];
             contrib_next[vbase + row] = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
         }
     }
@@ -106,14 +129,15 @@ struct PageRankPull : SumF64 {
 
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
 struct CCPullIn : MinU32 {
+    static constexpr bool kWeighted = false;
     const uint32_t* __restrict__ cur;   // replica, global ids
     uint32_t* __restrict__ next;        // replica, global ids (owned slice written)
     int64_t vbase;
-    __device__ T gather(int64_t, int32_t u, uint64_t, uint64_t pol) const {
-        return ld_gather(cur + u, pol);
-    }
+    const void* gather_base() const { return cur; }
+    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters&) const {
-        uint32_t c = cur[vbase + row];
+        const uint32_t c = cur[vbase + row];
         next[vbase + row] = m < c ? m : c;
     }
 };
@@ -121,16 +145,17 @@ struct CCPullIn : MinU32 {
 // Hash-Min CC, second half: min over the CSR row (the symmetrised graph's reverse edges), then
 // "if value < old: broadcast" -> changed / messages counters (degree in the symmetrised graph).
 struct CCPullOut : MinU32 {
+    static constexpr bool kWeighted = false;
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
     const int32_t* __restrict__ in_off;   // owned CSC offsets
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
-    __device__ T gather(int64_t, int32_t u, uint64_t, uint64_t pol) const {
-        return ld_gather(cur + u, pol);
-    }
+    const void* gather_base() const { return cur; }
+    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
-        uint32_t old = cur[vbase + row];
+        const uint32_t old = cur[vbase + row];
         uint32_t v = next[vbase + row];
         v = m < v ? m : v;
         next[vbase + row] = v;
@@ -145,18 +170,17 @@ struct CCPullOut : MinU32 {
 // SSSP, Fig. 10 with weights: message on edge (u -> v, w) is sat(dist_u + w), applied at the
 // recipient from the CSC weight (reading R8); "if mindist < value: broadcast".
 struct SSSPPull : MinU32 {
+    static constexpr bool kWeighted = true;
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
-    const uint32_t* __restrict__ in_w;    // owned CSC weights or NULL (= 1)
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
-    __device__ T gather(int64_t e, int32_t u, uint64_t ps, uint64_t pol) const {
-        uint32_t w = in_w ? ld_stream(in_w + e, ps) : 1u;
-        return sat_add(ld_gather(cur + u, pol), w);
-    }
+    const void* gather_base() const { return cur; }
+    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ static T message(T g, uint32_t w) { return sat_add(g, w); }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
-        uint32_t old = cur[vbase + row];
-        uint32_t v = m < old ? m : old;
+        const uint32_t old = cur[vbase + row];
+        const uint32_t v = m < old ? m : old;
         next[vbase + row] = v;
         if (v < old) {
             c.changed += 1;
@@ -165,148 +189,230 @@ struct SSSPPull : MinU32 {
     }
 };
 
-// ---- block-wide segmented inclusive scan (flag = a row ended inside this thread) ----------
-template <class Op>
-__device__ __forceinline__ void block_seg_scan(int& flag, typename Op::T& val,
-                                               typename Op::T* s_wval, int* s_wflag) {
-    using T = typename Op::T;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ---- one warp, one range -----------------------------------------------------------------------
+struct ChunkLoad {
+    int4 idx;      // column indices of the lane's 4 edges (-1 = outside the partition)
+    uint4 w;       // weights (SSSP; 1 otherwise)
+};
+
+template <bool kWeighted, bool kAligned>
+__device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
+                                                const uint32_t* __restrict__ wts, int32_t e0,
+                                                int32_t lo, int32_t hi, int lane, uint64_t pol) {
+    ChunkLoad L;
+    const int32_t e = e0 + 4 * lane;
+    if (kAligned && e >= lo && e + 4 <= hi) {
+        L.idx = ld_stream4(reinterpret_cast<const int4*>(idx + e), pol);
+        if (kWeighted && wts) {
+            const int4 t = ld_stream4(reinterpret_cast<const int4*>(wts + e), pol);
+            L.w = make_uint4((uint32_t)t.x, (uint32_t)t.y, (uint32_t)t.z, (uint32_t)t.w);
+        } else {
+            L.w = make_uint4(1u, 1u, 1u, 1u);
+        }
+    } else {
+        int v[4];
+        uint32_t ww[4];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        T vp = shfl_up(val, d);
-        int fp = shfl_up(flag, d);
-        if (lane >= d) {
-            if (!flag) val = Op::combine(vp, val);
-            flag |= fp;
+        for (int j = 0; j < 4; ++j) {
+            const bool in = e + j >= lo && e + j < hi;
+            v[j] = in ? ld_stream(idx + e + j, pol) : -1;
+            ww[j] = (kWeighted && in && wts) ? ld_stream(wts + e + j, pol) : 1u;
         }
+        L.idx = make_int4(v[0], v[1], v[2], v[3]);
+        L.w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
     }
-    if (lane == 31) { s_wval[warp] = val; s_wflag[warp] = flag; }
-    __syncthreads();
-    if (warp > 0 && !flag) {
-        // exclusive segmented prefix over the preceding warps, nearest first
-        T pre = s_wval[warp - 1];
-        int pf = s_wflag[warp - 1];
-        for (int w = warp - 2; w >= 0 && !pf; --w) {
-            pre = Op::combine(s_wval[w], pre);
-            pf = s_wflag[w];
-        }
-        val = Op::combine(pre, val);
-    }
+    return L;
 }
 
-// One tile per CTA.  tile_base = local tile index; thread j's local diagonal is
-// tile * kItems - phase + j * kIPT clamped to the tile.
 template <class Op>
-__global__ void __launch_bounds__(kPullThreads)
-k_pull_tiles(Op op, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-             const int32_t* __restrict__ cx, const int32_t* __restrict__ cy, int32_t rows,
-             int64_t phase, typename Op::T* __restrict__ carry, typename Op::T* __restrict__ head,
-             PullCounters* __restrict__ counters) {
+__device__ __forceinline__ void gather_chunk(const Op& op, const ChunkLoad& L,
+                                             typename Op::T (&g)[4], uint64_t pol) {
+    g[0] = L.idx.x >= 0 ? op.gather(L.idx.x, pol) : Op::identity();
+    g[1] = L.idx.y >= 0 ? op.gather(L.idx.y, pol) : Op::identity();
+    g[2] = L.idx.z >= 0 ? op.gather(L.idx.z, pol) : Op::identity();
+    g[3] = L.idx.w >= 0 ? op.gather(L.idx.w, pol) : Op::identity();
+}
+
+template <class Op, bool kAligned>
+__global__ void __launch_bounds__(kPullThreads, 4)
+k_pull_ranges(Op op, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+              const uint32_t* __restrict__ wts, const int32_t* __restrict__ cx,
+              const int32_t* __restrict__ cy, int32_t rows, int32_t cphase, int32_t num_ranges,
+              typename Op::T* __restrict__ carry_out, typename Op::T* __restrict__ head_out,
+              PullCounters* __restrict__ counters, int gather_policy, const void* gbase,
+              uint32_t ghot, uint32_t gtotal) {
     using T = typename Op::T;
-    __shared__ T s_val[kPullItems];
-    __shared__ int32_t s_end[kPullItems + 1];
-    __shared__ T s_scan[kPullThreads];
-    __shared__ T s_wval[kPullThreads / 32];
-    __shared__ int s_wflag[kPullThreads / 32];
+    __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums, slot-major (conflict-free)
     __shared__ unsigned long long s_cnt[2];
-
-    const int tile = blockIdx.x;
-    const int32_t x0 = cx[tile], y0 = cy[tile], x1 = cx[tile + 1], y1 = cy[tile + 1];
-    const int n_ends = x1 - x0;             // rows finished in this tile
-    const int n_edges = y1 - y0;
-    const int n_a = (x1 < rows ? x1 : rows - 1) - x0 + 1;  // row-end entries staged
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_gather = policy_evict_last();
-
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
     if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
-    for (int i = threadIdx.x; i < n_a; i += kPullThreads) s_end[i] = off[x0 + i + 1] - y0;
-
-    // Column indices: scalar head up to 16-byte alignment, then int4 loads.
-    {
-        const int32_t* base = idx + y0;
-        int head_n = (int)((16 - ((uintptr_t)base & 15)) & 15) >> 2;
-        if (head_n > n_edges) head_n = n_edges;
-        for (int i = threadIdx.x; i < head_n; i += kPullThreads)
-            s_val[i] = op.gather((int64_t)y0 + i, ld_stream(base + i, pol_stream), pol_stream, pol_gather);
-        const int n_vec = (n_edges - head_n) >> 2;
-        const int4* vbase = reinterpret_cast<const int4*>(base + head_n);
-        for (int q = threadIdx.x; q < n_vec; q += kPullThreads) {
-            int4 u = ld_stream4(vbase + q, pol_stream);
-            int i = head_n + 4 * q;
-            T a = op.gather((int64_t)y0 + i, u.x, pol_stream, pol_gather);
-            T b = op.gather((int64_t)y0 + i + 1, u.y, pol_stream, pol_gather);
-            T c = op.gather((int64_t)y0 + i + 2, u.z, pol_stream, pol_gather);
-            T d = op.gather((int64_t)y0 + i + 3, u.w, pol_stream, pol_gather);
-            s_val[i] = a; s_val[i + 1] = b; s_val[i + 2] = c; s_val[i + 3] = d;
-        }
-        for (int i = head_n + 4 * n_vec + threadIdx.x; i < n_edges; i += kPullThreads)
-            s_val[i] = op.gather((int64_t)y0 + i, ld_stream(base + i, pol_stream), pol_stream, pol_gather);
-    }
     __syncthreads();
-
-    // This thread's merge range.
-    const int tile_items = n_ends + n_edges;
-    int64_t lo_g = (int64_t)tile * kPullItems - phase;          // local diag of the tile grid
-    int64_t tile_lo = (int64_t)x0 + y0;                         // clamped tile start (local)
-    int d0 = (int)(lo_g + (int64_t)threadIdx.x * kPullIPT - tile_lo);
-    d0 = d0 < 0 ? 0 : (d0 > tile_items ? tile_items : d0);
-    int d1 = (int)(lo_g + (int64_t)(threadIdx.x + 1) * kPullIPT - tile_lo);
-    d1 = d1 < 0 ? 0 : (d1 > tile_items ? tile_items : d1);
-
-    int lo = d0 - n_edges > 0 ? d0 - n_edges : 0;
-    int hi = d0 < n_ends ? d0 : n_ends;
-    while (lo < hi) {
-        int p = (lo + hi) >> 1;
-        if (s_end[p] <= d0 - p - 1) lo = p + 1; else hi = p;
-    }
-    int x = lo, y = d0 - lo;
 
     PullCounters cnt{0, 0};
-    T acc = Op::identity();
-    T head_part = Op::identity();
-    int emitted = 0;
+    if (q < num_ranges) {
+        const uint64_t pol_s = policy_evict_first();
+        const uint64_t pol_g = policy_for(gather_policy, gbase, ghot, gtotal);
+        const int32_t x1 = cx[q + 1], y0 = cy[q], y1 = cy[q + 1];
+        int32_t r = cx[q];                       // next row to finish
+        // the row entering the range with edges before it is finished by k_pull_fixup
+        int32_t Bc = r < rows ? off[r] : y1;     // first edge of row r
+        int32_t Ec = r < rows ? off[r + 1] : y1; // end of row r
+        const int32_t defer = (q > 0 && r < rows && Bc < y0) ? r : -1;
+        T carry = Op::identity();                // partial of row r from earlier slow chunks
+        T la = Op::identity();                   // lane-private partial of row r (fast chunks)
+        T* my_sum = s_sum[wid];
+        // chunks on the global 128-edge grid covering [y0, y1)
+        const int32_t c0 = y0 - ((y0 + cphase) & (kChunk - 1));
+
+        ChunkLoad Lc = load_chunk<Op::kWeighted, kAligned>(idx, wts, c0, y0, y1, lane, pol_s);
+        ChunkLoad Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, c0 + kChunk, y0, y1, lane,
+                                                           pol_s);
+        T gc[4];
+        gather_chunk(op, Lc, gc, pol_g);
+
+        for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
+            T gn[4];
+            gather_chunk(op, Ln, gn, pol_g);
+            const uint4 wc = Lc.w;
+            Lc = Ln;
+            Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, e0 + 2 * kChunk, y0, y1, lane,
+                                                     pol_s);
+            T v0 = Op::message(gc[0], wc.x), v1 = Op::message(gc[1], wc.y);
+            T v2 = Op::message(gc[2], wc.z), v3 = Op::message(gc[3], wc.w);
 #pragma unroll
-    for (int k = 0; k < kPullIPT; ++k) {
-        if (d0 + k < d1) {
-            if (y < s_end[x]) {
-                acc = Op::combine(acc, s_val[y]);
-                ++y;
-            } else {
-                if (!emitted) head_part = acc;
-                else op.finish(x0 + x, acc, cnt);
-                emitted = 1;
-                acc = Op::identity();
-                ++x;
+            for (int j = 0; j < 4; ++j) gc[j] = gn[j];
+
+            // The partition's first chunk when its first edge is not on the 128-edge grid: on
+            // one GPU the previous partition's last row ends there, so it takes the slow path
+            // with a segment head at the partition start (same combine tree for any partition).
+            const bool part_head = e0 < 0;
+            if (!part_head && (r >= x1 || Ec > e0 + kChunk)) {
+                // fast path: the whole chunk belongs to row r (no row ends here)
+                la = Op::combine(la, Op::combine(Op::combine(v0, v1), Op::combine(v2, v3)));
+                continue;
             }
-        }
-    }
-    // Segmented scan of the tail partials; S_j = partial of the row leaving thread j.
-    int flag = emitted;
-    T val = acc;
-    block_seg_scan<Op>(flag, val, s_wval, s_wflag);
-    s_scan[threadIdx.x] = val;
-    __syncthreads();
+            // slow path: rows end in this chunk.  Fold the lane partials of row r first.
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const T o = shfl_xor(la, d);
+                la = (lane & d) ? Op::combine(o, la) : Op::combine(la, o);
+            }
+            carry = Op::combine(carry, la);
+            la = Op::identity();
 
-    if (emitted) {
-        const int first_row = lo;  // the thread's start row is the first one it finishes
-        T v = threadIdx.x > 0 ? Op::combine(s_scan[threadIdx.x - 1], head_part) : head_part;
-        if (first_row == 0 && tile > 0) {
-            // The row entering the tile is cut by boundary `tile`: pull_fixup finishes it.
-            head[tile] = v;
-        } else {
-            op.finish(x0 + first_row, v, cnt);
-        }
-    }
-    if (threadIdx.x == kPullThreads - 1) carry[tile] = val;
+            // head flags of rows ending at chunk position p in [1,127]; n_emit rows end here
+            uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+            int32_t n_emit = 0;
+            int32_t E0 = 0;   // window 0's row end for this lane (reused by the emission)
+            for (int32_t rw = r;; rw += 32) {
+                const int32_t row = rw + lane;
+                const int32_t E = row < x1 ? off[row + 1] : INT_MAX;
+                if (rw == r) E0 = E;
+                const int32_t p = E == INT_MAX ? INT_MAX : E - e0;
+                const bool fl = p >= 1 && p <= 127;
+                const uint32_t bit = fl ? 1u << (p & 31) : 0u;
+                const int word = fl ? (p >> 5) : -1;
+                f0 |= __reduce_or_sync(kFull, word == 0 ? bit : 0u);
+                f1 |= __reduce_or_sync(kFull, word == 1 ? bit : 0u);
+                f2 |= __reduce_or_sync(kFull, word == 2 ? bit : 0u);
+                f3 |= __reduce_or_sync(kFull, word == 3 ? bit : 0u);
+                const int n = __popc(__ballot_sync(kFull, p <= kChunk));
+                n_emit += n;
+                if (n < 32) break;
+            }
+            if (part_head) {
+                const int p = -e0;   // in [1, 127]
+                const uint32_t bit = 1u << (p & 31);
+                if ((p >> 5) == 0) f0 |= bit; else if ((p >> 5) == 1) f1 |= bit;
+                else if ((p >> 5) == 2) f2 |= bit; else f3 |= bit;
+            }
+            const int sel = lane >> 3;
+            const uint32_t fw = sel == 0 ? f0 : (sel == 1 ? f1 : (sel == 2 ? f2 : f3));
+            const uint32_t fl4 = (fw >> ((4 * lane) & 31)) & 0xFu;
 
-    // Counters: warp reduce, then one shared atomic per warp, one global atomic per CTA.
+            // segmented scan: sequential within the lane (carry enters lane 0's first segment)
+            if (lane == 0 && !(fl4 & 1u)) v0 = Op::combine(carry, v0);
+            v1 = (fl4 & 2u) ? v1 : Op::combine(v0, v1);
+            v2 = (fl4 & 4u) ? v2 : Op::combine(v1, v2);
+            v3 = (fl4 & 8u) ? v3 : Op::combine(v2, v3);
+            T tail = v3;
+            int hf = fl4 != 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const T tp = shfl_up(tail, d);
+                const int hp = shfl_up(hf, d);
+                if (lane >= d) {
+                    if (!hf) tail = Op::combine(tp, tail);
+                    hf |= hp;
+                }
+            }
+            const T pre = shfl_up(tail, 1);
+            if (lane > 0 && !(fl4 & 1u)) {
+                v0 = Op::combine(pre, v0);
+                if (!(fl4 & 2u)) {
+                    v1 = Op::combine(pre, v1);
+                    if (!(fl4 & 4u)) {
+                        v2 = Op::combine(pre, v2);
+                        if (!(fl4 & 8u)) v3 = Op::combine(pre, v3);
+                    }
+                }
+            }
+            my_sum[0 * 32 + lane] = v0;
+            my_sum[1 * 32 + lane] = v1;
+            my_sum[2 * 32 + lane] = v2;
+            my_sum[3 * 32 + lane] = v3;
+            T next_carry = shfl_idx(tail, 31);
+            __syncwarp();
+
+            // emit every row ending here: sum = S(p - 1); rows without in-edges get identity
+            bool ended_at_end = false;
+            for (int32_t k = 0; k < n_emit; k += 32) {
+                const int32_t row = r + k + lane;
+                const int32_t E = k == 0 ? E0 : (row < x1 ? off[row + 1] : INT_MAX);
+                int32_t B = shfl_up(E, 1);
+                const int32_t Bw = k == 0 ? Bc : off[r + k];   // start of the window's first row
+                if (lane == 0) B = Bw;
+                if (k + lane < n_emit) {
+                    T val = Op::identity();
+                    if (B < E) {
+                        const int pos = E - e0 - 1;
+                        val = pos >= 0 ? my_sum[(pos & 3) * 32 + (pos >> 2)] : carry;
+                        if (E - e0 == kChunk) ended_at_end = true;
+                    }
+                    if (row == defer) head_out[q] = val;
+                    else op.finish(row, val, cnt);
+                }
+            }
+            r += n_emit;
+            Bc = r < rows ? off[r] : y1;
+            Ec = r < rows ? off[r + 1] : y1;
+            if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
+            carry = next_carry;
+            __syncwarp();
+        }
+        // rows finished after the last edge of the range (rows without in-edges)
+        for (int32_t row = r + lane; row < x1; row += 32) {
+            if (row == defer) head_out[q] = Op::identity();
+            else op.finish(row, Op::identity(), cnt);
+        }
+        // partial of the row leaving the range
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const T o = shfl_xor(la, d);
+            la = (lane & d) ? Op::combine(o, la) : Op::combine(la, o);
+        }
+        if (lane == 0) carry_out[q] = Op::combine(carry, la);
+    }
+
+    // counters: warp reduce, one shared atomic per warp, one global atomic per CTA
     unsigned long long c0 = cnt.changed, c1 = cnt.messages;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         c0 += __shfl_xor_sync(kFull, c0, d);
         c1 += __shfl_xor_sync(kFull, c1, d);
     }
-    if ((threadIdx.x & 31) == 0 && (c0 | c1)) {
+    if (lane == 0 && (c0 | c1)) {
         atomicAdd(&s_cnt[0], c0);
         atomicAdd(&s_cnt[1], c1);
     }
@@ -317,7 +423,7 @@ k_pull_tiles(Op op, const int32_t* __restrict__ off, const int32_t* __restrict__
     }
 }
 
-// Rows cut by tile boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
+// Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
 // carry[a-1] (+) carry[a] (+) ... (+) carry[b-1] (+) head[b], folded in a fixed order
 // (lane-strided partials, then a fixed xor tree).  One warp per spanning row.
 template <class Op>
@@ -334,7 +440,7 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     for (int t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        T o = shfl_xor(acc, d);
+        const T o = shfl_xor(acc, d);
         acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
     }
     if (lane == 0) {
