@@ -129,6 +129,17 @@ typedef struct {
     const uint32_t* csr_weights;/* [csr_edges] or NULL                                          */
     int32_t memory;             /* ipregel_memory                                               */
     int32_t validate;           /* 1: O(E) device validation during create (INVALID_GRAPH)      */
+    /* Optional internal vertex layout.  vertex_ids[v] = ORIGINAL id of internal vertex v (a
+     * permutation of [0, N), the full array on every partition; device or host per `memory`), or
+     * NULL for the identity.  With it, Hash-Min labels are original ids, sssp_source is an
+     * original id and ipregel_get_values returns values indexed by original id, so results equal
+     * those on the original numbering (the layout only changes memory locality).            */
+    const int32_t* vertex_ids;
+    /* 1: internal ids ascend by decreasing out-degree (e.g. vertex_ids from a degree sort).  The
+     * pull gathers then keep the hot prefix of the outbox arrays L2-resident (evict-last address
+     * range policy) and stream the rest.                                                       */
+    int32_t degree_ordered;
+    int32_t reserved;           /* must be 0                                                    */
 } ipregel_graph_desc;
 
 typedef struct {

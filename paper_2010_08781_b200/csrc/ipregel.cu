@@ -74,10 +74,11 @@ std::atomic<unsigned long long> g_launches{0};
         CU(cudaGetLastError());                          \
     } while (0)
 
-// Tuning knob read once per process: L2 policy of the pull gathers (default evict_last).
+// Tuning knob read once per process: L2 policy of the pull gathers (-1 = per graph: range policy
+// for degree-ordered layouts, else evict_last).
 int read_gather_policy() {
     const char* e = getenv("IPREGEL_GATHER_POLICY");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : -1;
 }
 int g_gather_policy = read_gather_policy();
 // Hot-prefix bytes kept evict-last under policy 3 (IPREGEL_HOT_BYTES, default 64 MiB).
@@ -192,7 +193,12 @@ struct ipregel_graph {
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
-    double* gather_tmp = nullptr;  // multi-GPU get_values scratch
+    double* gather_tmp = nullptr;  // get_values scratch (full vector, internal order)
+    double* gather_tmp2 = nullptr; // get_values scratch (original order)
+    const int32_t* vertex_ids = nullptr;  // internal -> original id, or NULL
+    bool degree_ordered = false;
+    int gather_policy = 1;
+    DeviceBuffers graph_mem;       // graph-level copies (vertex_ids from host)
 };
 
 // =============================================================================================
@@ -263,7 +269,8 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
 
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
-                 const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global) {
+                 const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global,
+                 int policy) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
     const unsigned grid = (unsigned)ceil_div(P.num_tiles, kWarpsPerCta);
@@ -272,12 +279,12 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
     if (P.aligned)
         k_pull_ranges<Op, true><<<grid, kPullThreads, 0, s>>>(
             op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
-            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, g_gather_policy,
+            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
             op.gather_base(), hot, (uint32_t)total);
     else
         k_pull_ranges<Op, false><<<grid, kPullThreads, 0, s>>>(
             op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
-            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, g_gather_policy,
+            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
             op.gather_base(), hot, (uint32_t)total);
     LAUNCH_CHECK();
     if (P.num_groups) {
@@ -673,7 +680,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.ratio = ratio;
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
-                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n);
+                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy);
             } else {
                 k_expand<0><<<1184, kExpandThreads, 0, s>>>(
                     p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -717,6 +724,20 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     const uint64_t pull_edges = cc ? 2ull * (uint64_t)g->e : (uint64_t)g->e;
 
     for (auto& p : g->parts) ensure_push_view(g, p);
+    // SSSP_SOURCE is an original id; find its internal id under a relabelled layout
+    int64_t source = (int64_t)P.sssp_source;
+    if (!cc && g->vertex_ids) {
+        Partition& p0 = g->parts[0];
+        const unsigned long long none = ~0ull;
+        CU(cudaMemcpyAsync(p0.dscratch + 32, &none, 8, cudaMemcpyHostToDevice, s));
+        k_find_index<<<std::min<unsigned>(grid_for(n, 256), 4096), 256, 0, s>>>(
+            g->vertex_ids, n, (int32_t)P.sssp_source, p0.dscratch + 32);
+        LAUNCH_CHECK();
+        CU(cudaMemcpyAsync(p0.host_cnt + 15, p0.dscratch + 32, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        source = (int64_t)p0.host_cnt[15];
+        if (source < 0 || source >= n) fail(IPREGEL_ERR_INVALID_GRAPH, "vertex_ids is not a permutation");
+    }
 
     // ---------------- superstep 0
     g->steps.assign(1, StepRecord{});
@@ -725,8 +746,8 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     T0.kbegin();
     for (auto& p : g->parts) {
         AppState& S = p.st[app];
-        if (cc) k_init_cc<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n);
-        else k_init_sssp<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, (int64_t)P.sssp_source);
+        if (cc) k_init_cc<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, g->vertex_ids);
+        else k_init_sssp<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, source);
         LAUNCH_CHECK();
     }
     T0.kend();
@@ -739,8 +760,8 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
         // the source's broadcast: its frontier entry and out-degree come from the compaction
         for (auto& p : g->parts) {
             AppState& S = p.st[app];
-            if ((int64_t)P.sssp_source >= p.vb && (int64_t)P.sssp_source < p.ve) {
-                k_set_bit<<<1, 1, 0, s>>>(S.bits, (int64_t)P.sssp_source - p.vb);
+            if (source >= p.vb && source < p.ve) {
+                k_set_bit<<<1, 1, 0, s>>>(S.bits, source - p.vb);
                 LAUNCH_CHECK();
             }
             compact_bitmap(g, p, S, S.val[0], false);
@@ -833,16 +854,16 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 if (cc) {
                     CCPullIn a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy);
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
-                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n);
+                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n, g->gather_policy);
                 } else {
                     SSSPPull a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n, g->gather_policy);
                 }
             }
             T.kend();
@@ -891,6 +912,9 @@ void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "csc_weights and csr_weights must both be set or NULL");
     if (d->memory != IPREGEL_MEMORY_DEVICE && d->memory != IPREGEL_MEMORY_HOST)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown memory kind %d", d->memory);
+    if (d->reserved != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "reserved must be 0");
+    if (d->degree_ordered != 0 && d->degree_ordered != 1)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "degree_ordered must be 0 or 1");
     if ((d->vertex_end - d->vertex_begin) + std::max(d->csc_edges, d->csr_edges) > 2147483647LL)
         fail(IPREGEL_ERR_UNSUPPORTED, "rows + edges of a partition beyond int32 merge coordinates");
     *n_out = d->num_vertices;
@@ -981,6 +1005,8 @@ void destroy_graph(ipregel_graph* g) {
     }
     for (auto e : g->events) cudaEventDestroy(e);
     if (g->gather_tmp) cudaFree(g->gather_tmp);
+    if (g->gather_tmp2) cudaFree(g->gather_tmp2);
+    g->graph_mem.release();
     delete g;
 }
 
@@ -1186,6 +1212,34 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
             }
             if (expect != n) fail(IPREGEL_ERR_INVALID_ARGUMENT, "rank ranges do not cover [0, N)");
         }
+        for (int i = 0; i < np; ++i) {
+            if ((descs[i].vertex_ids == nullptr) != (descs[0].vertex_ids == nullptr) ||
+                descs[i].degree_ordered != descs[0].degree_ordered)
+                fail(IPREGEL_ERR_INVALID_ARGUMENT, "partitions disagree on the vertex layout");
+        }
+        g->degree_ordered = descs[0].degree_ordered != 0;
+        g->gather_policy = g_gather_policy >= 0 ? g_gather_policy : (g->degree_ordered ? 3 : 1);
+        if (descs[0].vertex_ids) {
+            if (descs[0].memory == IPREGEL_MEMORY_HOST) {
+                int32_t* d = g->graph_mem.alloc<int32_t>(n, g->stream);
+                CU(cudaMemcpyAsync(d, descs[0].vertex_ids, n * 4, cudaMemcpyHostToDevice, g->stream));
+                g->vertex_ids = d;
+            } else {
+                g->vertex_ids = descs[0].vertex_ids;
+            }
+            if (descs[0].validate) {
+                DeviceBuffers tmp;
+                int32_t* seen = tmp.alloc<int32_t>(n, g->stream, true);
+                unsigned* flags = tmp.alloc<unsigned>(1, g->stream, true);
+                k_count_ids<<<grid_for(n, 256), 256, 0, g->stream>>>(g->vertex_ids, n, seen, flags);
+                LAUNCH_CHECK();
+                unsigned h = 0;
+                CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, g->stream));
+                CU(cudaStreamSynchronize(g->stream));
+                tmp.release();
+                if (h) fail(IPREGEL_ERR_INVALID_GRAPH, "vertex_ids is not a permutation of [0, N)");
+            }
+        }
         for (int i = 0; i < np; ++i) init_partition(g, g->parts[i], descs[i]);
         build_plans(g);
     } catch (...) {
@@ -1282,29 +1336,38 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
     cudaStream_t s = g->stream;
     const cudaMemcpyKind kind = out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     try {
+        // full N-vector in internal order (device)
+        const void* full = nullptr;
         if (pr) {
-            if (multi_rank(g)) {
-                if (!g->gather_tmp) CU(cudaMalloc(&g->gather_tmp, g->n * sizeof(double)));
-                Partition& p = g->parts[0];
+            if (!g->gather_tmp) CU(cudaMalloc(&g->gather_tmp, g->n * sizeof(double)));
+            for (auto& p : g->parts)
                 if (p.rows)
                     CU(cudaMemcpyAsync(g->gather_tmp + p.vb, p.st[0].rank, p.rows * 8,
                                        cudaMemcpyDeviceToDevice, s));
+            if (multi_rank(g)) {
                 NC(ncclGroupStart());
                 for (int r = 0; r < g->comm->world; ++r)
                     if (g->rank_rows[r])
                         NC(ncclBroadcast(g->gather_tmp + g->rank_vb[r], g->gather_tmp + g->rank_vb[r],
                                          (size_t)g->rank_rows[r], ncclFloat64, r, g->comm->nccl, s));
                 NC(ncclGroupEnd());
-                CU(cudaMemcpyAsync(out, g->gather_tmp, g->n * 8, kind, s));
-            } else {
-                for (auto& p : g->parts)
-                    if (p.rows)
-                        CU(cudaMemcpyAsync((double*)out + p.vb, p.st[0].rank, p.rows * 8, kind, s));
             }
+            full = g->gather_tmp;
         } else {
-            Partition& p = g->parts[0];
-            CU(cudaMemcpyAsync(out, p.st[g->last_app].val[g->cur], g->n * 4, kind, s));
+            full = g->parts[0].st[g->last_app].val[g->cur];
         }
+        if (g->vertex_ids) {
+            if (!g->gather_tmp2) CU(cudaMalloc(&g->gather_tmp2, g->n * sizeof(double)));
+            if (pr)
+                k_to_original<double><<<grid_for(g->n, 256), 256, 0, s>>>(
+                    (const double*)full, g->vertex_ids, g->n, g->gather_tmp2);
+            else
+                k_to_original<uint32_t><<<grid_for(g->n, 256), 256, 0, s>>>(
+                    (const uint32_t*)full, g->vertex_ids, g->n, (uint32_t*)g->gather_tmp2);
+            LAUNCH_CHECK();
+            full = g->gather_tmp2;
+        }
+        CU(cudaMemcpyAsync(out, full, g->n * esz, kind, s));
         CU(cudaStreamSynchronize(s));
     } catch (const Failure& f) {
         if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;

@@ -20,10 +20,36 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
     }
 }
 
-// Hash-Min CC, Fig. 9: value = id (every replica initialises all N locally -- no exchange).
-__global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n) {
+// Hash-Min CC, Fig. 9: value = id, the ORIGINAL id under a relabelled layout (every replica
+// initialises all N locally -- no exchange).
+__global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n, const int32_t* __restrict__ ids) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) val[i] = (uint32_t)i;
+    if (i < n) val[i] = ids ? (uint32_t)ids[i] : (uint32_t)i;
+}
+
+// internal id of original vertex `orig` (vertex_ids is a permutation)
+__global__ void k_find_index(const int32_t* __restrict__ ids, int64_t n, int32_t orig,
+                             unsigned long long* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (ids[i] == orig) *out = (unsigned long long)i;
+}
+
+// out[ids[i]] = in[i]: values in internal order -> original order
+template <class T>
+__global__ void k_to_original(const T* __restrict__ in, const int32_t* __restrict__ ids, int64_t n,
+                              T* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[ids[i]] = in[i];
+}
+
+// permutation check: every id in [0, n) exactly once
+__global__ void k_count_ids(const int32_t* __restrict__ ids, int64_t n, int32_t* __restrict__ seen,
+                            unsigned* __restrict__ flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t v = ids[i];
+    if (v < 0 || (int64_t)v >= n || atomicAdd(seen + v, 1) != 0) atomicOr(flags, 8u);
 }
 
 // SSSP, Fig. 10: source = 0, everyone else INF.

@@ -53,6 +53,8 @@ class GraphDesc(ctypes.Structure):
         ("csr_offsets", ctypes.c_void_p), ("csr_indices", ctypes.c_void_p),
         ("csr_weights", ctypes.c_void_p),
         ("memory", ctypes.c_int32), ("validate", ctypes.c_int32),
+        ("vertex_ids", ctypes.c_void_p), ("degree_ordered", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -229,6 +231,8 @@ class Partition:
     csr_indices: object
     csc_weights: object = None
     csr_weights: object = None
+    vertex_ids: object = None        # original id of each internal vertex (full [N]) or None
+    degree_ordered: bool = False
 
     def desc(self, validate: bool = False) -> GraphDesc:
         host = isinstance(self.csc_offsets, np.ndarray)
@@ -247,6 +251,9 @@ class Partition:
         d.csr_weights = _ptr(self.csr_weights)
         d.memory = MEMORY_HOST if host else MEMORY_DEVICE
         d.validate = 1 if validate else 0
+        d.vertex_ids = _ptr(self.vertex_ids)
+        d.degree_ordered = 1 if self.degree_ordered else 0
+        d.reserved = 0
         return d
 
 
@@ -346,14 +353,15 @@ class Graph:
 
 
 def full_partition(n: int, e: int, csc_offsets, csc_indices, csr_offsets, csr_indices,
-                   csc_weights=None, csr_weights=None) -> Partition:
+                   csc_weights=None, csr_weights=None, vertex_ids=None,
+                   degree_ordered=False) -> Partition:
     """The whole graph as one partition (single GPU)."""
     return Partition(n, e, 0, n, csc_offsets, csc_indices, csr_offsets, csr_indices,
-                     csc_weights, csr_weights)
+                     csc_weights, csr_weights, vertex_ids, degree_ordered)
 
 
 def split_partitions(n: int, e: int, bounds, csc_offsets, csc_indices, csr_offsets, csr_indices,
-                     csc_weights=None, csr_weights=None):
+                     csc_weights=None, csr_weights=None, vertex_ids=None, degree_ordered=False):
     """Slice a full CSC/CSR (torch CUDA tensors) into destination ranges `bounds` (rebased
     offsets; index/weight arrays are views, not copies).  Create-time plumbing only."""
     parts = []
@@ -366,7 +374,7 @@ def split_partitions(n: int, e: int, bounds, csc_offsets, csc_indices, csr_offse
             (csc_offsets[vb:ve + 1] - cb).contiguous(), csc_indices[cb:ce],
             (csr_offsets[vb:ve + 1] - rb).contiguous(), csr_indices[rb:re_],
             None if csc_weights is None else csc_weights[cb:ce],
-            None if csr_weights is None else csr_weights[rb:re_]))
+            None if csr_weights is None else csr_weights[rb:re_], vertex_ids, degree_ordered))
     return parts
 
 

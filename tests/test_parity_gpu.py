@@ -313,3 +313,93 @@ def test_loopback_with_empty_partition():
         G.run(app)
     o = oracle.sssp(n, src, src + 1, None)
     np.testing.assert_array_equal(G.values(host=True), o["values"])
+
+
+# ------------------------------------------------------------------ internal vertex layouts
+
+def _permuted(n, src, dst, w, perm):
+    """Graph arrays with internal id perm[v] for original vertex v; vertex_ids = inverse."""
+    g = csr_csc(n, perm[src], perm[dst], w)
+    inv = np.empty(n, np.int32)
+    inv[perm] = np.arange(n, dtype=np.int32)
+    g["vertex_ids"] = inv
+    return g
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_relabelled_layout_matches_oracle(seed):
+    import torch
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.integers(2, 4000))
+    src, dst, w = checkers.random_graph(rng, n, 6 * n, weighted=True)
+    perm = rng.permutation(n).astype(np.int64)
+    g = _permuted(n, src, dst, w, perm)
+    d = to_device(g)
+    ids = torch.from_numpy(g["vertex_ids"]).cuda()
+    source = int(rng.integers(0, n))
+    for parts in (1, 3):
+        if parts == 1:
+            P = ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"], d["csr_idx"],
+                                   d["csc_w"], d["csr_w"], vertex_ids=ids,
+                                   degree_ordered=bool(seed % 2))
+            G = ipr.Graph(P, validate=True)
+        else:
+            b = ipr.edge_balanced_bounds(g["csc_off"], parts, g["csr_off"])
+            G = ipr.Graph(ipr.split_partitions(n, d["e"], b, d["csc_off"], d["csc_idx"],
+                                               d["csr_off"], d["csr_idx"], d["csc_w"], d["csr_w"],
+                                               vertex_ids=ids, degree_ordered=bool(seed % 2)))
+        for mode in ("pull", "push", "auto"):
+            o = oracle.hashmin_cc(n, src, dst)
+            G.run("cc", mode=mode)
+            np.testing.assert_array_equal(G.values(host=True), o["values"])
+            np.testing.assert_array_equal(G.stats()["messages"], o["messages"])
+            o = oracle.sssp(n, src, dst, w, source=source)
+            G.run("sssp", mode=mode, source=source)
+            np.testing.assert_array_equal(G.values(host=True), o["values"])
+            np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
+        o = oracle.pagerank(n, src, dst)
+        G.run("pagerank", mode="pull")
+        assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
+        G.close()
+
+
+def test_vertex_ids_must_be_a_permutation():
+    import torch
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    g = csr_csc(5, [0, 1, 2], [1, 2, 3])
+    d = to_device(g)
+    bad = torch.tensor([0, 1, 1, 3, 4], dtype=torch.int32, device="cuda")
+    P = ipr.full_partition(5, 3, d["csc_off"], d["csc_idx"], d["csr_off"], d["csr_idx"],
+                           vertex_ids=bad)
+    with pytest.raises(ipr.IpregelError) as e:
+        ipr.Graph(P, validate=True)
+    assert e.value.status == ipr.ERR_INVALID_GRAPH
+
+
+def test_gpu_fixture_degree_order_matches_cpu_coo():
+    # the degree-ordered device layout is the same graph: results equal the oracle's on the COO
+    import inputs
+    import paper_2010_08781_b200 as ipr
+    from inputs.gpu import config_graph_device
+    cfg = inputs.Config("t", "all", 13, 16, 21, True)
+    src, dst, w = inputs.rmat_coo(cfg.scale, cfg.edgefactor, cfg.seed, weighted=True)
+    for order in (False, True):
+        g = config_graph_device(cfg, degree_order=order)
+        assert g["e"] == len(src)
+        G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
+                                         g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
+                                         degree_ordered=order))
+        G.run("cc")
+        np.testing.assert_array_equal(G.values(host=True),
+                                      oracle.hashmin_cc(cfg.n, src, dst)["values"])
+        G.run("sssp")
+        np.testing.assert_array_equal(G.values(host=True),
+                                      oracle.sssp(cfg.n, src, dst, w)["values"])
+        G.run("pagerank", mode="pull")
+        assert np.abs(G.values(host=True) - oracle.pagerank(cfg.n, src, dst)["values"]).max() < 1e-12
+        if order:
+            deg = g["csr_off"].diff().cpu().numpy()
+            assert np.all(np.diff(deg) <= 0)  # internal ids ascend by decreasing out-degree
