@@ -37,8 +37,8 @@ METRIC = "GTEPS per superstep and % of HBM roofline at 1/2/4/8 B200"
 UNIT = "GTEPS"
 APP_CODES = {"pagerank": 0, "cc": 1, "sssp": 2}
 # bounded sample of the cfg4 workload for the oracle: same generator and parameters
-# (a, b, c, d, edgefactor 28, seed 5), 1/64 of the vertices
-SAMPLE_SCALE = 20
+# (a, b, c, d, edgefactor 28, seed 5), 1/16 of the vertices (~10-30 s of one core)
+SAMPLE_SCALE = 22
 
 
 def log(*a):
@@ -113,7 +113,8 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """Per-launch DRAM bytes of the PageRank pull kernel from the committed ncu summary."""
+    """Per-launch DRAM bytes (read + write) of the PageRank pull kernel from the committed
+    `ncu --set full` capture summary (profiles/pr_pull_ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "pr_pull_ncu_summary.json")
     try:
         with open(p) as f:
@@ -136,24 +137,27 @@ def build_graph_device(cfg_name, rank, world):
     from inputs.gpu import config_graph_device
     cfg = inputs.CONFIGS[cfg_name]
     t = time.time()
-    g = config_graph_device(cfg, weighted=True)
+    g = config_graph_device(cfg, weighted=True, degree_order=True)
     torch.cuda.synchronize()
     log(f"[rank {rank}] graph {cfg_name}: N={g['n']} E={g['e']} built in {time.time() - t:.1f}s")
     if world == 1:
         part = ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
-                                  g["csr_idx"], g["csc_w"], g["csr_w"])
+                                  g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
+                                  degree_ordered=True)
         return g, part, np.array([0, g["n"]])
     bounds = ipr.edge_balanced_bounds(g["csc_off"].cpu().numpy(), world, g["csr_off"].cpu().numpy())
     parts = ipr.split_partitions(g["n"], g["e"], bounds, g["csc_off"], g["csc_idx"], g["csr_off"],
-                                 g["csr_idx"], g["csc_w"], g["csr_w"])
+                                 g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
+                                 degree_ordered=True)
     # keep only this rank's slices alive (copies, so the full graph can be freed)
     p = parts[rank]
     own = ipr.Partition(p.num_vertices, p.num_edges, p.vertex_begin, p.vertex_end,
                         p.csc_offsets.clone(), p.csc_indices.clone(), p.csr_offsets.clone(),
-                        p.csr_indices.clone(), p.csc_weights.clone(), p.csr_weights.clone())
+                        p.csr_indices.clone(), p.csc_weights.clone(), p.csr_weights.clone(),
+                        g["vertex_ids"], True)
     del parts
     for k in list(g.keys()):
-        if k not in ("n", "e"):
+        if k not in ("n", "e", "vertex_ids"):
             g[k] = None
     torch.cuda.empty_cache()
     return g, own, bounds
@@ -320,7 +324,7 @@ def main():
             achieved = float(np.mean(mb) / (float(t.item()) * 1e-3) / 1e9)  # per-rank bytes
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(),
-                "kernel": "k_pull_tiles<PageRankPull> + k_pull_fixup",
+                "kernel": "k_pull_ranges<PageRankPull> + k_pull_fixup",
                 "bytes_per_launch": float(np.mean(mb)),
                 "model": "12 B/edge (4 B index + 8 B gathered f64 outbox) + 16 B/vertex",
                 "avg_launch_ms": float(np.mean(k_ms)), "peak_source": peak_src,
@@ -341,6 +345,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
         "config": {"workload": f"{args.config}: R-MAT scale 26 ef 28 seed 5, "
                                f"{'+'.join(args.apps)} per step",
+                   "layout": "degree-ordered internal ids (results in original ids)",
                    "n": n, "e": e, "parallelism": f"1D destination partition x{world}",
                    "l2": "inputs larger than L2 (7.5 GB per adjacency array), no flush",
                    "apps": apps_out},
@@ -368,7 +373,7 @@ def e2e_measure(g, args, msgs_per_step, stream):
     import paper_2010_08781_b200 as ipr
     host = {}
     h2d = 0
-    for k in ("csc_off", "csc_idx", "csc_w", "csr_off", "csr_idx", "csr_w"):
+    for k in ("csc_off", "csc_idx", "csc_w", "csr_off", "csr_idx", "csr_w", "vertex_ids"):
         t = g[k]
         if t is None:
             continue
@@ -377,7 +382,8 @@ def e2e_measure(g, args, msgs_per_step, stream):
         host[k] = h.numpy()
         h2d += h.numel() * h.element_size()
     part = ipr.full_partition(g["n"], g["e"], host["csc_off"], host["csc_idx"], host["csr_off"],
-                              host["csr_idx"], host["csc_w"], host["csr_w"])
+                              host["csr_idx"], host["csc_w"], host["csr_w"], host["vertex_ids"],
+                              degree_ordered=True)
     out_pr = torch.empty(g["n"], dtype=torch.float64, pin_memory=True)
     out_u = torch.empty(g["n"], dtype=torch.int32, pin_memory=True)
     d2h = 0

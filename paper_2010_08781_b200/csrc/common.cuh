@@ -76,6 +76,24 @@ __device__ __forceinline__ uint32_t ld_gather(const uint32_t* p, uint64_t pol) {
     return r;
 }
 
+// Gather with an L1 choice: hot (L1 evict-last) or cold (no L1 allocation) per lane.
+__device__ __forceinline__ double ld_gather_l1(const double* p, uint64_t pol, int hot) {
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+        "@q ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;\n\t"
+        "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n\t}"
+        : "=d"(r) : "l"(p), "l"(pol), "r"(hot));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_gather_l1(const uint32_t* p, uint64_t pol, int hot) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+        "@q ld.global.nc.L1::evict_last.L2::cache_hint.u32 %0, [%1], %2;\n\t"
+        "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n\t}"
+        : "=r"(r) : "l"(p), "l"(pol), "r"(hot));
+    return r;
+}
+
 // Saturating u32 add: INF + w = INF (reading R9).
 __device__ __forceinline__ uint32_t sat_add(uint32_t a, uint32_t b) {
     uint32_t s = a + b;

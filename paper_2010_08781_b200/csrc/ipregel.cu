@@ -87,6 +87,11 @@ uint64_t read_hot_bytes() {
     return e ? strtoull(e, nullptr, 10) : (64ull << 20);
 }
 uint64_t g_hot_bytes = read_hot_bytes();
+// Tuning knobs: L1-cached hot vertices (IPREGEL_L1_HOT, -1 = default L1 policy) and an L2
+// persisting access-policy window over the hot prefix (IPREGEL_PERSIST_BYTES, 0 = off).
+int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -1;
+uint64_t g_persist_bytes =
+    getenv("IPREGEL_PERSIST_BYTES") ? strtoull(getenv("IPREGEL_PERSIST_BYTES"), nullptr, 10) : 0;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline unsigned grid_for(int64_t n, int threads) {
@@ -276,16 +281,30 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
     const unsigned grid = (unsigned)ceil_div(P.num_tiles, kWarpsPerCta);
     const uint64_t total = std::min<uint64_t>((uint64_t)n_global * sizeof(T), 0xFFFFFFFFull);
     const uint32_t hot = (uint32_t)std::min<uint64_t>(g_hot_bytes, total);
+    if (g_persist_bytes) {
+        static bool limit_set = false;
+        if (!limit_set) {
+            CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_persist_bytes));
+            limit_set = true;
+        }
+        cudaStreamAttrValue a = {};
+        a.accessPolicyWindow.base_ptr = const_cast<void*>(op.gather_base());
+        a.accessPolicyWindow.num_bytes = std::min<uint64_t>(g_persist_bytes, total);
+        a.accessPolicyWindow.hitRatio = 1.0f;
+        a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CU(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
+    }
     if (P.aligned)
         k_pull_ranges<Op, true><<<grid, kPullThreads, 0, s>>>(
             op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
             static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
-            op.gather_base(), hot, (uint32_t)total);
+            op.gather_base(), hot, (uint32_t)total, g_l1_hot);
     else
         k_pull_ranges<Op, false><<<grid, kPullThreads, 0, s>>>(
             op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
             static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
-            op.gather_base(), hot, (uint32_t)total);
+            op.gather_base(), hot, (uint32_t)total, g_l1_hot);
     LAUNCH_CHECK();
     if (P.num_groups) {
         k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(

@@ -115,7 +115,7 @@ struct PageRankPull : SumF64 {
     int broadcast;                            // s < k
     int write_rank;
     const void* gather_base() const { return contrib_cur; }
-    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(contrib_cur + u, pol); }
+    __device__ const T* gptr() const { return contrib_cur; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T sum, PullCounters&) const {
         const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
@@ -134,7 +134,7 @@ struct CCPullIn : MinU32 {
     uint32_t* __restrict__ next;        // replica, global ids (owned slice written)
     int64_t vbase;
     const void* gather_base() const { return cur; }
-    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ const T* gptr() const { return cur; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters&) const {
         const uint32_t c = cur[vbase + row];
@@ -152,7 +152,7 @@ struct CCPullOut : MinU32 {
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
     const void* gather_base() const { return cur; }
-    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ const T* gptr() const { return cur; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
         const uint32_t old = cur[vbase + row];
@@ -176,7 +176,7 @@ struct SSSPPull : MinU32 {
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
     const void* gather_base() const { return cur; }
-    __device__ T gather(int32_t u, uint64_t pol) const { return ld_gather(cur + u, pol); }
+    __device__ const T* gptr() const { return cur; }
     __device__ static T message(T g, uint32_t w) { return sat_add(g, w); }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
         const uint32_t old = cur[vbase + row];
@@ -224,13 +224,23 @@ __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
     return L;
 }
 
+// Outbox gathers.  l1hot < 0: default L1 allocation; else vertices below l1hot are cached in L1
+// (evict-last) and the rest bypass L1 (tuning knob IPREGEL_L1_HOT).
+template <class Op>
+__device__ __forceinline__ typename Op::T gather_one(const Op& op, int32_t u, uint64_t pol,
+                                                     int32_t l1hot) {
+    if (u < 0) return Op::identity();
+    if (l1hot < 0) return ld_gather(op.gptr() + u, pol);
+    return ld_gather_l1(op.gptr() + u, pol, u < l1hot);
+}
+
 template <class Op>
 __device__ __forceinline__ void gather_chunk(const Op& op, const ChunkLoad& L,
-                                             typename Op::T (&g)[4], uint64_t pol) {
-    g[0] = L.idx.x >= 0 ? op.gather(L.idx.x, pol) : Op::identity();
-    g[1] = L.idx.y >= 0 ? op.gather(L.idx.y, pol) : Op::identity();
-    g[2] = L.idx.z >= 0 ? op.gather(L.idx.z, pol) : Op::identity();
-    g[3] = L.idx.w >= 0 ? op.gather(L.idx.w, pol) : Op::identity();
+                                             typename Op::T (&g)[4], uint64_t pol, int32_t l1hot) {
+    g[0] = gather_one(op, L.idx.x, pol, l1hot);
+    g[1] = gather_one(op, L.idx.y, pol, l1hot);
+    g[2] = gather_one(op, L.idx.z, pol, l1hot);
+    g[3] = gather_one(op, L.idx.w, pol, l1hot);
 }
 
 template <class Op, bool kAligned>
@@ -240,7 +250,7 @@ k_pull_ranges(Op op, const int32_t* __restrict__ off, const int32_t* __restrict_
               const int32_t* __restrict__ cy, int32_t rows, int32_t cphase, int32_t num_ranges,
               typename Op::T* __restrict__ carry_out, typename Op::T* __restrict__ head_out,
               PullCounters* __restrict__ counters, int gather_policy, const void* gbase,
-              uint32_t ghot, uint32_t gtotal) {
+              uint32_t ghot, uint32_t gtotal, int32_t l1hot) {
     using T = typename Op::T;
     __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums, slot-major (conflict-free)
     __shared__ unsigned long long s_cnt[2];
@@ -269,11 +279,11 @@ k_pull_ranges(Op op, const int32_t* __restrict__ off, const int32_t* __restrict_
         ChunkLoad Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, c0 + kChunk, y0, y1, lane,
                                                            pol_s);
         T gc[4];
-        gather_chunk(op, Lc, gc, pol_g);
+        gather_chunk(op, Lc, gc, pol_g, l1hot);
 
         for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
             T gn[4];
-            gather_chunk(op, Ln, gn, pol_g);
+            gather_chunk(op, Ln, gn, pol_g, l1hot);
             const uint4 wc = Lc.w;
             Lc = Ln;
             Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, e0 + 2 * kChunk, y0, y1, lane,
