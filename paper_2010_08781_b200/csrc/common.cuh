@@ -94,6 +94,22 @@ __device__ __forceinline__ uint32_t ld_gather_l1(const uint32_t* p, uint64_t pol
     return r;
 }
 
+// Predicated gather (no branch): returns `fallback` bits when pred == 0.
+__device__ __forceinline__ double ld_gather_pred(const double* p, uint64_t pol, int pred) {
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tmov.b64 %0, 0;\n\t"
+        "@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n\t}"
+        : "=d"(r) : "l"(p), "l"(pol), "r"(pred));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_gather_pred(const uint32_t* p, uint64_t pol, int pred) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tmov.b32 %0, 0;\n\t"
+        "@q ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;\n\t}"
+        : "=r"(r) : "l"(p), "l"(pol), "r"(pred));
+    return r;
+}
+
 // Saturating u32 add: INF + w = INF (reading R9).
 __device__ __forceinline__ uint32_t sat_add(uint32_t a, uint32_t b) {
     uint32_t s = a + b;

@@ -89,7 +89,8 @@ uint64_t read_hot_bytes() {
 uint64_t g_hot_bytes = read_hot_bytes();
 // Tuning knobs: L1-cached hot vertices (IPREGEL_L1_HOT, -1 = default L1 policy) and an L2
 // persisting access-policy window over the hot prefix (IPREGEL_PERSIST_BYTES, 0 = off).
-int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -1;
+// -1 (default): 64 KiB worth of the hottest vertices for degree-ordered layouts, else off.
+int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -2;
 uint64_t g_persist_bytes =
     getenv("IPREGEL_PERSIST_BYTES") ? strtoull(getenv("IPREGEL_PERSIST_BYTES"), nullptr, 10) : 0;
 
@@ -231,11 +232,8 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
     P.phase = (vertex_base + edge_base) % kRangeItems;
     P.cphase = edge_base % kChunk;
     P.num_tiles = rows > 0 ? (int32_t)ceil_div(rows + edges + P.phase, kRangeItems) : 0;
-    // 16-byte chunk loads need (pointer - 4 * edge_base) 16-byte aligned
-    auto al = [&](const void* ptr) {
-        return ptr == nullptr || ((uintptr_t)ptr - 4 * (uintptr_t)edge_base) % 16 == 0;
-    };
-    P.aligned = al(idx) && al(w);
+    (void)idx;
+    (void)w;
     if (P.num_tiles == 0) return;
     const int32_t Q = P.num_tiles;
     P.cx = mem.alloc<int32_t>(Q + 1, s);
@@ -275,10 +273,9 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
                  const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global,
-                 int policy) {
+                 int policy, bool degree_ordered) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
-    const unsigned grid = (unsigned)ceil_div(P.num_tiles, kWarpsPerCta);
     const uint64_t total = std::min<uint64_t>((uint64_t)n_global * sizeof(T), 0xFFFFFFFFull);
     const uint32_t hot = (uint32_t)std::min<uint64_t>(g_hot_bytes, total);
     if (g_persist_bytes) {
@@ -295,16 +292,13 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
         a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         CU(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
     }
-    if (P.aligned)
-        k_pull_ranges<Op, true><<<grid, kPullThreads, 0, s>>>(
-            op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
-            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
-            op.gather_base(), hot, (uint32_t)total, g_l1_hot);
-    else
-        k_pull_ranges<Op, false><<<grid, kPullThreads, 0, s>>>(
-            op, off, idx, w, P.cx, P.cy, P.rows, (int32_t)P.cphase, P.num_tiles,
-            static_cast<T*>(P.carry), static_cast<T*>(P.head), cnt, policy,
-            op.gather_base(), hot, (uint32_t)total, g_l1_hot);
+    RangeArgs A;
+    A.off = off; A.idx = idx; A.wts = w; A.cx = P.cx; A.cy = P.cy; A.rows = P.rows;
+    A.cphase = (int32_t)P.cphase; A.num_ranges = P.num_tiles; A.carry_out = P.carry;
+    A.head_out = P.head; A.counters = cnt; A.gather_policy = policy; A.gbase = op.gather_base();
+    A.ghot = hot; A.gtotal = (uint32_t)total;
+    A.l1hot = g_l1_hot != -2 ? g_l1_hot : (degree_ordered ? (int32_t)(65536 / sizeof(T)) : -1);
+    k_pull_ranges<Op><<<(unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads, 0, s>>>(op, A);
     LAUNCH_CHECK();
     if (P.num_groups) {
         k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
@@ -699,7 +693,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.ratio = ratio;
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
-                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy);
+                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered);
             } else {
                 k_expand<0><<<1184, kExpandThreads, 0, s>>>(
                     p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -873,16 +867,16 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 if (cc) {
                     CCPullIn a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered);
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
-                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n, g->gather_policy);
+                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
                 } else {
                     SSSPPull a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n, g->gather_policy);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
                 }
             }
             T.kend();

@@ -11,12 +11,13 @@
 // edges + rows whatever the degree distribution (hub rows of in-degree ~1.5M at scale 26, long
 // runs of rows without in-edges) -- no degree binning pass, no shared-memory staging, no block
 // barrier.  A warp walks the edges of its range in CHUNKS of 128 (4 per lane):
-//   1. column indices arrive with 16-byte L2-evict-first loads two chunks ahead and the outbox
-//      values are gathered one chunk ahead (software pipeline, 8 gathers in flight per lane);
+//   1. column indices arrive with coalesced L2-evict-first loads two chunks ahead and the
+//      outbox values are gathered one chunk ahead (software pipeline, 8 gathers in flight per
+//      lane); each gather instruction reads the sources of 32 consecutive edges;
 //   2. a chunk inside one row (most edges: long rows) only adds into lane-private accumulators;
 //   3. a chunk where rows end builds a 128-bit head-flag mask from the CSC offsets
-//      (__reduce_or_sync), folds with a segmented scan (4 sequential adds per lane + a 5-step
-//      shuffle scan across lanes), and each row ending there reads its sum from a per-warp slot
+//      (__reduce_or_sync), folds it with four 5-step segmented shuffle scans (segment starts read
+//      off the uniform flag words), and each row ending there reads its sum from a per-warp slot
 //      array and runs the recipient compute (fused epilogue);
 //   4. a row cut by a range boundary is joined by k_pull_fixup in a fixed order.
 // Range boundaries sit at multiples of kRangeItems in GLOBAL merge coordinates and chunks at
@@ -28,6 +29,9 @@
 
 namespace ipr {
 
+#ifndef IPREGEL_PULL_MINBLOCKS
+#define IPREGEL_PULL_MINBLOCKS 4
+#endif
 constexpr int kPullThreads = 256;                 // 8 warps per CTA
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
@@ -51,7 +55,6 @@ struct TilePlan {
     int4* groups = nullptr;   // rows cut by range boundaries: (row, first boundary a, last b, 0)
     void* carry = nullptr;    // [num_tiles] partial of the row leaving the range (8-byte slots)
     void* head = nullptr;     // [num_tiles] partial of the row entering and ending in the range
-    bool aligned = false;     // 16-byte chunk loads possible
 };
 
 // Range boundary b: local diagonal clamp(b * kRangeItems - phase, 0, rows + edges) and its merge
@@ -190,36 +193,27 @@ struct SSSPPull : MinU32 {
 };
 
 // ---- one warp, one range -----------------------------------------------------------------------
+// A chunk is 128 consecutive edges on the global grid, held as 4 sub-chunks of 32: lane l owns
+// edges e0 + 32k + l (k = 0..3), so each gather instruction of the warp reads the sources of 32
+// CONSECUTIVE edges.  CSC rows list their sources in ascending order, so consecutive edges of a
+// row often share a 128-byte line and the coalescer merges their requests (the L1 -> L2 request
+// rate is what bounds this kernel; profiles/r01).
 struct ChunkLoad {
-    int4 idx;      // column indices of the lane's 4 edges (-1 = outside the partition)
-    uint4 w;       // weights (SSSP; 1 otherwise)
+    int32_t idx[4];   // column index of edge e0 + 32k + lane (-1 = outside the partition/range)
+    uint32_t w[4];    // weights (SSSP; 1 otherwise)
 };
 
-template <bool kWeighted, bool kAligned>
+template <bool kWeighted>
 __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
                                                 const uint32_t* __restrict__ wts, int32_t e0,
                                                 int32_t lo, int32_t hi, int lane, uint64_t pol) {
     ChunkLoad L;
-    const int32_t e = e0 + 4 * lane;
-    if (kAligned && e >= lo && e + 4 <= hi) {
-        L.idx = ld_stream4(reinterpret_cast<const int4*>(idx + e), pol);
-        if (kWeighted && wts) {
-            const int4 t = ld_stream4(reinterpret_cast<const int4*>(wts + e), pol);
-            L.w = make_uint4((uint32_t)t.x, (uint32_t)t.y, (uint32_t)t.z, (uint32_t)t.w);
-        } else {
-            L.w = make_uint4(1u, 1u, 1u, 1u);
-        }
-    } else {
-        int v[4];
-        uint32_t ww[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const bool in = e + j >= lo && e + j < hi;
-            v[j] = in ? ld_stream(idx + e + j, pol) : -1;
-            ww[j] = (kWeighted && in && wts) ? ld_stream(wts + e + j, pol) : 1u;
-        }
-        L.idx = make_int4(v[0], v[1], v[2], v[3]);
-        L.w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+    for (int k = 0; k < 4; ++k) {
+        const int32_t e = e0 + 32 * k + lane;
+        const bool in = e >= lo && e < hi;
+        L.idx[k] = in ? ld_stream(idx + e, pol) : -1;
+        L.w[k] = (kWeighted && in && wts) ? ld_stream(wts + e, pol) : 1u;
     }
     return L;
 }
@@ -237,185 +231,32 @@ __device__ __forceinline__ typename Op::T gather_one(const Op& op, int32_t u, ui
 template <class Op>
 __device__ __forceinline__ void gather_chunk(const Op& op, const ChunkLoad& L,
                                              typename Op::T (&g)[4], uint64_t pol, int32_t l1hot) {
-    g[0] = gather_one(op, L.idx.x, pol, l1hot);
-    g[1] = gather_one(op, L.idx.y, pol, l1hot);
-    g[2] = gather_one(op, L.idx.z, pol, l1hot);
-    g[3] = gather_one(op, L.idx.w, pol, l1hot);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g[k] = gather_one(op, L.idx[k], pol, l1hot);
 }
 
-template <class Op, bool kAligned>
-__global__ void __launch_bounds__(kPullThreads, 4)
-k_pull_ranges(Op op, const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-              const uint32_t* __restrict__ wts, const int32_t* __restrict__ cx,
-              const int32_t* __restrict__ cy, int32_t rows, int32_t cphase, int32_t num_ranges,
-              typename Op::T* __restrict__ carry_out, typename Op::T* __restrict__ head_out,
-              PullCounters* __restrict__ counters, int gather_policy, const void* gbase,
-              uint32_t ghot, uint32_t gtotal, int32_t l1hot) {
-    using T = typename Op::T;
-    __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums, slot-major (conflict-free)
-    __shared__ unsigned long long s_cnt[2];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
+struct RangeArgs {
+    const int32_t* off;
+    const int32_t* idx;
+    const uint32_t* wts;
+    const int32_t* cx;
+    const int32_t* cy;
+    int32_t rows;
+    int32_t cphase;
+    int32_t num_ranges;
+    void* carry_out;
+    void* head_out;
+    PullCounters* counters;
+    int gather_policy;
+    const void* gbase;
+    uint32_t ghot, gtotal;
+    int32_t l1hot;
+};
 
-    PullCounters cnt{0, 0};
-    if (q < num_ranges) {
-        const uint64_t pol_s = policy_evict_first();
-        const uint64_t pol_g = policy_for(gather_policy, gbase, ghot, gtotal);
-        const int32_t x1 = cx[q + 1], y0 = cy[q], y1 = cy[q + 1];
-        int32_t r = cx[q];                       // next row to finish
-        // the row entering the range with edges before it is finished by k_pull_fixup
-        int32_t Bc = r < rows ? off[r] : y1;     // first edge of row r
-        int32_t Ec = r < rows ? off[r + 1] : y1; // end of row r
-        const int32_t defer = (q > 0 && r < rows && Bc < y0) ? r : -1;
-        T carry = Op::identity();                // partial of row r from earlier slow chunks
-        T la = Op::identity();                   // lane-private partial of row r (fast chunks)
-        T* my_sum = s_sum[wid];
-        // chunks on the global 128-edge grid covering [y0, y1)
-        const int32_t c0 = y0 - ((y0 + cphase) & (kChunk - 1));
-
-        ChunkLoad Lc = load_chunk<Op::kWeighted, kAligned>(idx, wts, c0, y0, y1, lane, pol_s);
-        ChunkLoad Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, c0 + kChunk, y0, y1, lane,
-                                                           pol_s);
-        T gc[4];
-        gather_chunk(op, Lc, gc, pol_g, l1hot);
-
-        for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
-            T gn[4];
-            gather_chunk(op, Ln, gn, pol_g, l1hot);
-            const uint4 wc = Lc.w;
-            Lc = Ln;
-            Ln = load_chunk<Op::kWeighted, kAligned>(idx, wts, e0 + 2 * kChunk, y0, y1, lane,
-                                                     pol_s);
-            T v0 = Op::message(gc[0], wc.x), v1 = Op::message(gc[1], wc.y);
-            T v2 = Op::message(gc[2], wc.z), v3 = Op::message(gc[3], wc.w);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) gc[j] = gn[j];
-
-            // The partition's first chunk when its first edge is not on the 128-edge grid: on
-            // one GPU the previous partition's last row ends there, so it takes the slow path
-            // with a segment head at the partition start (same combine tree for any partition).
-            const bool part_head = e0 < 0;
-            if (!part_head && (r >= x1 || Ec > e0 + kChunk)) {
-                // fast path: the whole chunk belongs to row r (no row ends here)
-                la = Op::combine(la, Op::combine(Op::combine(v0, v1), Op::combine(v2, v3)));
-                continue;
-            }
-            // slow path: rows end in this chunk.  Fold the lane partials of row r first.
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const T o = shfl_xor(la, d);
-                la = (lane & d) ? Op::combine(o, la) : Op::combine(la, o);
-            }
-            carry = Op::combine(carry, la);
-            la = Op::identity();
-
-            // head flags of rows ending at chunk position p in [1,127]; n_emit rows end here
-            uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;
-            int32_t n_emit = 0;
-            int32_t E0 = 0;   // window 0's row end for this lane (reused by the emission)
-            for (int32_t rw = r;; rw += 32) {
-                const int32_t row = rw + lane;
-                const int32_t E = row < x1 ? off[row + 1] : INT_MAX;
-                if (rw == r) E0 = E;
-                const int32_t p = E == INT_MAX ? INT_MAX : E - e0;
-                const bool fl = p >= 1 && p <= 127;
-                const uint32_t bit = fl ? 1u << (p & 31) : 0u;
-                const int word = fl ? (p >> 5) : -1;
-                f0 |= __reduce_or_sync(kFull, word == 0 ? bit : 0u);
-                f1 |= __reduce_or_sync(kFull, word == 1 ? bit : 0u);
-                f2 |= __reduce_or_sync(kFull, word == 2 ? bit : 0u);
-                f3 |= __reduce_or_sync(kFull, word == 3 ? bit : 0u);
-                const int n = __popc(__ballot_sync(kFull, p <= kChunk));
-                n_emit += n;
-                if (n < 32) break;
-            }
-            if (part_head) {
-                const int p = -e0;   // in [1, 127]
-                const uint32_t bit = 1u << (p & 31);
-                if ((p >> 5) == 0) f0 |= bit; else if ((p >> 5) == 1) f1 |= bit;
-                else if ((p >> 5) == 2) f2 |= bit; else f3 |= bit;
-            }
-            const int sel = lane >> 3;
-            const uint32_t fw = sel == 0 ? f0 : (sel == 1 ? f1 : (sel == 2 ? f2 : f3));
-            const uint32_t fl4 = (fw >> ((4 * lane) & 31)) & 0xFu;
-
-            // segmented scan: sequential within the lane (carry enters lane 0's first segment)
-            if (lane == 0 && !(fl4 & 1u)) v0 = Op::combine(carry, v0);
-            v1 = (fl4 & 2u) ? v1 : Op::combine(v0, v1);
-            v2 = (fl4 & 4u) ? v2 : Op::combine(v1, v2);
-            v3 = (fl4 & 8u) ? v3 : Op::combine(v2, v3);
-            T tail = v3;
-            int hf = fl4 != 0;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const T tp = shfl_up(tail, d);
-                const int hp = shfl_up(hf, d);
-                if (lane >= d) {
-                    if (!hf) tail = Op::combine(tp, tail);
-                    hf |= hp;
-                }
-            }
-            const T pre = shfl_up(tail, 1);
-            if (lane > 0 && !(fl4 & 1u)) {
-                v0 = Op::combine(pre, v0);
-                if (!(fl4 & 2u)) {
-                    v1 = Op::combine(pre, v1);
-                    if (!(fl4 & 4u)) {
-                        v2 = Op::combine(pre, v2);
-                        if (!(fl4 & 8u)) v3 = Op::combine(pre, v3);
-                    }
-                }
-            }
-            my_sum[0 * 32 + lane] = v0;
-            my_sum[1 * 32 + lane] = v1;
-            my_sum[2 * 32 + lane] = v2;
-            my_sum[3 * 32 + lane] = v3;
-            T next_carry = shfl_idx(tail, 31);
-            __syncwarp();
-
-            // emit every row ending here: sum = S(p - 1); rows without in-edges get identity
-            bool ended_at_end = false;
-            for (int32_t k = 0; k < n_emit; k += 32) {
-                const int32_t row = r + k + lane;
-                const int32_t E = k == 0 ? E0 : (row < x1 ? off[row + 1] : INT_MAX);
-                int32_t B = shfl_up(E, 1);
-                const int32_t Bw = k == 0 ? Bc : off[r + k];   // start of the window's first row
-                if (lane == 0) B = Bw;
-                if (k + lane < n_emit) {
-                    T val = Op::identity();
-                    if (B < E) {
-                        const int pos = E - e0 - 1;
-                        val = pos >= 0 ? my_sum[(pos & 3) * 32 + (pos >> 2)] : carry;
-                        if (E - e0 == kChunk) ended_at_end = true;
-                    }
-                    if (row == defer) head_out[q] = val;
-                    else op.finish(row, val, cnt);
-                }
-            }
-            r += n_emit;
-            Bc = r < rows ? off[r] : y1;
-            Ec = r < rows ? off[r + 1] : y1;
-            if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
-            carry = next_carry;
-            __syncwarp();
-        }
-        // rows finished after the last edge of the range (rows without in-edges)
-        for (int32_t row = r + lane; row < x1; row += 32) {
-            if (row == defer) head_out[q] = Op::identity();
-            else op.finish(row, Op::identity(), cnt);
-        }
-        // partial of the row leaving the range
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const T o = shfl_xor(la, d);
-            la = (lane & d) ? Op::combine(o, la) : Op::combine(la, o);
-        }
-        if (lane == 0) carry_out[q] = Op::combine(carry, la);
-    }
-
-    // counters: warp reduce, one shared atomic per warp, one global atomic per CTA
+// counters: warp reduce, one shared atomic per warp, one global atomic per CTA
+__device__ __forceinline__ void flush_counters(const PullCounters& cnt, unsigned long long* s_cnt,
+                                               PullCounters* counters) {
+    const int lane = threadIdx.x & 31;
     unsigned long long c0 = cnt.changed, c1 = cnt.messages;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -431,6 +272,170 @@ k_pull_ranges(Op op, const int32_t* __restrict__ off, const int32_t* __restrict_
         atomicAdd(&counters->changed, s_cnt[0]);
         atomicAdd(&counters->messages, s_cnt[1]);
     }
+}
+
+// Fixed xor-tree reduction of a lane-private partial (result on every lane).
+template <class Op>
+__device__ __forceinline__ typename Op::T warp_fold(typename Op::T x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const typename Op::T o = shfl_xor(x, d);
+        x = (lane & d) ? Op::combine(o, x) : Op::combine(x, o);
+    }
+    return x;
+}
+
+// One warp, one range q (see the file header).  `my_sum` is the warp's 128-slot sum array.
+template <class Op>
+__device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int64_t q,
+                                           typename Op::T* my_sum, PullCounters& cnt) {
+    using T = typename Op::T;
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_g = policy_for(A.gather_policy, A.gbase, A.ghot, A.gtotal);
+    const int32_t x1 = A.cx[q + 1], y0 = A.cy[q], y1 = A.cy[q + 1];
+    int32_t r = A.cx[q];                           // next row to finish
+    int32_t Bc = r < A.rows ? A.off[r] : y1;       // first edge of row r
+    int32_t Ec = r < A.rows ? A.off[r + 1] : y1;   // end of row r
+    // the row entering the range with edges before it is finished by k_pull_fixup
+    const int32_t defer = (q > 0 && r < A.rows && Bc < y0) ? r : -1;
+    T carry = Op::identity();   // partial of row r from earlier slow chunks
+    T la = Op::identity();      // lane-private partial of row r from fast chunks
+    // chunks on the global 128-edge grid covering [y0, y1)
+    const int32_t c0 = y0 - ((y0 + A.cphase) & (kChunk - 1));
+
+    // software pipeline: indices two chunks ahead, gathered values one chunk ahead
+    ChunkLoad Lc = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
+    ChunkLoad Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
+    T gc[4];
+    gather_chunk(op, Lc, gc, pol_g, A.l1hot);
+
+#pragma unroll 2
+    for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
+        T gn[4];
+        gather_chunk(op, Ln, gn, pol_g, A.l1hot);
+        uint32_t wc[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wc[k] = Lc.w[k];
+        Lc = Ln;
+        Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 2 * kChunk, y0, y1, lane, pol_s);
+        T v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = Op::message(gc[k], wc[k]);
+            gc[k] = gn[k];
+        }
+
+        // The partition's first chunk when its first edge is not on the 128-edge grid: on one
+        // GPU the previous partition's last row ends there, so it takes the slow path with a
+        // segment head at the partition start (same combine tree for any partition).
+        const bool part_head = e0 < 0;
+        if (!part_head && (r >= x1 || Ec > e0 + kChunk)) {
+            // fast path: the whole chunk belongs to row r (no row ends here)
+            la = Op::combine(la, Op::combine(Op::combine(v[0], v[1]), Op::combine(v[2], v[3])));
+            continue;
+        }
+        // slow path: rows end in this chunk.  Fold the lane partials of row r first.
+        carry = Op::combine(carry, warp_fold<Op>(la));
+        la = Op::identity();
+
+        // head flags: word k bit l <=> a row ends at chunk position 32k + l (in [1, 127])
+        uint32_t f[4] = {0u, 0u, 0u, 0u};
+        int32_t n_emit = 0;
+        int32_t E0 = 0;   // window 0's row end for this lane (reused by the emission)
+        for (int32_t rw = r;; rw += 32) {
+            const int32_t row = rw + lane;
+            const int32_t E = row < x1 ? A.off[row + 1] : INT_MAX;
+            if (rw == r) E0 = E;
+            const int32_t p = E == INT_MAX ? INT_MAX : E - e0;
+            const bool fl = p >= 1 && p <= 127;
+            const uint32_t bit = fl ? 1u << (p & 31) : 0u;
+            const int word = fl ? (p >> 5) : -1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] |= __reduce_or_sync(kFull, word == k ? bit : 0u);
+            const int n = __popc(__ballot_sync(kFull, p <= kChunk));
+            n_emit += n;
+            if (n < 32) break;
+        }
+        if (part_head) {
+            const int p = -e0;   // in [1, 127]
+            f[p >> 5] |= 1u << (p & 31);
+        }
+
+        // segmented scan over positions 0..127: 4 independent warp scans (segment starts from
+        // the uniform flag words), then the carries are chained through the sub-chunks
+        int start[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t m = f[k] & (0xFFFFFFFFu >> (31 - lane));   // flags at lanes <= l
+            start[k] = m ? 31 - __clz(m) : -1;
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const T y = shfl_up(v[k], d);
+                if (lane >= d && lane - d >= start[k]) v[k] = Op::combine(y, v[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (start[k] < 0) v[k] = Op::combine(carry, v[k]);
+            carry = shfl_idx(v[k], 31);
+            my_sum[k * 32 + lane] = v[k];
+        }
+        T next_carry = carry;
+        __syncwarp();
+
+        // emit every row ending here: sum = S(p - 1); rows without in-edges get identity
+        bool ended_at_end = false;
+        for (int32_t k = 0; k < n_emit; k += 32) {
+            const int32_t row = r + k + lane;
+            const int32_t E = k == 0 ? E0 : (row < x1 ? A.off[row + 1] : INT_MAX);
+            int32_t B = shfl_up(E, 1);
+            const int32_t Bw = k == 0 ? Bc : A.off[r + k];   // start of the window's first row
+            if (lane == 0) B = Bw;
+            if (k + lane < n_emit) {
+                T val = Op::identity();
+                if (B < E) {
+                    const int pos = E - e0 - 1;
+                    val = pos >= 0 ? my_sum[pos] : Op::identity();
+                    if (E - e0 == kChunk) ended_at_end = true;
+                }
+                if (row == defer) static_cast<T*>(A.head_out)[q] = val;
+                else op.finish(row, val, cnt);
+            }
+        }
+        r += n_emit;
+        Bc = r < A.rows ? A.off[r] : y1;
+        Ec = r < A.rows ? A.off[r + 1] : y1;
+        if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
+        carry = next_carry;
+        __syncwarp();
+    }
+    // rows finished after the last edge of the range (rows without in-edges)
+    for (int32_t row = r + lane; row < x1; row += 32) {
+        if (row == defer) static_cast<T*>(A.head_out)[q] = Op::identity();
+        else op.finish(row, Op::identity(), cnt);
+    }
+    // partial of the row leaving the range
+    const T out = Op::combine(carry, warp_fold<Op>(la));
+    if (lane == 0) static_cast<T*>(A.carry_out)[q] = out;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_ranges(Op op, RangeArgs A) {
+    using T = typename Op::T;
+    __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums by position (conflict-free)
+    __shared__ unsigned long long s_cnt[2];
+    const int wid = threadIdx.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    PullCounters cnt{0, 0};
+    if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
+    flush_counters(cnt, s_cnt, A.counters);
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is

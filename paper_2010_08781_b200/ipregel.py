@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libipregel.so")
+LIB_PATH = os.environ.get("IPREGEL_LIB") or os.path.join(_HERE, "libipregel.so")
 
 APP_PAGERANK, APP_HASHMIN_CC, APP_SSSP = 0, 1, 2
 COMBINE_SUM, COMBINE_MIN = 0, 1

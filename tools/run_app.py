@@ -24,7 +24,8 @@ ap.add_argument("--degree-order", action="store_true")
 a = ap.parse_args()
 g = config_graph_device(a.config, weighted=True, degree_order=a.degree_order)
 G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
-                                 g["csr_idx"], g["csc_w"], g["csr_w"]))
+                                 g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
+                                 degree_ordered=a.degree_order))
 for _ in range(a.repeat):
     t = time.time()
     G.run(a.app, mode=a.mode, iterations=a.iterations)
