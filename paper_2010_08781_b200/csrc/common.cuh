@@ -43,17 +43,37 @@ __device__ __forceinline__ uint64_t policy_for(int mode, const void* base = null
     return mode == 1 ? policy_evict_last() : (mode == 2 ? policy_evict_first() : policy_evict_normal());
 }
 
+// Compile-time variants (tuning builds): IPREGEL_GATHER_HINT 1 = gathers carry the L2 policy
+// operand, 0 = plain ld.global.nc; IPREGEL_STREAM_CS 1 = index stream uses ld.global.cs (evict
+// first without a policy operand), 0 = L2::cache_hint evict_first policy.
+#ifndef IPREGEL_GATHER_HINT
+#define IPREGEL_GATHER_HINT 1
+#endif
+#ifndef IPREGEL_STREAM_CS
+#define IPREGEL_STREAM_CS 0
+#endif
+
 // Streamed (read-once) loads: non-coherent path, no L1 allocation, L2 evict-first.
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
     int32_t r;
+#if IPREGEL_STREAM_CS
+    (void)pol;
+    asm("ld.global.cs.s32 %0, [%1];" : "=r"(r) : "l"(p));
+#else
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
                  : "=r"(r) : "l"(p), "l"(pol));
+#endif
     return r;
 }
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
     uint32_t r;
+#if IPREGEL_STREAM_CS
+    (void)pol;
+    asm("ld.global.cs.u32 %0, [%1];" : "=r"(r) : "l"(p));
+#else
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
                  : "=r"(r) : "l"(p), "l"(pol));
+#endif
     return r;
 }
 __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {
@@ -67,18 +87,36 @@ __device__ __forceinline__ int4 ld_stream4(const int4* p, uint64_t pol) {
 // explicit L2 policy.
 __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
     double r;
+#if IPREGEL_GATHER_HINT
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+#else
+    (void)pol;
+    asm("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+#endif
     return r;
 }
 __device__ __forceinline__ uint32_t ld_gather(const uint32_t* p, uint64_t pol) {
     uint32_t r;
+#if IPREGEL_GATHER_HINT
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+#else
+    (void)pol;
+    asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+#endif
     return r;
 }
 
 // Gather with an L1 choice: hot (L1 evict-last) or cold (no L1 allocation) per lane.
 __device__ __forceinline__ double ld_gather_l1(const double* p, uint64_t pol, int hot) {
     double r;
+#if !IPREGEL_GATHER_HINT
+    (void)pol;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q ld.global.nc.L1::evict_last.f64 %0, [%1];\n\t"
+        "@!q ld.global.nc.L1::no_allocate.f64 %0, [%1];\n\t}"
+        : "=d"(r) : "l"(p), "r"(hot));
+    return r;
+#endif
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
         "@q ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;\n\t"
         "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n\t}"
@@ -87,6 +125,14 @@ __device__ __forceinline__ double ld_gather_l1(const double* p, uint64_t pol, in
 }
 __device__ __forceinline__ uint32_t ld_gather_l1(const uint32_t* p, uint64_t pol, int hot) {
     uint32_t r;
+#if !IPREGEL_GATHER_HINT
+    (void)pol;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q ld.global.nc.L1::evict_last.u32 %0, [%1];\n\t"
+        "@!q ld.global.nc.L1::no_allocate.u32 %0, [%1];\n\t}"
+        : "=r"(r) : "l"(p), "r"(hot));
+    return r;
+#endif
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
         "@q ld.global.nc.L1::evict_last.L2::cache_hint.u32 %0, [%1], %2;\n\t"
         "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n\t}"

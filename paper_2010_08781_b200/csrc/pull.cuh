@@ -208,6 +208,15 @@ __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
                                                 const uint32_t* __restrict__ wts, int32_t e0,
                                                 int32_t lo, int32_t hi, int lane, uint64_t pol) {
     ChunkLoad L;
+    if (e0 >= lo && e0 + kChunk <= hi) {   // warp-uniform: interior chunk, no bounds checks
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t e = e0 + 32 * k + lane;
+            L.idx[k] = ld_stream(idx + e, pol);
+            L.w[k] = (kWeighted && wts) ? ld_stream(wts + e, pol) : 1u;
+        }
+        return L;
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int32_t e = e0 + 32 * k + lane;
