@@ -251,56 +251,91 @@ k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restri
          const unsigned long long* __restrict__ counters_edges, int64_t dst_base,
          uint32_t* __restrict__ val, uint32_t* __restrict__ bits,
          const double* __restrict__ contrib, double* __restrict__ acc) {
-    __shared__ long long s_pre[kExpandItems + 1];
-    __shared__ int32_t s_id[kExpandItems + 1];
+    // per chunk of kExpandItems edges: the frontier entries it touches, each with its adjacency
+    // bases resolved once, and an owner table (edge slot -> entry) from a block scan of the
+    // entries' start flags -- no per-edge search, no per-edge offset loads
+    constexpr int kPer = kExpandItems / kExpandThreads;
+    __shared__ int32_t s_start[kExpandItems + 1];   // entry start relative to the chunk
+    __shared__ int32_t s_b1[kExpandItems + 1], s_d1[kExpandItems + 1], s_b2[kExpandItems + 1];
     __shared__ uint32_t s_val[kExpandItems + 1];
+    __shared__ int32_t s_id[kExpandItems + 1];
+    __shared__ uint16_t s_owner[kExpandItems];
     __shared__ int s_range[2];
+    __shared__ int s_wsum[kExpandThreads / 32];
     const int64_t n = (int64_t)*counters_len;
     const int64_t total = (int64_t)*counters_edges;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t e0 = (int64_t)blockIdx.x * kExpandItems; e0 < total;
          e0 += (int64_t)gridDim.x * kExpandItems) {
         const int64_t e1 = e0 + kExpandItems < total ? e0 + kExpandItems : total;
+        const int span = (int)(e1 - e0);
         if (threadIdx.x < 2) {
             // entry owning edge e: last i with e_pre[i] <= e
-            int64_t target = threadIdx.x == 0 ? e0 : e1 - 1;
+            const int64_t target = threadIdx.x == 0 ? e0 : e1 - 1;
             int64_t lo = 0, hi = n - 1;
             while (lo < hi) {
-                int64_t mid = (lo + hi + 1) >> 1;
+                const int64_t mid = (lo + hi + 1) >> 1;
                 if (e_pre[mid] <= target) lo = mid; else hi = mid - 1;
             }
             s_range[threadIdx.x] = (int)lo;
         }
+        for (int j = threadIdx.x; j < kExpandItems; j += kExpandThreads) s_owner[j] = 0;
         __syncthreads();
         const int f0 = s_range[0], nf = s_range[1] - s_range[0] + 1;
         for (int i = threadIdx.x; i < nf; i += kExpandThreads) {
-            s_pre[i] = e_pre[f0 + i];
-            s_id[i] = e_id[f0 + i];
+            const int64_t st = e_pre[f0 + i] - e0;
+            s_start[i] = (int32_t)st;
+            const int32_t u = e_id[f0 + i];
+            s_id[i] = u;
             s_val[i] = e_val[f0 + i];
+            const int64_t r = (int64_t)u - adj.src_base;
+            const int32_t b1 = adj.off1[r];
+            s_b1[i] = b1;
+            s_d1[i] = adj.off1[r + 1] - b1;
+            s_b2[i] = adj.off2 ? adj.off2[r] : 0;
+            if (i > 0) s_owner[st] = 1;   // start flag (entries have degree >= 1: distinct)
         }
         __syncthreads();
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += kExpandThreads) {
-            int lo = 0, hi = nf - 1;
-            while (lo < hi) {
-                int mid = (lo + hi + 1) >> 1;
-                if (s_pre[mid] <= e) lo = mid; else hi = mid - 1;
-            }
-            const int32_t u = s_id[lo];
-            int64_t pos = e - s_pre[lo];
-            const int64_t r = (int64_t)u - adj.src_base;
+        // owner(j) = number of entry starts in (0, j]: block inclusive scan of the flags
+        int f[kPer];
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            f[k] = s_owner[threadIdx.x * kPer + k];
+            c += f[k];
+        }
+        int inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += o;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        int pre = inc - c;
+        for (int w = 0; w < warp; ++w) pre += s_wsum[w];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            pre += f[k];
+            s_owner[threadIdx.x * kPer + k] = (uint16_t)pre;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < span; j += kExpandThreads) {
+            const int o = s_owner[j];
+            const int32_t pos = j - s_start[o];
             int32_t v;
             uint32_t w = 1u;
-            const int64_t d1 = adj.off1[r + 1] - adj.off1[r];
-            if (pos < d1) {
-                v = adj.idx1[adj.off1[r] + pos];
-                if (kProgram == 2 && adj.w1) w = adj.w1[adj.off1[r] + pos];
+            if (pos < s_d1[o]) {
+                v = adj.idx1[s_b1[o] + pos];
+                if (kProgram == 2 && adj.w1) w = adj.w1[s_b1[o] + pos];
             } else {
-                v = adj.idx2[adj.off2[r] + (pos - d1)];
+                v = adj.idx2[s_b2[o] + (pos - s_d1[o])];
             }
             const int64_t lv = (int64_t)v - dst_base;
             if (kProgram == 0) {
-                atomicAdd(acc + lv, contrib[u]);
+                atomicAdd(acc + lv, contrib[s_id[o]]);
             } else {
-                const uint32_t msg = kProgram == 2 ? sat_add(s_val[lo], w) : s_val[lo];
+                const uint32_t msg = kProgram == 2 ? sat_add(s_val[o], w) : s_val[o];
                 if (msg < val[v]) {  // cheap filter; the atomic decides
                     const uint32_t old = atomicMin(val + v, msg);
                     if (msg < old) atomicOr(bits + (lv >> 5), 1u << (lv & 31));
