@@ -32,6 +32,9 @@ namespace ipr {
 #ifndef IPREGEL_PULL_MINBLOCKS
 #define IPREGEL_PULL_MINBLOCKS 4
 #endif
+#ifndef IPREGEL_GATHER_AHEAD
+#define IPREGEL_GATHER_AHEAD 1   // chunks of gathers in flight ahead of the one being folded
+#endif
 constexpr int kPullThreads = 256;                 // 8 warps per CTA
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
@@ -119,6 +122,7 @@ struct PageRankPull : SumF64 {
     int write_rank;
     const void* gather_base() const { return contrib_cur; }
     __device__ const T* gptr() const { return contrib_cur; }
+    __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T sum, PullCounters&) const {
         const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
@@ -138,6 +142,8 @@ struct CCPullIn : MinU32 {
     int64_t vbase;
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
+    // label 0 is the smallest id: a row already at 0 cannot change (skip its gathers)
+    __device__ bool absorbed(int32_t row) const { return cur[vbase + row] == 0u; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters&) const {
         const uint32_t c = cur[vbase + row];
@@ -156,6 +162,7 @@ struct CCPullOut : MinU32 {
     int64_t vbase;
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
+    __device__ bool absorbed(int32_t row) const { return next[vbase + row] == 0u; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
         const uint32_t old = cur[vbase + row];
@@ -180,6 +187,7 @@ struct SSSPPull : MinU32 {
     int64_t vbase;
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
+    __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t w) { return sat_add(g, w); }
     __device__ void finish(int32_t row, T m, PullCounters& c) const {
         const uint32_t old = cur[vbase + row];
@@ -239,9 +247,10 @@ __device__ __forceinline__ typename Op::T gather_one(const Op& op, int32_t u, ui
 
 template <class Op>
 __device__ __forceinline__ void gather_chunk(const Op& op, const ChunkLoad& L,
-                                             typename Op::T (&g)[4], uint64_t pol, int32_t l1hot) {
+                                             typename Op::T (&g)[4], uint64_t pol, int32_t l1hot,
+                                             bool skip = false) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) g[k] = gather_one(op, L.idx[k], pol, l1hot);
+    for (int k = 0; k < 4; ++k) g[k] = gather_one(op, skip ? -1 : L.idx[k], pol, l1hot);
 }
 
 struct RangeArgs {
@@ -311,9 +320,37 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
     const int32_t defer = (q > 0 && r < A.rows && Bc < y0) ? r : -1;
     T carry = Op::identity();   // partial of row r from earlier slow chunks
     T la = Op::identity();      // lane-private partial of row r from fast chunks
+    bool absorbed = r < x1 && op.absorbed(r);
     // chunks on the global 128-edge grid covering [y0, y1)
     const int32_t c0 = y0 - ((y0 + A.cphase) & (kChunk - 1));
 
+#if IPREGEL_GATHER_AHEAD == 2
+    // software pipeline: indices three chunks ahead, gathered values two chunks ahead
+    ChunkLoad L0 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
+    ChunkLoad L1 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
+    ChunkLoad L2 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + 2 * kChunk, y0, y1, lane, pol_s);
+    T g0[4], g1[4];
+    gather_chunk(op, L0, g0, pol_g, A.l1hot);
+    gather_chunk(op, L1, g1, pol_g, A.l1hot);
+
+#pragma unroll 1
+    for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
+        T g2[4];
+        gather_chunk(op, L2, g2, pol_g, A.l1hot);
+        uint32_t wc[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wc[k] = L0.w[k];
+        L0 = L1;
+        L1 = L2;
+        L2 = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 3 * kChunk, y0, y1, lane, pol_s);
+        T v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = Op::message(g0[k], wc[k]);
+            g0[k] = g1[k];
+            g1[k] = g2[k];
+        }
+#else
     // software pipeline: indices two chunks ahead, gathered values one chunk ahead
     ChunkLoad Lc = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
     ChunkLoad Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
@@ -323,7 +360,8 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
 #pragma unroll 2
     for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
         T gn[4];
-        gather_chunk(op, Ln, gn, pol_g, A.l1hot);
+        // the next chunk lies inside an absorbed open row: its messages cannot change it
+        gather_chunk(op, Ln, gn, pol_g, A.l1hot, absorbed && r < x1 && Ec > e0 + 2 * kChunk);
         uint32_t wc[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) wc[k] = Lc.w[k];
@@ -335,6 +373,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
             v[k] = Op::message(gc[k], wc[k]);
             gc[k] = gn[k];
         }
+#endif
 
         // The partition's first chunk when its first edge is not on the 128-edge grid: on one
         // GPU the previous partition's last row ends there, so it takes the slow path with a
@@ -419,6 +458,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         r += n_emit;
         Bc = r < A.rows ? A.off[r] : y1;
         Ec = r < A.rows ? A.off[r + 1] : y1;
+        absorbed = r < x1 && op.absorbed(r);
         if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
         carry = next_carry;
         __syncwarp();
