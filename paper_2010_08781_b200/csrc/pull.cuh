@@ -214,8 +214,17 @@ struct ChunkLoad {
 template <bool kWeighted>
 __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
                                                 const uint32_t* __restrict__ wts, int32_t e0,
-                                                int32_t lo, int32_t hi, int lane, uint64_t pol) {
+                                                int32_t lo, int32_t hi, int lane, uint64_t pol,
+                                                bool skip = false) {
     ChunkLoad L;
+    if (skip) {   // warp-uniform: the chunk's messages cannot change its (absorbed) row
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            L.idx[k] = -1;
+            L.w[k] = 1u;
+        }
+        return L;
+    }
     if (e0 >= lo && e0 + kChunk <= hi) {   // warp-uniform: interior chunk, no bounds checks
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -366,7 +375,8 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
 #pragma unroll
         for (int k = 0; k < 4; ++k) wc[k] = Lc.w[k];
         Lc = Ln;
-        Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 2 * kChunk, y0, y1, lane, pol_s);
+        Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 2 * kChunk, y0, y1, lane, pol_s,
+                                       absorbed && r < x1 && Ec > e0 + 3 * kChunk);
         T v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
