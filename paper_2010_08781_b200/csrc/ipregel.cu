@@ -212,7 +212,9 @@ struct ipregel_graph {
 // =============================================================================================
 namespace {
 
-bool multi_rank(const ipregel_graph* g) { return g->comm && g->comm->world > 1; }
+// Any graph created with a communicator exchanges through NCCL (a world of 1 included, which is
+// how the NCCL path is exercised on a single GPU).
+bool multi_rank(const ipregel_graph* g) { return g->comm != nullptr; }
 
 void check_device(int device) {
     cudaDeviceProp prop;
@@ -1193,7 +1195,7 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
             csc_base += descs[i].csc_edges;
             csr_base += descs[i].csr_edges;
         }
-        if (comm && comm->world > 1) {
+        if (comm) {
             // every rank's (vb, rows, csc_edges, csr_edges) -> ranges and global edge bases
             int64_t mine[4] = {descs[0].vertex_begin, descs[0].vertex_end - descs[0].vertex_begin,
                                descs[0].csc_edges, descs[0].csr_edges};

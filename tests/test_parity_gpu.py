@@ -403,3 +403,37 @@ def test_gpu_fixture_degree_order_matches_cpu_coo():
         if order:
             deg = g["csr_off"].diff().cpu().numpy()
             assert np.all(np.diff(deg) <= 0)  # internal ids ascend by decreasing out-degree
+
+
+# ------------------------------------------------------------------ NCCL path (world of 1)
+
+def test_nccl_path_single_rank_matches_oracle():
+    """A graph created with a communicator runs every exchange through NCCL (grouped in-place
+    broadcasts, all-reduced counters, all-gathered frontier sizes); with a world of one rank this
+    exercises the multi-GPU code path on the one GPU available."""
+    import torch
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    comm = ipr.Comm(0, 1, ipr.nccl_unique_id(), torch.cuda.current_device())
+    rng = np.random.default_rng(8)
+    n = 3000
+    src, dst, w = checkers.random_graph(rng, n, 20000, weighted=True)
+    d = to_device(csr_csc(n, src, dst, w))
+    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"],
+                                     d["csr_idx"], d["csc_w"], d["csr_w"]), comm=comm)
+    for mode in ("pull", "push", "auto"):
+        o = oracle.hashmin_cc(n, src, dst)
+        G.run("cc", mode=mode)
+        np.testing.assert_array_equal(G.values(host=True), o["values"])
+        np.testing.assert_array_equal(G.stats()["messages"], o["messages"])
+        o = oracle.sssp(n, src, dst, w, source=5)
+        G.run("sssp", mode=mode, source=5)
+        np.testing.assert_array_equal(G.values(host=True), o["values"])
+        np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
+    for mode in ("pull", "push"):
+        o = oracle.pagerank(n, src, dst)
+        G.run("pagerank", mode=mode)
+        assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
+        np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
+    G.close()
+    comm.close()
