@@ -148,14 +148,33 @@ typedef struct {
     uint32_t sssp_source;          /* SSSP_SOURCE of Fig. 10; default 0                         */
     float push_fraction;           /* AUTO: push when messages(s-1) < push_fraction * scanned
                                       edges of a pull superstep; default 0.04                  */
-    uint32_t flags;                /* reserved, must be 0                                       */
+    uint32_t flags;                /* IPREGEL_RUN_* bits below; default 0                       */
 } ipregel_run_params;
+
+/* Exchange of the broadcast array between partitions after a PULL superstep (ranks of a comm,
+ * or loopback partitions).  Default (neither bit): FUSED when every other replica is reachable,
+ * else COLLECTIVE.
+ *   FUSED: the pull kernel's recipient-compute epilogue stores each owned result into every
+ *     replica of the broadcast array (peer GPUs' replicas mapped with CUDA IPC over NVLink /
+ *     NVSwitch; the other partitions' replicas in loopback), so the exchange overlaps the
+ *     gathers tile by tile; a one-element AllReduce (PageRank) or the counter AllReduce
+ *     (CC/SSSP) on the run stream is the superstep barrier.  At most 8 ranks / partitions.
+ *     Requires every rank's graph to be destroyed collectively (peers stay mapped until then).
+ *   COLLECTIVE: a separate in-place AllGatherv (grouped ncclBroadcast; device copies in
+ *     loopback) after the kernel.
+ * Push supersteps always exchange the sparse (id, value) frontier through NCCL.  Values are
+ * bit-identical either way.  Setting both bits: INVALID_ARGUMENT; FUSED when peers are not
+ * reachable: UNSUPPORTED.  The choice is made collectively on the first run of each app. */
+#define IPREGEL_RUN_EXCHANGE_COLLECTIVE 0x1u
+#define IPREGEL_RUN_EXCHANGE_FUSED 0x2u
 
 /* Per-superstep record of the last run (index = superstep, 0 = initialisation). */
 typedef struct {
     uint32_t capacity;        /* in: length of every non-NULL array below                       */
     uint32_t supersteps;      /* out: supersteps executed (including superstep 0)               */
     int32_t status;           /* out: status of the last run                                    */
+    int32_t exchange;         /* out: exchange of the last run's pull supersteps: 0 none (one
+                                 partition), 1 COLLECTIVE, 2 FUSED (IPREGEL_RUN_EXCHANGE_*)      */
     float* time_ms;           /* superstep wall time on the stream (kernels + exchange + counters) */
     float* kernel_ms;         /* time of the superstep's main delivery kernel(s) only           */
     uint8_t* mode;            /* 0 init, 1 pull, 2 push                                         */

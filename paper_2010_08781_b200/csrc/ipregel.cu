@@ -153,6 +153,13 @@ struct AppState {
     unsigned long long* blk_b = nullptr;
     int32_t* iota = nullptr;                   // PageRank push: every vertex as a source
     unsigned long long* iota_len = nullptr;
+    // Fused exchange: the OTHER replicas of buffer w of the broadcast array
+    // (contrib[w] or val[w]) that receive this partition's owned slice from the pull epilogue.
+    // Loopback: the other partitions' buffers.  Ranks: peers' buffers mapped with CUDA IPC.
+    void* peer[2][kMaxPeers] = {};
+    int npeer = 0;
+    int peers_state = 0;                       // 0 not set up, 1 reachable, -1 not reachable
+    std::vector<void*> ipc_opened;
     DeviceBuffers mem;
 };
 
@@ -196,6 +203,7 @@ struct ipregel_graph {
     bool poisoned = false;
     int last_app = -1;
     int last_status = -1;
+    int last_exchange = 0;         // 0 none, 1 collective, 2 fused
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
@@ -578,6 +586,132 @@ std::vector<unsigned long long> frontier_counts(ipregel_graph* g) {
     return counts;
 }
 
+// ---- fused exchange ----------------------------------------------------
+void* replica_buf(AppState& S, int app, int w) {
+    return app == IPREGEL_APP_PAGERANK ? (void*)S.contrib[w] : (void*)S.val[w];
+}
+
+// Ranks: map every other rank's replica buffers into this process (CUDA IPC over NVLink /
+// NVSwitch).  Collective: the handles travel by ncclAllGather and the ranks agree (AllReduce)
+// that every mapping succeeded; otherwise nothing stays mapped and the run falls back to the
+// collective exchange.
+void setup_ipc_peers(ipregel_graph* g, int app) {
+    Partition& p = g->parts[0];
+    AppState& S = p.st[app];
+    if (S.peers_state != 0) return;
+    cudaStream_t s = g->stream;
+    const int world = g->comm->world, rank = g->comm->rank;
+    constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+    unsigned long long bad = world - 1 > kMaxPeers ? 1ull : 0ull;
+    std::vector<uint8_t> mine(2 * H, 0), all(2 * H * world, 0);
+    for (int w = 0; w < 2 && !bad; ++w) {
+        cudaIpcMemHandle_t h;
+        if (cudaIpcGetMemHandle(&h, replica_buf(S, app, w)) != cudaSuccess) {
+            cudaGetLastError();
+            bad = 1;
+        } else {
+            memcpy(mine.data() + w * H, &h, H);
+        }
+    }
+    DeviceBuffers tmp;
+    uint8_t* dsend = tmp.alloc<uint8_t>(2 * H, s);
+    uint8_t* drecv = tmp.alloc<uint8_t>(2 * H * world, s);
+    CU(cudaMemcpyAsync(dsend, mine.data(), 2 * H, cudaMemcpyHostToDevice, s));
+    NC(ncclAllGather(dsend, drecv, 2 * H, ncclUint8, g->comm->nccl, s));
+    CU(cudaMemcpyAsync(all.data(), drecv, all.size(), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    tmp.release();
+    std::vector<void*> opened;
+    int k = 0;
+    for (int r = 0; r < world && !bad; ++r) {
+        if (r == rank) continue;
+        for (int w = 0; w < 2 && !bad; ++w) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, all.data() + (2 * r + w) * H, H);
+            void* q = nullptr;
+            if (cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                bad = 1;
+                break;
+            }
+            opened.push_back(q);
+            S.peer[w][k] = q;
+        }
+        ++k;
+    }
+    // every rank must agree before any kernel stores into a peer
+    p.host_cnt[0] = bad;
+    CU(cudaMemcpyAsync(p.dscratch + 40, p.host_cnt, 8, cudaMemcpyHostToDevice, s));
+    NC(ncclAllReduce(p.dscratch + 40, p.dscratch + 41, 1, ncclUint64, ncclSum, g->comm->nccl, s));
+    CU(cudaMemcpyAsync(p.host_cnt + 1, p.dscratch + 41, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (p.host_cnt[1] != 0) {
+        for (void* q : opened) cudaIpcCloseMemHandle(q);
+        S.npeer = 0;
+        S.peers_state = -1;
+        return;
+    }
+    S.ipc_opened = opened;
+    S.npeer = world - 1;
+    S.peers_state = 1;
+}
+
+// Whether the pull supersteps of this run exchange through the fused epilogue stores.
+bool use_fused_exchange(ipregel_graph* g, int app, uint32_t flags) {
+    if (flags & IPREGEL_RUN_EXCHANGE_COLLECTIVE) return false;
+    const bool require = (flags & IPREGEL_RUN_EXCHANGE_FUSED) != 0;
+    if (multi_rank(g)) {
+        setup_ipc_peers(g, app);
+        if (g->parts[0].st[app].peers_state == 1) return true;
+        if (require)
+            fail(IPREGEL_ERR_UNSUPPORTED, "fused exchange: peer replicas not reachable (CUDA IPC)");
+        return false;
+    }
+    const int np = (int)g->parts.size();
+    if (np == 1) return true;   // nothing to exchange: the owned slice is the whole replica
+    if (np - 1 > kMaxPeers) {
+        if (require)
+            fail(IPREGEL_ERR_UNSUPPORTED, "fused exchange supports at most %d partitions",
+                 kMaxPeers + 1);
+        return false;
+    }
+    for (int a = 0; a < np; ++a) {
+        AppState& S = g->parts[a].st[app];
+        if (S.peers_state == 1) continue;
+        int k = 0;
+        for (int b = 0; b < np; ++b) {
+            if (b == a) continue;
+            for (int w = 0; w < 2; ++w) S.peer[w][k] = replica_buf(g->parts[b].st[app], app, w);
+            ++k;
+        }
+        S.npeer = k;
+        S.peers_state = 1;
+    }
+    return true;
+}
+
+int exchange_kind(ipregel_graph* g, bool fused) {
+    if (!multi_rank(g) && g->parts.size() == 1) return 0;
+    return fused ? 2 : 1;
+}
+
+template <class T>
+PeerSlots<T> peer_slots(const AppState& S, int w, bool fused) {
+    PeerSlots<T> ps{};
+    ps.n = fused ? S.npeer : 0;
+    for (int k = 0; k < ps.n; ++k) ps.p[k] = static_cast<T*>(S.peer[w][k]);
+    return ps;
+}
+
+// Superstep barrier after fused stores (ranks): a one-element AllReduce on the run stream.  It
+// completes on a rank only after every rank's pull kernel -- and so its peer stores -- finished.
+void fused_barrier(ipregel_graph* g) {
+    if (!multi_rank(g)) return;   // loopback: stream order
+    Partition& p = g->parts[0];
+    NC(ncclAllReduce(p.dscratch + 48, p.dscratch + 49, 1, ncclUint64, ncclSum, g->comm->nccl,
+                     g->stream));
+}
+
 // ---- timing -------------------------------------------------------------------------------
 cudaEvent_t ev(ipregel_graph* g, size_t i) {
     while (g->events.size() <= i) {
@@ -619,6 +753,8 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     const double inv_n = 1.0 / (double)n;    // initial_value
     const uint32_t last = std::min<uint32_t>(k, max_steps - 1);
     const bool push = P.mode == IPREGEL_MODE_PUSH;
+    const bool fused = !push && use_fused_exchange(g, IPREGEL_APP_PAGERANK, P.flags);
+    g->last_exchange = exchange_kind(g, fused);
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -689,6 +825,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 PageRankPull op;
                 op.contrib_cur = S.contrib[cur];
                 op.contrib_next = S.contrib[1 - cur];
+                op.peers = peer_slots<double>(S, 1 - cur, fused && broadcast);
                 op.rank = S.rank;
                 op.out_off = p.csr_off;
                 op.vbase = p.vb;
@@ -710,7 +847,8 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         T.kend();
         if (broadcast) {
             const int nx = 1 - cur;
-            exchange_owned<double>(g, [nx](Partition& p) { return p.st[0].contrib[nx]; });
+            if (fused) fused_barrier(g);
+            else exchange_owned<double>(g, [nx](Partition& p) { return p.st[0].contrib[nx]; });
         }
         T.end();
         StepRecord& R = g->steps.back();
@@ -737,6 +875,8 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     const bool multi = np > 1 || multi_rank(g);
     // edges a pull superstep scans (CC gathers over CSC and CSR rows: the symmetrised graph)
     const uint64_t pull_edges = cc ? 2ull * (uint64_t)g->e : (uint64_t)g->e;
+    const bool fused = P.mode != IPREGEL_MODE_PUSH && use_fused_exchange(g, app, P.flags);
+    g->last_exchange = exchange_kind(g, fused);
 
     for (auto& p : g->parts) ensure_push_view(g, p);
     // SSSP_SOURCE is an original id; find its internal id under a relabelled layout
@@ -873,17 +1013,22 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
+                    b.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
                     launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
                 } else {
                     SSSPPull a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
+                    a.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
                     launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
                 }
             }
             T.kend();
             const int nx = 1 - cur;
-            exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
+            // fused: the epilogue already stored the owned slice into every replica; the counter
+            // AllReduce below is the superstep barrier
+            if (!fused)
+                exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
             unsigned long long c[2];
             reduce_counters(g, false, c, 2);
             T.end();
@@ -1013,7 +1158,11 @@ void destroy_graph(ipregel_graph* g) {
     if (!g) return;
     cudaStreamSynchronize(g->stream);
     for (auto& p : g->parts) {
-        for (auto& S : p.st) S.mem.release();
+        for (auto& S : p.st) {
+            for (void* q : S.ipc_opened) cudaIpcCloseMemHandle(q);
+            S.ipc_opened.clear();
+            S.mem.release();
+        }
         p.graph_mem.release();
         if (p.host_cnt) cudaFreeHost(p.host_cnt);
         p.host_cnt = nullptr;
@@ -1313,7 +1462,10 @@ ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner c
     if (max_supersteps == 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "max_supersteps must be >= 1");
     if (P.mode < IPREGEL_MODE_AUTO || P.mode > IPREGEL_MODE_PUSH)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown mode %d", P.mode);
-    if (P.flags != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "flags must be 0");
+    if (P.flags & ~(uint32_t)(IPREGEL_RUN_EXCHANGE_COLLECTIVE | IPREGEL_RUN_EXCHANGE_FUSED))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", P.flags);
+    if ((P.flags & IPREGEL_RUN_EXCHANGE_COLLECTIVE) && (P.flags & IPREGEL_RUN_EXCHANGE_FUSED))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "EXCHANGE_COLLECTIVE and EXCHANGE_FUSED are exclusive");
     if (app == IPREGEL_APP_SSSP && (int64_t)P.sssp_source >= g->n)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "sssp_source %u >= N", P.sssp_source);
     if (!(P.push_fraction >= 0.0f)) fail(IPREGEL_ERR_INVALID_ARGUMENT, "push_fraction < 0");
@@ -1397,6 +1549,7 @@ ipregel_status ipregel_get_stats(ipregel_graph* g, ipregel_stats* st) {
     if (!g || !st) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or stats is NULL");
     st->supersteps = (uint32_t)g->steps.size();
     st->status = g->last_status;
+    st->exchange = g->last_exchange;
     const size_t m = std::min<size_t>(st->capacity, g->steps.size());
     for (size_t i = 0; i < m; ++i) {
         const StepRecord& R = g->steps[i];

@@ -106,6 +106,24 @@ struct MinU32 {
     __device__ static T combine(T a, T b) { return a > b ? b : a; }   // Fig. 5 ip_combine
 };
 
+// ---- fused exchange ---------------------------------------------------------
+// Every OTHER replica of the broadcast array that must receive this partition's owned slice: peer
+// GPUs' replicas mapped over NVLink (CUDA IPC) for ranks of a communicator, or the other
+// partitions' replicas in loopback mode.  The recipient compute stores each owned result into all
+// of them in its epilogue, so the exchange that a separate AllGatherv would do after the kernel is
+// carried by the kernel's own stores, overlapped with the gathers of the rest of the grid.
+constexpr int kMaxPeers = 7;
+template <class T>
+struct PeerSlots {
+    T* p[kMaxPeers];
+    int n;
+    __device__ __forceinline__ void store(int64_t i, T v) const {
+#pragma unroll
+        for (int k = 0; k < kMaxPeers; ++k)
+            if (k < n) p[k][i] = v;
+    }
+};
+
 // ---- vertex programs: gather = outbox value of the sender, message = value on the edge,
 // finish = recipient compute --------------------------------------------------------------------
 // PageRank, Fig. 8: the message of u is contrib[u] = r_u / outdeg(u); recipient compute is
@@ -114,6 +132,7 @@ struct PageRankPull : SumF64 {
     static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
+    PeerSlots<double> peers;                  // fused exchange: other replicas (n = 0: none)
     double* __restrict__ rank;                // owned, local ids (written when write_rank)
     const int32_t* __restrict__ out_off;      // owned CSR offsets (local rows)
     int64_t vbase;
@@ -129,7 +148,9 @@ struct PageRankPull : SumF64 {
         if (write_rank) rank[row] = r;
         if (broadcast) {
             const int32_t deg = out_off[row + 1] - out_off[row];
-            contrib_next[vbase + row] = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
+            const double c = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
+            contrib_next[vbase + row] = c;
+            peers.store(vbase + row, c);
         }
     }
 };
@@ -160,6 +181,7 @@ struct CCPullOut : MinU32 {
     const int32_t* __restrict__ in_off;   // owned CSC offsets
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
+    PeerSlots<uint32_t> peers;            // fused exchange: other replicas of `next`
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
     __device__ bool absorbed(int32_t row) const { return next[vbase + row] == 0u; }
@@ -169,6 +191,7 @@ struct CCPullOut : MinU32 {
         uint32_t v = next[vbase + row];
         v = m < v ? m : v;
         next[vbase + row] = v;
+        peers.store(vbase + row, v);
         if (v < old) {
             c.changed += 1;
             c.messages += (unsigned long long)(in_off[row + 1] - in_off[row]) +
@@ -185,6 +208,7 @@ struct SSSPPull : MinU32 {
     uint32_t* __restrict__ next;
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
+    PeerSlots<uint32_t> peers;            // fused exchange: other replicas of `next`
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
     __device__ bool absorbed(int32_t) const { return false; }
@@ -193,6 +217,7 @@ struct SSSPPull : MinU32 {
         const uint32_t old = cur[vbase + row];
         const uint32_t v = m < old ? m : old;
         next[vbase + row] = v;
+        peers.store(vbase + row, v);
         if (v < old) {
             c.changed += 1;
             c.messages += (unsigned long long)(out_off[row + 1] - out_off[row]);

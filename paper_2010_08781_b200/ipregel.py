@@ -35,6 +35,9 @@ ERR_UNSUPPORTED = 8
 APPS = {"pagerank": APP_PAGERANK, "cc": APP_HASHMIN_CC, "sssp": APP_SSSP}
 COMBINER_OF = {APP_PAGERANK: COMBINE_SUM, APP_HASHMIN_CC: COMBINE_MIN, APP_SSSP: COMBINE_MIN}
 MODES = {"auto": MODE_AUTO, "pull": MODE_PULL, "push": MODE_PUSH}
+RUN_EXCHANGE_COLLECTIVE, RUN_EXCHANGE_FUSED = 0x1, 0x2
+EXCHANGES = {"auto": 0, "collective": RUN_EXCHANGE_COLLECTIVE, "fused": RUN_EXCHANGE_FUSED}
+EXCHANGE_NAMES = {0: "none", 1: "collective", 2: "fused"}
 
 
 class IpregelError(RuntimeError):
@@ -66,7 +69,7 @@ class RunParams(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("capacity", ctypes.c_uint32), ("supersteps", ctypes.c_uint32),
-                ("status", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("exchange", ctypes.c_int32),
                 ("time_ms", ctypes.c_void_p), ("kernel_ms", ctypes.c_void_p),
                 ("mode", ctypes.c_void_p), ("changed", ctypes.c_void_p),
                 ("messages", ctypes.c_void_p), ("edges_scanned", ctypes.c_void_p),
@@ -295,13 +298,14 @@ class Graph:
 
     def run(self, app, max_supersteps: int = 1 << 30, mode="auto", iterations: int = 10,
             source: int = 0, push_fraction: float = 0.04, combiner=None,
-            allow_guard: bool = False) -> int:
+            allow_guard: bool = False, exchange: str = "auto") -> int:
         app = APPS[app] if isinstance(app, str) else int(app)
         p = run_params_default()
         p.mode = MODES[mode] if isinstance(mode, str) else int(mode)
         p.pagerank_iterations = iterations
         p.sssp_source = source
         p.push_fraction = push_fraction
+        p.flags = EXCHANGES[exchange]
         comb = COMBINER_OF.get(app, COMBINE_SUM) if combiner is None else combiner
         st = load().ipregel_run(self.handle, app, comb, max_supersteps, ctypes.byref(p))
         _check(st, "ipregel_run", allow=(ERR_MAX_SUPERSTEPS,) if allow_guard else ())
@@ -343,6 +347,7 @@ class Graph:
         out = {k: a[:m].copy() for k, a in arrs.items()}
         out["supersteps"] = st.supersteps
         out["status"] = st.status
+        out["exchange"] = EXCHANGE_NAMES.get(st.exchange, str(st.exchange))
         return out
 
     def memory_footprint(self):

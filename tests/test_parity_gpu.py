@@ -271,8 +271,12 @@ def test_message_storage_is_theta_n():
 
 # ------------------------------------------------------------------ partitions (loopback)
 
+@pytest.mark.parametrize("exchange", ["fused", "collective"])
 @pytest.mark.parametrize("parts", [2, 3, 8])
-def test_loopback_partitions_bit_identical(parts):
+def test_loopback_partitions_bit_identical(parts, exchange):
+    """G partitions on one GPU: the fused exchange (epilogue stores into every partition's
+    replica) and the collective one (copies after the kernel) give results
+    bit-identical to one partition."""
     rng = np.random.default_rng(77)
     import inputs
     src, dst, w = inputs.rmat_coo(13, 16, 11, weighted=True)
@@ -288,9 +292,10 @@ def test_loopback_partitions_bit_identical(parts):
             ref[(app, mode)] = (G1.values(host=True), G1.stats())
     Gp = make_graph(g, partitions=parts)
     for (app, mode), (v1, s1) in ref.items():
-        Gp.run(app, mode=mode)
+        Gp.run(app, mode=mode, exchange=exchange)
         vp = Gp.values(host=True)
         sp = Gp.stats()
+        assert sp["exchange"] == ("collective" if mode == "push" else exchange)
         if app == "pagerank" and mode == "push":
             assert np.abs(vp - v1).max() <= 1e-15  # atomicAdd order
         else:
@@ -299,9 +304,40 @@ def test_loopback_partitions_bit_identical(parts):
         np.testing.assert_array_equal(sp["changed"], s1["changed"])
         np.testing.assert_array_equal(sp["messages"], s1["messages"])
     o = oracle.sssp(n, src, dst, w, source=0)
-    Gp.run("sssp")
+    Gp.run("sssp", exchange=exchange)
     np.testing.assert_array_equal(Gp.values(host=True), o["values"])
     del rng
+
+
+def test_fused_exchange_flags():
+    import paper_2010_08781_b200 as ipr
+    n = 50
+    src = np.arange(n - 1)
+    g = csr_csc(n, src, src + 1)
+    G = make_graph(g, partitions=2, weighted=False)
+    import ctypes
+    p = ipr.run_params_default()
+    p.flags = ipr.RUN_EXCHANGE_FUSED | ipr.RUN_EXCHANGE_COLLECTIVE
+    st = ipr.load().ipregel_run(G.handle, ipr.APP_SSSP, ipr.COMBINE_MIN, 100, ctypes.byref(p))
+    assert st == ipr.ERR_INVALID_ARGUMENT
+    p.flags = 0x80
+    st = ipr.load().ipregel_run(G.handle, ipr.APP_SSSP, ipr.COMBINE_MIN, 100, ctypes.byref(p))
+    assert st == ipr.ERR_INVALID_ARGUMENT
+    G.run("sssp")
+    assert G.stats()["exchange"] == "fused"          # default with reachable replicas
+    G1 = make_graph(g, partitions=1, weighted=False)
+    G1.run("sssp")
+    assert G1.stats()["exchange"] == "none"
+    G9 = make_graph(g, partitions=9, weighted=False)  # more partitions than peer slots
+    G9.run("sssp")
+    assert G9.stats()["exchange"] == "collective"
+    with pytest.raises(ipr.IpregelError) as e:
+        G9.run("sssp", exchange="fused")
+    assert e.value.status == ipr.ERR_UNSUPPORTED
+    o = oracle.sssp(n, src, src + 1, None)
+    G9.run("pagerank")
+    G9.run("sssp", exchange="collective")
+    np.testing.assert_array_equal(G9.values(host=True), o["values"])
 
 
 def test_loopback_with_empty_partition():
@@ -407,7 +443,8 @@ def test_gpu_fixture_degree_order_matches_cpu_coo():
 
 # ------------------------------------------------------------------ NCCL path (world of 1)
 
-def test_nccl_path_single_rank_matches_oracle():
+@pytest.mark.parametrize("exchange", ["fused", "collective"])
+def test_nccl_path_single_rank_matches_oracle(exchange):
     """A graph created with a communicator runs every exchange through NCCL (grouped in-place
     broadcasts, all-reduced counters, all-gathered frontier sizes); with a world of one rank this
     exercises the multi-GPU code path on the one GPU available."""
@@ -423,16 +460,17 @@ def test_nccl_path_single_rank_matches_oracle():
                                      d["csr_idx"], d["csc_w"], d["csr_w"]), comm=comm)
     for mode in ("pull", "push", "auto"):
         o = oracle.hashmin_cc(n, src, dst)
-        G.run("cc", mode=mode)
+        G.run("cc", mode=mode, exchange=exchange)
         np.testing.assert_array_equal(G.values(host=True), o["values"])
         np.testing.assert_array_equal(G.stats()["messages"], o["messages"])
+        assert G.stats()["exchange"] == ("collective" if mode == "push" else exchange)
         o = oracle.sssp(n, src, dst, w, source=5)
-        G.run("sssp", mode=mode, source=5)
+        G.run("sssp", mode=mode, source=5, exchange=exchange)
         np.testing.assert_array_equal(G.values(host=True), o["values"])
         np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
     for mode in ("pull", "push"):
         o = oracle.pagerank(n, src, dst)
-        G.run("pagerank", mode=mode)
+        G.run("pagerank", mode=mode, exchange=exchange)
         assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
         np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
     G.close()
