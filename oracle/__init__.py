@@ -10,6 +10,9 @@ product path (``paper_2010_08781_b200``) never imports it and shares no code
 with it; the only common input is the COO edge list from ``inputs``.
 
 Parity status per function:
+  run(APP_PAGERANK, tol>=0)  pinned: closed forms of the per-superstep change
+                     (cycle, complete digraph, in-star), exact-rational deltas
+                     and stopping superstep on random graphs.
   run(APP_PAGERANK)  pinned: worked examples W1-W3 (exact rationals), closed
                      forms (cycle, complete digraph, in-star, out-star), the
                      mass invariant, scipy sparse power iteration.
@@ -60,7 +63,8 @@ def _load():
         lib.oracle_run.restype = ctypes.c_int
         lib.oracle_run.argtypes = [
             ctypes.c_int, ctypes.c_int64, ctypes.c_int64, p, p, p, ctypes.c_uint32,
-            ctypes.c_uint32, ctypes.c_uint32, p, p, ctypes.c_uint32, p, p, p, p, p]
+            ctypes.c_uint32, ctypes.c_uint32, p, p, ctypes.c_uint32, p, p, p, p, p,
+            ctypes.c_double, p]
         _lib = lib
     return _lib
 
@@ -70,11 +74,12 @@ def _ptr(a):
 
 
 def run(app: int, n: int, src, dst, w=None, k: int = 10, source: int = 0,
-        max_supersteps: int = 1 << 30, cap: int = 4096) -> dict:
+        max_supersteps: int = 1 << 30, cap: int = 4096, tol: float = -1.0) -> dict:
     """Run the interpreter; returns values, status and per-superstep counters.
 
     ``src``/``dst`` are the directed edges (int32), ``w`` optional uint32
-    weights (SSSP only; None means w = 1, Fig. 10).  PageRank values are f64,
+    weights (SSSP only; None means w = 1, Fig. 10).  ``tol`` >= 0 runs
+    PageRank to convergence (max per-vertex change <= tol, reading R27).  PageRank values are f64,
     CC labels and SSSP distances u32 (INF = 0xFFFFFFFF).
     """
     lib = _load()
@@ -91,9 +96,11 @@ def run(app: int, n: int, src, dst, w=None, k: int = 10, source: int = 0,
     messages = np.zeros(cap, np.uint64)
     secs = np.zeros(cap, np.float64)
     build_s = ctypes.c_double(0.0)
+    delta = np.zeros(cap, np.float64)
     rc = lib.oracle_run(app, n, m, _ptr(src), _ptr(dst), _ptr(w), k, source,
                         max_supersteps, _ptr(vals), ctypes.byref(steps), cap, _ptr(ran),
-                        _ptr(changed), _ptr(messages), _ptr(secs), ctypes.byref(build_s))
+                        _ptr(changed), _ptr(messages), _ptr(secs), ctypes.byref(build_s),
+                        float(tol), _ptr(delta))
     if rc not in (OK, GUARD):
         raise ValueError(f"oracle_run failed with status {rc}")
     s = min(steps.value, cap)
@@ -105,6 +112,7 @@ def run(app: int, n: int, src, dst, w=None, k: int = 10, source: int = 0,
         "changed": changed[:s].copy(),
         "messages": messages[:s].copy(),
         "seconds": secs[:s].copy(),
+        "delta": delta[:s].copy(),
         "build_seconds": build_s.value,
     }
 

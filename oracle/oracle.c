@@ -42,6 +42,15 @@
  *    saturates at INF (reading R9).  w == NULL means w = 1, i.e. exactly
  *    Fig. 10's "me->value + 1".
  *
+ *  - PageRank to convergence ("In practice however, a
+ *    PageRank application would typically run until convergence is
+ *    reached"; reading R27): with a tolerance eps >= 0, every
+ *    vertex of superstep s >= 1 folds |value_s - value_{s-1}| into a max
+ *    aggregator (Pregel's aggregators, Fig. 12 context),
+ *    and the master halts the run after the first superstep s >= 1 whose
+ *    aggregate is <= eps (its broadcast is never delivered), or after
+ *    superstep k as in Fig. 8.  eps < 0 disables it (Fig. 8 exactly).
+ *
  * Counters per executed superstep s: ran(s) = vertices computed,
  * changed(s) = vertices that broadcast, messages(s) = send() calls.
  * Termination: the run stops at the first superstep in which no vertex
@@ -122,6 +131,8 @@ typedef struct {
     uint32_t k;        /* PageRank supersteps that broadcast (Fig. 8's 10) */
     uint32_t source;   /* SSSP_SOURCE */
     double ratio;      /* 0.15 / N */
+    double tol;        /* PageRank convergence tolerance (< 0: off) */
+    double agg;        /* max |value_s - value_{s-1}| of the current superstep */
     double* fval;      /* PageRank vertex values */
     uint32_t* uval;    /* CC / SSSP vertex values */
     uint8_t* halted;
@@ -184,7 +195,11 @@ static void compute_pagerank(machine_t* M, int64_t v, uint32_t s, int has, doubl
     } else {
         double sum = 0.0;
         if (has) sum += m;                                     /* while(get_next_message) */
+        double old = M->fval[v];
         M->fval[v] = M->ratio + 0.85 * sum;
+        double d = M->fval[v] - old;                           /* max aggregator (R27) */
+        if (d < 0.0) d = -d;
+        if (d > M->agg) M->agg = d;
     }
     if (s < M->k) {
         int64_t deg = M->adj.off[v + 1] - M->adj.off[v];
@@ -239,12 +254,15 @@ static void compute_sssp(machine_t* M, int64_t v, uint32_t s, int has, uint32_t 
  *   Per-superstep counters (arrays of `cap`, may be NULL): ran, changed,
  *   messages, seconds.  *supersteps_out = supersteps executed.
  *   *build_seconds_out (may be NULL) = adjacency build time (not a superstep).
+ *   tol: PageRank convergence tolerance (< 0: off); delta_out (may be NULL):
+ *   per superstep, max_v |value_s(v) - value_{s-1}(v)| (0 for superstep 0 and
+ *   for the other apps).
  */
 int oracle_run(int app, int64_t n, int64_t m, const int32_t* src, const int32_t* dst,
                const uint32_t* w, uint32_t k, uint32_t source, uint32_t max_supersteps,
                void* values_out, uint32_t* supersteps_out, uint32_t cap, uint64_t* ran_out,
                uint64_t* changed_out, uint64_t* messages_out, double* seconds_out,
-               double* build_seconds_out) {
+               double* build_seconds_out, double tol, double* delta_out) {
     if (n < 1 || n > 2147483647LL || m < 0 || (m > 0 && (!src || !dst)) || !values_out ||
         max_supersteps == 0 || app < 0 || app > 2)
         return OR_INVALID;
@@ -256,6 +274,7 @@ int oracle_run(int app, int64_t n, int64_t m, const int32_t* src, const int32_t*
     memset(&M, 0, sizeof(M));
     M.app = app; M.n = n; M.k = k; M.source = source;
     M.ratio = 0.15 / (double)n;
+    M.tol = tol;
 
     double t0 = now_s();
     int rc = adj_build(n, m, src, dst, app == APP_SSSP ? w : NULL, app == APP_HASHMIN_CC, &M.adj);
@@ -293,6 +312,7 @@ int oracle_run(int app, int64_t n, int64_t m, const int32_t* src, const int32_t*
         uint64_t ran = 0;
         M.changed = 0;
         M.messages = 0;
+        M.agg = 0.0;
         for (int64_t v = 0; v < n; ++v) {
             /* naive selection */
             if (!(s == 0 || !M.halted[v] || M.cur.has[v])) continue;
@@ -316,8 +336,11 @@ int oracle_run(int app, int64_t n, int64_t m, const int32_t* src, const int32_t*
             if (changed_out) changed_out[executed] = M.changed;
             if (messages_out) messages_out[executed] = M.messages;
             if (seconds_out) seconds_out[executed] = te - ts;
+            if (delta_out) delta_out[executed] = M.agg;
         }
         executed += 1;
+        /* master halt: PageRank converged (reading R27) */
+        if (app == APP_PAGERANK && M.tol >= 0.0 && s >= 1 && M.agg <= M.tol) break;
     }
     if (ok) {
         if (app == APP_PAGERANK) memcpy(values_out, M.fval, un * sizeof(double));

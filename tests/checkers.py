@@ -31,6 +31,22 @@ def pagerank_exact(n, edges, k):
     return r
 
 
+def pagerank_exact_trajectory(n, edges, kmax):
+    """[r_0, r_1, ..., r_kmax] of the same exact-rational recursion."""
+    outdeg = [0] * n
+    for u, _ in edges:
+        outdeg[u] += 1
+    r = [Fraction(1, n)] * n
+    out = [r]
+    for _ in range(kmax):
+        acc = [Fraction(0)] * n
+        for u, v in edges:
+            acc[v] += r[u] / outdeg[u]
+        r = [Fraction(3, 20) / n + Fraction(17, 20) * a for a in acc]
+        out.append(r)
+    return out
+
+
 def pagerank_scipy(n, src, dst, k):
     """k steps of r <- 0.15/N + 0.85 * A^T D^+ r with scipy sparse (f64);
     duplicate edges are summed into A, i.e. counted with multiplicity."""

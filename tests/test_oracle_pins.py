@@ -139,6 +139,73 @@ def test_pagerank_rmat_vs_scipy():
     assert np.max(np.abs(r - ref) / ref) < 1e-12
 
 
+# ------------------------------------------------- PageRank to convergence (reading R27)
+# "a PageRank application would typically run until convergence"; the master
+# halts after the first superstep s >= 1 with max_v |r_s(v) - r_{s-1}(v)| <= tol.
+
+@pytest.mark.parametrize("n", [3, 64])
+def test_pagerank_tol_cycle_stops_at_once(n):
+    src = np.arange(n)
+    dst = (src + 1) % n
+    r = oracle.pagerank(n, src, dst, k=50, tol=1e-12)
+    assert r["supersteps"] == 2                       # r_1 = r_0 = 1/n (up to one rounding)
+    assert r["delta"][1] <= 2.0 ** -52 / n
+    np.testing.assert_allclose(r["values"], 1.0 / n, rtol=1e-15)
+    assert list(r["messages"]) == [n, n]              # the last broadcast is never delivered
+
+
+@pytest.mark.parametrize("n", [5, 1000])
+def test_pagerank_tol_in_star_closed_form(n):
+    # in-star (leaves -> 0): r_1 = (0.15/n + 0.85 (n-1)/n, 0.15/n ...),
+    # r_2 = ((0.15/n)(1 + 0.85 (n-1)), 0.15/n ...), r_3 = r_2 exactly: delta_3 = 0
+    leaves = np.arange(1, n)
+    r = oracle.pagerank(n, leaves, np.zeros(n - 1, dtype=np.int64), k=10, tol=0.0)
+    assert r["supersteps"] == 4
+    c1 = 0.15 / n + 0.85 * (n - 1) / n
+    c2 = (0.15 / n) * (1 + 0.85 * (n - 1))
+    d1 = max(abs(c1 - 1.0 / n), abs(0.15 / n - 1.0 / n))
+    assert r["delta"][1] == pytest.approx(d1, rel=1e-13)
+    assert r["delta"][2] == pytest.approx(abs(c2 - c1), rel=1e-13)
+    assert r["delta"][3] == 0.0
+    assert r["values"][0] == pytest.approx(c2, rel=1e-13)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pagerank_tol_random_vs_exact(seed):
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(5, 40))
+    src, dst, _ = checkers.random_graph(rng, n, int(rng.integers(n, 5 * n)))
+    kmax = 25
+    traj = checkers.pagerank_exact_trajectory(n, list(zip(src.tolist(), dst.tolist())), kmax)
+    dex = [0.0] + [float(max(abs(a - b) for a, b in zip(traj[t], traj[t - 1])))
+                   for t in range(1, kmax + 1)]
+    full = oracle.pagerank(n, src, dst, k=kmax, tol=-1.0)
+    # delta is the difference of two f64 iterates: error <= a few ulps of the ranks
+    np.testing.assert_allclose(full["delta"][1:kmax + 1], dex[1:], rtol=0, atol=1e-15)
+    # a tolerance halfway (geometrically) between two well-separated deltas
+    cand = [t for t in range(2, kmax) if dex[t] > 0 and dex[t] < 0.5 * dex[t - 1] and dex[t] > 1e-12]
+    if not cand:
+        return
+    t = cand[len(cand) // 2]
+    tol = math.sqrt(dex[t] * dex[t - 1])
+    first = next(s for s in range(1, kmax + 1) if dex[s] <= tol)
+    r = oracle.pagerank(n, src, dst, k=kmax, tol=tol)
+    assert r["supersteps"] == first + 1
+    np.testing.assert_allclose(r["values"], [float(x) for x in traj[first]], rtol=1e-14, atol=0)
+
+
+def test_pagerank_tol_capped_by_k_and_off_is_fig8():
+    rng = np.random.default_rng(5)
+    n = 100
+    src, dst, _ = checkers.random_graph(rng, n, 600)
+    a = oracle.pagerank(n, src, dst, k=10)
+    b = oracle.pagerank(n, src, dst, k=10, tol=-1.0)
+    c = oracle.pagerank(n, src, dst, k=10, tol=1e-300)   # never reached: Fig. 8's k wins
+    for r in (b, c):
+        np.testing.assert_array_equal(r["values"], a["values"])
+        assert r["supersteps"] == 11 and r["messages"][-1] == 0
+
+
 # ---------------------------------------------------------------- Hash-Min CC
 
 @pytest.mark.parametrize("case", WORKED["cc"], ids=lambda c: c["name"])
