@@ -149,6 +149,13 @@ typedef struct {
     float push_fraction;           /* AUTO: push when messages(s-1) < push_fraction * scanned
                                       edges of a pull superstep; default 0.04                  */
     uint32_t flags;                /* IPREGEL_RUN_* bits below; default 0                       */
+    double pagerank_tolerance;     /* < 0 (default -1): Fig. 8 exactly, k supersteps.  >= 0: run
+                                      to convergence: after each superstep s >= 1
+                                      the max over vertices of |r_s(v) - r_{s-1}(v)| is
+                                      aggregated (exact max, deterministic) and the run halts
+                                      after the first superstep where it is <= tolerance (its
+                                      broadcast is not delivered), or after superstep k.  NaN:
+                                      INVALID_ARGUMENT.  DESIGN.md reading R27.                */
 } ipregel_run_params;
 
 /* Exchange of the broadcast array between partitions after a PULL superstep (ranks of a comm,
@@ -182,6 +189,8 @@ typedef struct {
     uint64_t* messages;       /* messages sent in the superstep (sum of broadcasters' degrees)  */
     uint64_t* edges_scanned;  /* edges the superstep's delivery touched                         */
     uint64_t* model_bytes;    /* algorithmic DRAM bytes of the superstep (DESIGN.md roofline)   */
+    double* pagerank_delta;   /* PageRank: max_v |r_s(v) - r_{s-1}(v)| when run to convergence,
+                                 else 0                                                         */
 } ipregel_stats;
 
 /* ---- errors / device ---------------------------------------------------------------------- */

@@ -189,6 +189,7 @@ struct StepRecord {
     float time_ms = 0, kernel_ms = 0;
     uint8_t mode = 0;
     uint64_t changed = 0, messages = 0, edges_scanned = 0, model_bytes = 0;
+    double delta = 0.0;   // PageRank: max_v |r_s(v) - r_{s-1}(v)| (to-convergence runs)
 };
 
 }  // namespace
@@ -350,6 +351,26 @@ void exchange_owned(ipregel_graph* g, Get get) {
                                (size_t)pa.rows * sizeof(T), cudaMemcpyDeviceToDevice, g->stream));
         }
     }
+}
+
+// PageRank to convergence: max over partitions / ranks of the superstep's max per-vertex change
+// (f64 bits of a non-negative value, so the u64 max is the f64 max; exact, order-independent).
+unsigned long long reduce_max_delta(ipregel_graph* g) {
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        NC(ncclAllReduce(&p.pull_cnt->dmax, p.dscratch + 56, 1, ncclUint64, ncclMax,
+                         g->comm->nccl, g->stream));
+        CU(cudaMemcpyAsync(p.host_cnt + 3, p.dscratch + 56, 8, cudaMemcpyDeviceToHost, g->stream));
+        CU(cudaStreamSynchronize(g->stream));
+        return p.host_cnt[3];
+    }
+    for (auto& p : g->parts)
+        CU(cudaMemcpyAsync(p.host_cnt + 3, &p.pull_cnt->dmax, 8, cudaMemcpyDeviceToHost,
+                           g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    unsigned long long m = 0;
+    for (auto& p : g->parts) m = std::max(m, p.host_cnt[3]);
+    return m;
 }
 
 // Sum u64 device counters over partitions / ranks into out[0..count).
@@ -755,6 +776,10 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     const bool push = P.mode == IPREGEL_MODE_PUSH;
     const bool fused = !push && use_fused_exchange(g, IPREGEL_APP_PAGERANK, P.flags);
     g->last_exchange = exchange_kind(g, fused);
+    // to convergence (reading R27): ranks are kept every superstep and the max
+    // per-vertex change is aggregated on the device; the host halts the run once it is <= tol
+    const double tol = P.pagerank_tolerance;
+    const bool track = tol >= 0.0;
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -777,7 +802,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         AppState& S = p.st[IPREGEL_APP_PAGERANK];
         if (p.rows == 0) continue;
         k_init_pagerank<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, p.vb, inv_n,
-                                                              k > 0, last == 0, S.rank,
+                                                              k > 0, last == 0 || track, S.rank,
                                                               S.contrib[0]);
         LAUNCH_CHECK();
     }
@@ -813,10 +838,12 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     for (uint32_t step = 1; step <= k; ++step) {
         if (step == max_steps) { status = IPREGEL_ERR_MAX_SUPERSTEPS; break; }
         const int broadcast = step < k;
-        const int write_rank = step == last;
+        const int write_rank = step == last || track;
         g->steps.push_back(StepRecord{});
         StepTimer T{g, step};
         T.begin();
+        if (track)
+            for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
         T.kbegin();
         for (auto& p : g->parts) {
             AppState& S = p.st[IPREGEL_APP_PAGERANK];
@@ -832,7 +859,10 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.ratio = ratio;
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
-                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered);
+                op.track = track;
+                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr,
+                            track ? p.pull_cnt : nullptr, s, n, g->gather_policy,
+                            g->degree_ordered);
             } else {
                 k_expand<0><<<1184, kExpandThreads, 0, s>>>(
                     p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -840,7 +870,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 LAUNCH_CHECK();
                 k_pr_push_apply<<<grid_for(p.rows, 256), 256, 0, s>>>(
                     S.acc, p.csr_off, p.rows, p.vb, ratio, broadcast, write_rank, S.rank,
-                    S.contrib[1 - cur]);
+                    S.contrib[1 - cur], track ? &p.pull_cnt->dmax : nullptr);
                 LAUNCH_CHECK();
             }
         }
@@ -857,7 +887,15 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         R.messages = broadcast ? (uint64_t)g->e : 0;
         R.edges_scanned = (uint64_t)g->e;
         R.model_bytes = push ? 12ull * g->e + 24ull * n : 12ull * g->e + 16ull * n;
+        if (track) R.model_bytes += 16ull * n;   // rank read + write every superstep
         cur = 1 - cur;
+        if (track) {
+            const unsigned long long bits = reduce_max_delta(g);
+            double d;
+            memcpy(&d, &bits, 8);
+            R.delta = d;
+            if (d <= tol) break;   // master halt: converged
+        }
     }
     g->cur = cur;
     finalize_times(g);
@@ -1232,6 +1270,7 @@ ipregel_status ipregel_run_params_default(ipregel_run_params* out) {
     out->sssp_source = 0;
     out->push_fraction = 0.04f;
     out->flags = 0;
+    out->pagerank_tolerance = -1.0;
     return IPREGEL_OK;
 }
 
@@ -1469,6 +1508,8 @@ ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner c
     if (app == IPREGEL_APP_SSSP && (int64_t)P.sssp_source >= g->n)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "sssp_source %u >= N", P.sssp_source);
     if (!(P.push_fraction >= 0.0f)) fail(IPREGEL_ERR_INVALID_ARGUMENT, "push_fraction < 0");
+    if (P.pagerank_tolerance != P.pagerank_tolerance)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "pagerank_tolerance is NaN");
     if (app == IPREGEL_APP_SSSP && g->parts[0].csc_w == nullptr) {
         // unit weights (Fig. 10) -- fine
     }
@@ -1560,6 +1601,7 @@ ipregel_status ipregel_get_stats(ipregel_graph* g, ipregel_stats* st) {
         if (st->messages) st->messages[i] = R.messages;
         if (st->edges_scanned) st->edges_scanned[i] = R.edges_scanned;
         if (st->model_bytes) st->model_bytes[i] = R.model_bytes;
+        if (st->pagerank_delta) st->pagerank_delta[i] = R.delta;
     }
     return IPREGEL_OK;
     ABI_END

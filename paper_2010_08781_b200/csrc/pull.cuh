@@ -43,6 +43,7 @@ constexpr int kRangeItems = 4096;                 // merge items (edges + rows) 
 struct PullCounters {
     unsigned long long changed;
     unsigned long long messages;
+    unsigned long long dmax;   // PageRank to convergence: max |r_s - r_{s-1}| as f64 bits (>= 0)
 };
 
 // Range plan for one adjacency of one partition.
@@ -139,12 +140,18 @@ struct PageRankPull : SumF64 {
     double ratio;
     int broadcast;                            // s < k
     int write_rank;
+    int track;                                // to convergence: rank holds r_{s-1}; fold |dr|
     const void* gather_base() const { return contrib_cur; }
     __device__ const T* gptr() const { return contrib_cur; }
     __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t) { return g; }
-    __device__ void finish(int32_t row, T sum, PullCounters&) const {
+    __device__ void finish(int32_t row, T sum, PullCounters& c) const {
         const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
+        if (track) {   // max aggregator of the per-vertex change (reading R27)
+            const unsigned long long d =
+                (unsigned long long)__double_as_longlong(fabs(__dsub_rn(r, rank[row])));
+            c.dmax = d > c.dmax ? d : c.dmax;
+        }
         if (write_rank) rank[row] = r;
         if (broadcast) {
             const int32_t deg = out_off[row + 1] - out_off[row];
@@ -309,20 +316,24 @@ struct RangeArgs {
 __device__ __forceinline__ void flush_counters(const PullCounters& cnt, unsigned long long* s_cnt,
                                                PullCounters* counters) {
     const int lane = threadIdx.x & 31;
-    unsigned long long c0 = cnt.changed, c1 = cnt.messages;
+    unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         c0 += __shfl_xor_sync(kFull, c0, d);
         c1 += __shfl_xor_sync(kFull, c1, d);
+        const unsigned long long o = __shfl_xor_sync(kFull, c2, d);
+        c2 = o > c2 ? o : c2;
     }
-    if (lane == 0 && (c0 | c1)) {
+    if (lane == 0 && (c0 | c1 | c2)) {
         atomicAdd(&s_cnt[0], c0);
         atomicAdd(&s_cnt[1], c1);
+        atomicMax(&s_cnt[2], c2);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1])) {
+    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1] | s_cnt[2])) {
         atomicAdd(&counters->changed, s_cnt[0]);
         atomicAdd(&counters->messages, s_cnt[1]);
+        atomicMax(&counters->dmax, s_cnt[2]);
     }
 }
 
@@ -512,12 +523,12 @@ template <class Op>
 __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_ranges(Op op, RangeArgs A) {
     using T = typename Op::T;
     __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums by position (conflict-free)
-    __shared__ unsigned long long s_cnt[2];
+    __shared__ unsigned long long s_cnt[3];
     const int wid = threadIdx.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    PullCounters cnt{0, 0};
+    PullCounters cnt{0, 0, 0};
     if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
     flush_counters(cnt, s_cnt, A.counters);
 }
@@ -544,11 +555,12 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     }
     if (lane == 0) {
         acc = Op::combine(acc, head[G.z]);
-        PullCounters c{0, 0};
+        PullCounters c{0, 0, 0};
         op.finish(G.x, acc, c);
-        if (counters && (c.changed | c.messages)) {
+        if (counters && (c.changed | c.messages | c.dmax)) {
             atomicAdd(&counters->changed, c.changed);
             atomicAdd(&counters->messages, c.messages);
+            atomicMax(&counters->dmax, c.dmax);
         }
     }
 }

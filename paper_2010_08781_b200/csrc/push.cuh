@@ -358,13 +358,28 @@ __global__ void k_bitmap_from_diff(const uint32_t* __restrict__ before,
 }
 
 // PageRank push apply: r = ratio + 0.85 * acc; next contribution; reset the accumulator.
+// dmax != NULL (to convergence): rank holds r_{s-1}; fold max |r_s - r_{s-1}| (reading R27).
 __global__ void k_pr_push_apply(double* __restrict__ acc, const int32_t* __restrict__ out_off,
                                 int64_t rows, int64_t vbase, double ratio, int broadcast,
                                 int write_rank, double* __restrict__ rank,
-                                double* __restrict__ contrib_next) {
+                                double* __restrict__ contrib_next,
+                                unsigned long long* __restrict__ dmax) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double r = 0.0;
+    unsigned long long d = 0;
+    if (i < rows) {
+        r = __dadd_rn(ratio, __dmul_rn(0.85, acc[i]));
+        if (dmax) d = (unsigned long long)__double_as_longlong(fabs(__dsub_rn(r, rank[i])));
+    }
+    if (dmax) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(kFull, d, o);
+            d = x > d ? x : d;
+        }
+        if ((threadIdx.x & 31) == 0 && d) atomicMax(dmax, d);
+    }
     if (i >= rows) return;
-    const double r = __dadd_rn(ratio, __dmul_rn(0.85, acc[i]));
     acc[i] = 0.0;
     if (write_rank) rank[i] = r;
     if (broadcast) {

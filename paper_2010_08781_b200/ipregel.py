@@ -64,7 +64,7 @@ class GraphDesc(ctypes.Structure):
 class RunParams(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("pagerank_iterations", ctypes.c_uint32),
                 ("sssp_source", ctypes.c_uint32), ("push_fraction", ctypes.c_float),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("pagerank_tolerance", ctypes.c_double)]
 
 
 class Stats(ctypes.Structure):
@@ -73,7 +73,7 @@ class Stats(ctypes.Structure):
                 ("time_ms", ctypes.c_void_p), ("kernel_ms", ctypes.c_void_p),
                 ("mode", ctypes.c_void_p), ("changed", ctypes.c_void_p),
                 ("messages", ctypes.c_void_p), ("edges_scanned", ctypes.c_void_p),
-                ("model_bytes", ctypes.c_void_p)]
+                ("model_bytes", ctypes.c_void_p), ("pagerank_delta", ctypes.c_void_p)]
 
 
 # every symbol include/ipregel.h declares (tests check the library exports all of them)
@@ -298,7 +298,7 @@ class Graph:
 
     def run(self, app, max_supersteps: int = 1 << 30, mode="auto", iterations: int = 10,
             source: int = 0, push_fraction: float = 0.04, combiner=None,
-            allow_guard: bool = False, exchange: str = "auto") -> int:
+            allow_guard: bool = False, exchange: str = "auto", tolerance: float = -1.0) -> int:
         app = APPS[app] if isinstance(app, str) else int(app)
         p = run_params_default()
         p.mode = MODES[mode] if isinstance(mode, str) else int(mode)
@@ -306,6 +306,7 @@ class Graph:
         p.sssp_source = source
         p.push_fraction = push_fraction
         p.flags = EXCHANGES[exchange]
+        p.pagerank_tolerance = tolerance
         comb = COMBINER_OF.get(app, COMBINE_SUM) if combiner is None else combiner
         st = load().ipregel_run(self.handle, app, comb, max_supersteps, ctypes.byref(p))
         _check(st, "ipregel_run", allow=(ERR_MAX_SUPERSTEPS,) if allow_guard else ())
@@ -337,6 +338,7 @@ class Graph:
             "messages": np.zeros(capacity, np.uint64),
             "edges_scanned": np.zeros(capacity, np.uint64),
             "model_bytes": np.zeros(capacity, np.uint64),
+            "pagerank_delta": np.zeros(capacity, np.float64),
         }
         st = Stats()
         st.capacity = capacity

@@ -44,6 +44,31 @@ def test_run_params_default():
     p = ipr.run_params_default()
     assert (p.mode, p.pagerank_iterations, p.sssp_source, p.flags) == (ipr.MODE_AUTO, 10, 0, 0)
     assert abs(p.push_fraction - 0.04) < 1e-7
+    assert p.pagerank_tolerance == -1.0
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """sizeof/offsetof of every ABI struct from the C compiler equal the ctypes binding's."""
+    import subprocess
+    structs = {"ipregel_graph_desc": ipr.ipregel.GraphDesc, "ipregel_run_params": ipr.RunParams,
+               "ipregel_stats": ipr.ipregel.Stats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.abspath(HEADER)}"',
+             "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("%zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-o", str(exe), str(src)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = []
+    for cls in structs.values():
+        want.append(ctypes.sizeof(cls))
+        want += [getattr(cls, f).offset for f, _ in cls._fields_]
+    assert got == want
 
 
 def test_partition_edge_balanced():

@@ -475,3 +475,88 @@ def test_nccl_path_single_rank_matches_oracle(exchange):
         np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
     G.close()
     comm.close()
+
+
+# ------------------------------------------------------------------ PageRank to convergence
+
+def _pr_tol_case(seed):
+    rng = np.random.default_rng(6100 + seed)
+    n = int(rng.integers(50, 3000))
+    src, dst, _ = checkers.random_graph(rng, n, int(rng.integers(2 * n, 8 * n)))
+    full = oracle.pagerank(n, src, dst, k=60)
+    dl = full["delta"]
+    # a tolerance geometrically between two well-separated deltas, so rounding order cannot
+    # move the stopping superstep
+    cand = [t for t in range(2, 60) if 0 < dl[t] < 0.5 * dl[t - 1] and dl[t] > 1e-13]
+    t = cand[len(cand) // 2] if cand else 3
+    return n, src, dst, float(np.sqrt(dl[t] * dl[t - 1]))
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("mode,parts", [("pull", 1), ("push", 1), ("pull", 3)])
+def test_pagerank_to_convergence_matches_oracle(seed, mode, parts):
+    n, src, dst, tol = _pr_tol_case(seed)
+    o = oracle.pagerank(n, src, dst, k=60, tol=tol)
+    assert o["supersteps"] < 61
+    g = csr_csc(n, src, dst)
+    G = make_graph(g, partitions=parts, weighted=False)
+    G.run("pagerank", mode=mode, iterations=60, tolerance=tol)
+    v = G.values(host=True)
+    s = G.stats()
+    assert s["supersteps"] == o["supersteps"]
+    assert np.abs(v - o["values"]).max() <= PR_ABS
+    rel = np.abs(v - o["values"]) / np.maximum(np.abs(o["values"]), 1e-300)
+    assert rel.max() <= PR_REL
+    np.testing.assert_allclose(s["pagerank_delta"], o["delta"], rtol=1e-9, atol=1e-16)
+    np.testing.assert_array_equal(s["messages"], o["messages"])
+    G.close()
+
+
+def test_pagerank_to_convergence_closed_forms_and_k_cap():
+    # in-star: delta_3 == 0 exactly -> 4 supersteps with tol = 0 (tests/test_oracle_pins.py)
+    n = 1000
+    leaves = np.arange(1, n)
+    G = make_graph(csr_csc(n, leaves, np.zeros(n - 1, np.int64)), weighted=False)
+    G.run("pagerank", mode="pull", iterations=10, tolerance=0.0)
+    s = G.stats()
+    assert s["supersteps"] == 4 and s["pagerank_delta"][3] == 0.0
+    G.close()
+    # an unreachable tolerance: Fig. 8's k wins and values equal the plain run
+    rng = np.random.default_rng(12)
+    src, dst, _ = checkers.random_graph(rng, 500, 3000)
+    G = make_graph(csr_csc(500, src, dst), weighted=False)
+    G.run("pagerank", mode="pull", iterations=10, tolerance=1e-300)
+    a = G.values(host=True)
+    assert G.stats()["supersteps"] == 11
+    G.run("pagerank", mode="pull", iterations=10)
+    np.testing.assert_array_equal(a, G.values(host=True))
+    assert not G.stats()["pagerank_delta"].any()
+    import paper_2010_08781_b200 as ipr
+    with pytest.raises(ipr.IpregelError) as e:
+        G.run("pagerank", tolerance=float("nan"))
+    assert e.value.status == ipr.ERR_INVALID_ARGUMENT
+    G.close()
+
+
+def test_pagerank_to_convergence_cfg3_scale():
+    """BASELINE configs[3]'s graph (R-MAT scale 22, ef 28, seed 4) to convergence at 1e-10."""
+    import inputs
+    from inputs.gpu import config_graph_device
+    import paper_2010_08781_b200 as ipr
+    cfg = inputs.CONFIGS["cfg3"]
+    src, dst, _ = inputs.rmat_coo(cfg.scale, cfg.edgefactor, cfg.seed)
+    o = oracle.pagerank(cfg.n, src, dst, k=100, tol=1e-10)
+    g = config_graph_device(cfg, degree_order=True)
+    G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
+                                     g["csr_idx"], None, None, g["vertex_ids"], degree_ordered=True))
+    G.run("pagerank", mode="pull", iterations=100, tolerance=1e-10)
+    s = G.stats()
+    d = o["delta"]
+    # the stopping decision is robust only if no delta sits within rounding of the tolerance
+    assert np.all(np.abs(d[1:] - 1e-10) > 1e-14)
+    assert s["supersteps"] == o["supersteps"]
+    v = G.values(host=True)
+    assert np.abs(v - o["values"]).max() <= PR_ABS
+    # deltas are differences of f64 sums taken in another order: equal up to ~1e-16 absolute
+    np.testing.assert_allclose(s["pagerank_delta"], d, rtol=1e-9, atol=1e-15)
+    G.close()
