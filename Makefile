@@ -16,10 +16,15 @@ LIB_ORACLE   := oracle/liboracle.so
 all: $(LIB_IPREGEL) $(LIB_RMAT_GPU) $(LIB_RMAT_CPU) $(LIB_ORACLE)
 
 IPREGEL_SRC := paper_2010_08781_b200/csrc/ipregel.cu $(wildcard paper_2010_08781_b200/csrc/*.cuh) include/ipregel.h
+JIT_INC := paper_2010_08781_b200/csrc/jit_headers.inc
 
-$(LIB_IPREGEL): $(IPREGEL_SRC)
+# the device headers, embedded for NVRTC compilation of user vertex programs (program.cuh)
+$(JIT_INC): $(wildcard paper_2010_08781_b200/csrc/*.cuh) paper_2010_08781_b200/csrc/embed_headers.py
+	python paper_2010_08781_b200/csrc/embed_headers.py $@
+
+$(LIB_IPREGEL): $(IPREGEL_SRC) $(JIT_INC)
 	$(NVCC) $(NVFLAGS) -I$(NCCL_DIR)/include -o $@ paper_2010_08781_b200/csrc/ipregel.cu \
-	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib
+	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib -ldl
 
 $(LIB_RMAT_GPU): inputs/rmat_gpu.cu
 	$(NVCC) $(NVFLAGS) -o $@ $<
@@ -32,6 +37,6 @@ $(LIB_ORACLE): oracle/oracle.c
 	$(CC) -O2 -std=c99 -D_POSIX_C_SOURCE=199309L -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $<
 
 clean:
-	rm -f $(LIB_IPREGEL) $(LIB_RMAT_GPU) $(LIB_RMAT_CPU) $(LIB_ORACLE)
+	rm -f $(JIT_INC) $(LIB_IPREGEL) $(LIB_RMAT_GPU) $(LIB_RMAT_CPU) $(LIB_ORACLE)
 
 .PHONY: all clean

@@ -74,8 +74,9 @@ typedef enum {
                                    IPREGEL_INF (0xFFFFFFFF) if unreachable; sums saturate      */
 } ipregel_app;
 
-/* Fig. 1's combine: Fig. 8 sums; Fig. 5 keeps the minimum (:213-221). */
-typedef enum { IPREGEL_COMBINE_SUM = 0, IPREGEL_COMBINE_MIN = 1 } ipregel_combiner;
+/* Fig. 1's combine: Fig. 8 sums; Fig. 5 keeps the minimum (:213-221).  MAX is
+ * available to user programs (ipregel_program_desc). */
+typedef enum { IPREGEL_COMBINE_SUM = 0, IPREGEL_COMBINE_MIN = 1, IPREGEL_COMBINE_MAX = 2 } ipregel_combiner;
 
 /* Message delivery (Sec. 4.3.2).  PULL: every recipient gathers from its
  * in-neighbours' outboxes (CSC gather-combine).  PUSH: every sender in the frontier folds its
@@ -95,6 +96,7 @@ typedef enum {
 #define IPREGEL_INF 0xFFFFFFFFu
 
 typedef struct ipregel_graph ipregel_graph; /* opaque */
+typedef struct ipregel_program ipregel_program; /* opaque: a compiled user vertex program */
 typedef struct ipregel_comm ipregel_comm;   /* opaque; NULL means a single GPU */
 
 /*
@@ -251,13 +253,74 @@ ipregel_status ipregel_run(ipregel_graph* graph, ipregel_app app, ipregel_combin
                            uint32_t max_supersteps, const ipregel_run_params* params);
 
 /* Copies the full N-vertex result of the last run into `out` (host or device memory per
- * out_is_device).  out_bytes must be N * 8 (PageRank) or N * 4 (CC, SSSP).  Multi-GPU: every
+ * out_is_device).  out_bytes must be N * 8 (PageRank, f64 programs) or N * 4 (CC, SSSP, u32
+ * programs).  Multi-GPU: every
  * rank receives all N values (collective). */
 ipregel_status ipregel_get_values(ipregel_graph* graph, void* out, size_t out_bytes,
                                   int out_is_device);
 
 /* Fills the caller-owned arrays of *inout (up to capacity entries) for the last run. */
 ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
+
+/* ---- user vertex programs (Fig. 1: the user supplies compute and combine) --------- */
+/*
+ * A program is CUDA C++ source compiled at run time (NVRTC, sm_100a, IEEE arithmetic as
+ * written: no FMA contraction) together with the library's own superstep kernels, which are
+ * then instantiated on it (pull: merge-path CSC gather-combine with compute in the epilogue;
+ * push: atomic combine into single-slot mailboxes; AUTO switch, fused exchange, partitions and
+ * ranks -- everything ipregel_run does).  Values, messages and mailboxes share one type
+ * `ipr_value_t` (value_type).  The source must define:
+ *
+ *   __device__ unsigned ipr_init(const ipr_ctx& c, ipr_value_t* value, ipr_value_t* message);
+ *       superstep 0: set *value (and *message); return flags.
+ *   __device__ unsigned ipr_compute(const ipr_ctx& c, ipr_value_t* value, ipr_value_t mailbox,
+ *                                   ipr_value_t* message);
+ *       superstep s >= 1: mailbox = the combiner's fold of the messages received, its identity
+ *       if none (SUM 0, MIN the type's max / +inf, MAX 0 / -inf); update *value; return flags.
+ *   __device__ ipr_value_t ipr_edge(ipr_value_t message, unsigned weight);
+ *       the message as delivered along one edge (weight 1 when the graph has none); must map
+ *       the combiner's identity to itself (e.g. SSSP: ipr_sat_add(message, weight)).
+ *
+ * Flags: IPR_BROADCAST = send *message to every out-neighbour (with symmetric = 1
+ * to every in- and out-neighbour); IPR_STAY_ACTIVE = do not vote to halt.
+ * ipr_ctx (read-only): id (ORIGINAL vertex id under a relabelled layout), num_vertices,
+ * superstep, out_degree, in_degree, params[0..7] (the run's program parameters, 0 if unset).
+ * Helpers: ipr_sat_add(a, b) (u32, saturating at IPR_INF_U32 = 0xFFFFFFFF).
+ * The run ends when a superstep has no broadcast and no active vertex.
+ * Selection (R28): push supersteps run compute on recipients and active vertices
+ * only; pull supersteps run it on every vertex, the non-recipients getting the identity, so a
+ * halted vertex given the identity must leave its value and not broadcast (Figs. 8-10 do).
+ * The combiner (SUM, MIN, MAX) must be what the program folds with: it is applied in a fixed
+ * order in pull mode and by atomics in push mode (SUM f64 in push is order-nondeterministic).
+ */
+typedef enum { IPREGEL_VALUE_U32 = 0, IPREGEL_VALUE_F64 = 1 } ipregel_value_type;
+
+typedef struct {
+    const char* source;   /* NUL-terminated CUDA C++ source (copied; the caller keeps ownership) */
+    int32_t value_type;   /* ipregel_value_type                                                 */
+    int32_t combiner;     /* ipregel_combiner                                                   */
+    int32_t symmetric;    /* 1: messages travel along every edge in both directions (Hash-Min's
+                             neighbourhood; the graph's CSR row U CSC row), 0: out-edges only   */
+    int32_t reserved;     /* must be 0                                                          */
+} ipregel_program_desc;
+
+/* Compiles the program (host only; no GPU needed).  A compile error returns INVALID_ARGUMENT
+ * with the NVRTC log in ipregel_last_error(); UNSUPPORTED if NVRTC is not installed.  The
+ * kernels are loaded on the current device at the first run. */
+ipregel_status ipregel_program_create(const ipregel_program_desc* desc, ipregel_program** out);
+/* NVRTC log of the successful compile (warnings), never NULL; owned by the program. */
+const char* ipregel_program_log(const ipregel_program* program);
+/* Size of the compiled sm_100a CUBIN (diagnostic). */
+uint64_t ipregel_program_cubin_bytes(const ipregel_program* program);
+void ipregel_program_destroy(ipregel_program* program);
+
+/* Runs `program` on the graph like ipregel_run (same params: mode, push_fraction, exchange
+ * flags; pagerank_* fields are ignored).  program_params: up to 8 doubles visible as
+ * ipr_ctx.params (NULL / 0 = all zero).  ipregel_get_values then returns N values of the
+ * program's value_type; ipregel_get_stats the per-superstep record.  Collective across ranks. */
+ipregel_status ipregel_run_program(ipregel_graph* graph, ipregel_program* program,
+                                   uint32_t max_supersteps, const ipregel_run_params* params,
+                                   const double* program_params, int num_program_params);
 
 #ifdef __cplusplus
 }

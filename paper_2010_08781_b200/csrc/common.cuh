@@ -1,8 +1,25 @@
 // paper_2010_08781_b200/csrc/common.cuh -- device helpers shared by the superstep kernels.
 // sm_100a only (compiled with -gencode arch=compute_100a,code=sm_100a).
 #pragma once
+#ifdef __CUDACC_RTC__
+// compiled at run time by NVRTC together with a user vertex program (program.cuh): no host
+// headers are available there
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#ifndef INT_MAX
+#define INT_MAX 2147483647
+#endif
+#else
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace ipr {
 

@@ -8,7 +8,9 @@
 // partitions, and the host reads the counters to decide termination ("every active vertex has
 // been processed and every outgoing message delivered").
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
+#include <nvrtc.h>
 
 #include <algorithm>
 #include <atomic>
@@ -24,7 +26,9 @@
 #include "common.cuh"
 #include "pull.cuh"
 #include "push.cuh"
+#include "program.cuh"
 #include "setup.cuh"
+#include "jit_headers.inc"
 
 using namespace ipr;
 
@@ -160,8 +164,17 @@ struct AppState {
     int npeer = 0;
     int peers_state = 0;                       // 0 not set up, 1 reachable, -1 not reachable
     std::vector<void*> ipc_opened;
+    // user vertex programs (app slot kAppProgram): 8-byte slots hold u32 or f64 values
+    void* pv_value = nullptr;                  // owned values [rows]
+    void* pv_out[2] = {nullptr, nullptr};      // outbox replicas [N] (identity = no broadcast)
+    void* pv_mbox = nullptr;                   // owned mailboxes [rows]
+    uint8_t* pv_active = nullptr;              // owned: did not vote to halt
+    uint32_t* pv_recv = nullptr;               // owned recipient bitmap (push)
+    double* pv_params = nullptr;               // program parameters [8]
     DeviceBuffers mem;
 };
+
+constexpr int kAppProgram = 3;   // app slot of user programs (after the paper's three)
 
 struct Partition {
     int64_t vb = 0, ve = 0, rows = 0;
@@ -178,7 +191,7 @@ struct Partition {
     bool push_view_ready = false;
     int64_t nondangling = 0;
     DeviceBuffers graph_mem;      // host copies, tile plans, push view
-    AppState st[3];
+    AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
     unsigned long long* host_cnt = nullptr;   // pinned [16]
@@ -202,7 +215,8 @@ struct ipregel_graph {
     std::vector<Partition> parts;
     std::vector<int64_t> rank_vb, rank_rows;  // multi-GPU: every rank's owned range
     bool poisoned = false;
-    int last_app = -1;
+    int last_app = -1;             // ipregel_app, or kAppProgram
+    int last_vsz = 0;              // value bytes of the last run (8 PageRank / f64, 4 u32)
     int last_status = -1;
     int last_exchange = 0;         // 0 none, 1 collective, 2 fused
     int cur = 0;
@@ -281,13 +295,32 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
     }
 }
 
+RangeArgs range_args(const TilePlan& P, const int32_t* off, const int32_t* idx, const uint32_t* w,
+                     PullCounters* cnt, cudaStream_t s, const void* gbase, int64_t n_global,
+                     size_t vsz, int policy, bool degree_ordered);
+
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
                  const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global,
                  int policy, bool degree_ordered) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
-    const uint64_t total = std::min<uint64_t>((uint64_t)n_global * sizeof(T), 0xFFFFFFFFull);
+    RangeArgs A = range_args(P, off, idx, w, cnt, s, op.gather_base(), n_global, sizeof(T), policy,
+                             degree_ordered);
+    k_pull_ranges<Op><<<(unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads, 0, s>>>(op, A);
+    LAUNCH_CHECK();
+    if (P.num_groups) {
+        k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
+            op, P.groups, P.num_groups, static_cast<const T*>(P.carry),
+            static_cast<const T*>(P.head), cnt);
+        LAUNCH_CHECK();
+    }
+}
+
+RangeArgs range_args(const TilePlan& P, const int32_t* off, const int32_t* idx, const uint32_t* w,
+                     PullCounters* cnt, cudaStream_t s, const void* gbase, int64_t n_global,
+                     size_t vsz, int policy, bool degree_ordered) {
+    const uint64_t total = std::min<uint64_t>((uint64_t)n_global * vsz, 0xFFFFFFFFull);
     const uint32_t hot = (uint32_t)std::min<uint64_t>(g_hot_bytes, total);
     if (g_persist_bytes) {
         static bool limit_set = false;
@@ -296,7 +329,7 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
             limit_set = true;
         }
         cudaStreamAttrValue a = {};
-        a.accessPolicyWindow.base_ptr = const_cast<void*>(op.gather_base());
+        a.accessPolicyWindow.base_ptr = const_cast<void*>(gbase);
         a.accessPolicyWindow.num_bytes = std::min<uint64_t>(g_persist_bytes, total);
         a.accessPolicyWindow.hitRatio = 1.0f;
         a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -306,17 +339,10 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
     RangeArgs A;
     A.off = off; A.idx = idx; A.wts = w; A.cx = P.cx; A.cy = P.cy; A.rows = P.rows;
     A.cphase = (int32_t)P.cphase; A.num_ranges = P.num_tiles; A.carry_out = P.carry;
-    A.head_out = P.head; A.counters = cnt; A.gather_policy = policy; A.gbase = op.gather_base();
+    A.head_out = P.head; A.counters = cnt; A.gather_policy = policy; A.gbase = gbase;
     A.ghot = hot; A.gtotal = (uint32_t)total;
-    A.l1hot = g_l1_hot != -2 ? g_l1_hot : (degree_ordered ? (int32_t)(65536 / sizeof(T)) : -1);
-    k_pull_ranges<Op><<<(unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads, 0, s>>>(op, A);
-    LAUNCH_CHECK();
-    if (P.num_groups) {
-        k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
-            op, P.groups, P.num_groups, static_cast<const T*>(P.carry),
-            static_cast<const T*>(P.head), cnt);
-        LAUNCH_CHECK();
-    }
+    A.l1hot = g_l1_hot != -2 ? g_l1_hot : (degree_ordered ? (int32_t)(65536 / vsz) : -1);
+    return A;
 }
 
 template <class T>
@@ -409,6 +435,26 @@ void ensure_state(ipregel_graph* g, int app) {
             S.rank = S.mem.alloc<double>(p.rows, s);
             S.contrib[0] = S.mem.alloc<double>(n, s, true);
             S.contrib[1] = S.mem.alloc<double>(n, s, true);
+        } else if (app == kAppProgram) {
+            S.pv_value = S.mem.alloc<uint64_t>(p.rows, s, true);
+            S.pv_out[0] = S.mem.alloc<uint64_t>(n, s, true);
+            S.pv_out[1] = S.mem.alloc<uint64_t>(n, s, true);
+            S.pv_mbox = S.mem.alloc<uint64_t>(p.rows, s, true);
+            S.pv_active = S.mem.alloc<uint8_t>(p.rows, s, true);
+            S.pv_recv = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
+            S.pv_params = S.mem.alloc<double>(kProgParams, s, true);
+            S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
+            S.f_id = S.mem.alloc<int32_t>(p.rows, s);
+            S.f_val = S.mem.alloc<uint32_t>(p.rows, s);
+            if (g->parts.size() > 1 || multi_rank(g)) {
+                S.g_id = S.mem.alloc<int32_t>(n, s);
+                S.g_val = S.mem.alloc<uint32_t>(n, s);
+                S.g_len = S.mem.alloc<unsigned long long>(1, s, true);
+            } else {
+                S.g_id = S.f_id;
+                S.g_val = S.f_val;
+                S.g_len = &p.front_cnt->changed;
+            }
         } else {
             S.val[0] = S.mem.alloc<uint32_t>(n, s);
             S.val[1] = S.mem.alloc<uint32_t>(n, s);
@@ -461,8 +507,8 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
     if (g->parts.size() == 1 && !multi_rank(g)) {
-        p.push_sssp = PushAdj{p.csr_off, p.csr_idx, p.csr_w, nullptr, nullptr, 0, n};
-        p.push_cc = PushAdj{p.csr_off, p.csr_idx, nullptr, p.csc_off, p.csc_idx, 0, n};
+        p.push_sssp = PushAdj{p.csr_off, p.csr_idx, p.csr_w, nullptr, nullptr, nullptr, 0, n};
+        p.push_cc = PushAdj{p.csr_off, p.csr_idx, p.csr_w, p.csc_off, p.csc_idx, p.csc_w, 0, n};
         p.push_view_ready = true;
         return;
     }
@@ -492,11 +538,11 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
         if (out_w) *out_w = wx;
     };
     int32_t *o1, *i1, *o2, *i2;
-    uint32_t* w1 = nullptr;
+    uint32_t *w1 = nullptr, *w2 = nullptr;
     transpose(p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, &o1, &i1, &w1);
-    transpose(p.csr_off, p.csr_idx, nullptr, p.csr_edges, false, &o2, &i2, nullptr);
-    p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, 0, n};
-    p.push_cc = PushAdj{o1, i1, nullptr, o2, i2, 0, n};
+    transpose(p.csr_off, p.csr_idx, p.csr_w, p.csr_edges, p.csr_w != nullptr, &o2, &i2, &w2);
+    p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, nullptr, 0, n};
+    p.push_cc = PushAdj{o1, i1, w1, o2, i2, w2, 0, n};
     p.push_view_ready = true;
 }
 
@@ -522,6 +568,8 @@ void compact_bitmap(ipregel_graph* g, Partition& p, AppState& S, const uint32_t*
 void exchange_frontier(ipregel_graph* g, int app, const std::vector<unsigned long long>& counts,
                        int cur) {
     auto replica = [app](Partition& p, int w) { return p.st[app].val[w]; };
+    // user programs read broadcast payloads from their (exchanged) outbox replicas: ids only
+    const bool scatter = app != kAppProgram;
     cudaStream_t s = g->stream;
     if (multi_rank(g)) {
         Partition& p = g->parts[0];
@@ -539,10 +587,12 @@ void exchange_frontier(ipregel_graph* g, int app, const std::vector<unsigned lon
         }
         NC(ncclGroupEnd());
         CU(cudaMemcpyAsync(S.g_len, &total, sizeof(total), cudaMemcpyHostToDevice, s));
-        k_scatter_frontier<<<grid_for(std::max<unsigned long long>(total, 1ull), 256) > 2048
-                                 ? 2048 : grid_for(std::max<unsigned long long>(total, 1ull), 256),
-                             256, 0, s>>>(S.g_id, S.g_val, S.g_len, replica(p, cur));
-        LAUNCH_CHECK();
+        if (scatter) {
+            k_scatter_frontier<<<grid_for(std::max<unsigned long long>(total, 1ull), 256) > 2048
+                                     ? 2048 : grid_for(std::max<unsigned long long>(total, 1ull), 256),
+                                 256, 0, s>>>(S.g_id, S.g_val, S.g_len, replica(p, cur));
+            LAUNCH_CHECK();
+        }
         CU(cudaStreamSynchronize(s));  // `total` lives on the host stack
         return;
     }
@@ -562,10 +612,12 @@ void exchange_frontier(ipregel_graph* g, int app, const std::vector<unsigned lon
                                cudaMemcpyDeviceToDevice, s));
         }
         CU(cudaMemcpyAsync(Sb.g_len, &total, sizeof(total), cudaMemcpyHostToDevice, s));
-        unsigned gr = grid_for(std::max<unsigned long long>(total, 1ull), 256);
-        k_scatter_frontier<<<gr > 2048 ? 2048 : gr, 256, 0, s>>>(Sb.g_id, Sb.g_val, Sb.g_len,
-                                                                replica(g->parts[b], cur));
-        LAUNCH_CHECK();
+        if (scatter) {
+            unsigned gr = grid_for(std::max<unsigned long long>(total, 1ull), 256);
+            k_scatter_frontier<<<gr > 2048 ? 2048 : gr, 256, 0, s>>>(Sb.g_id, Sb.g_val, Sb.g_len,
+                                                                    replica(g->parts[b], cur));
+            LAUNCH_CHECK();
+        }
     }
     CU(cudaStreamSynchronize(s));  // `total` lives on the host stack
 }
@@ -609,6 +661,7 @@ std::vector<unsigned long long> frontier_counts(ipregel_graph* g) {
 
 // ---- fused exchange ----------------------------------------------------
 void* replica_buf(AppState& S, int app, int w) {
+    if (app == kAppProgram) return S.pv_out[w];
     return app == IPREGEL_APP_PAGERANK ? (void*)S.contrib[w] : (void*)S.val[w];
 }
 
@@ -1215,6 +1268,343 @@ void destroy_graph(ipregel_graph* g) {
 }  // namespace
 
 // =============================================================================================
+// user vertex programs: NVRTC compilation and the generic superstep loop
+// =============================================================================================
+enum { PK_INIT, PK_PULL0, PK_PULL1, PK_PULL2, PK_FIX0, PK_FIX1, PK_FIX2, PK_EXPAND, PK_APPLY,
+       PK_COUNT };
+static const char* const kProgKernelNames[PK_COUNT] = {
+    "ipr::k_prog_init<UserProgram>",
+    "ipr::k_pull_ranges<ipr::ProgPull<UserProgram, 0> >",
+    "ipr::k_pull_ranges<ipr::ProgPull<UserProgram, 1> >",
+    "ipr::k_pull_ranges<ipr::ProgPull<UserProgram, 2> >",
+    "ipr::k_pull_fixup<ipr::ProgPull<UserProgram, 0> >",
+    "ipr::k_pull_fixup<ipr::ProgPull<UserProgram, 1> >",
+    "ipr::k_pull_fixup<ipr::ProgPull<UserProgram, 2> >",
+    "ipr::k_prog_expand<UserProgram>",
+    "ipr::k_prog_apply<UserProgram>",
+};
+
+struct ipregel_program {
+    int value_type = 0;   // ipregel_value_type
+    int combiner = 0;     // ipregel_combiner
+    int sym = 0;
+    std::vector<char> cubin;
+    std::string log;
+    std::string lowered[PK_COUNT];
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t k[PK_COUNT] = {};
+};
+
+namespace {
+
+// NVRTC is loaded on first use (dlopen), so the library itself loads without it.
+struct Nvrtc {
+    bool ok = false;
+    std::string why;
+    nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*,
+                          const char* const*) = nullptr;
+    nvrtcResult (*add_name)(nvrtcProgram, const char*) = nullptr;
+    nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+    nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*lowered)(nvrtcProgram, const char*, const char**) = nullptr;
+    nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+    const char* (*err)(nvrtcResult) = nullptr;
+};
+
+Nvrtc load_nvrtc() {
+    Nvrtc N;
+    const char* cands[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+    void* h = nullptr;
+    for (const char* c : cands)
+        if ((h = dlopen(c, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
+    if (!h) {
+        N.why = "libnvrtc.so.12 not found";
+        return N;
+    }
+    bool ok = true;
+    auto sym = [&](const char* name) {
+        void* f = dlsym(h, name);
+        if (!f) ok = false;
+        return f;
+    };
+    N.create = (decltype(N.create))sym("nvrtcCreateProgram");
+    N.add_name = (decltype(N.add_name))sym("nvrtcAddNameExpression");
+    N.compile = (decltype(N.compile))sym("nvrtcCompileProgram");
+    N.log_size = (decltype(N.log_size))sym("nvrtcGetProgramLogSize");
+    N.log = (decltype(N.log))sym("nvrtcGetProgramLog");
+    N.cubin_size = (decltype(N.cubin_size))sym("nvrtcGetCUBINSize");
+    N.cubin = (decltype(N.cubin))sym("nvrtcGetCUBIN");
+    N.lowered = (decltype(N.lowered))sym("nvrtcGetLoweredName");
+    N.destroy = (decltype(N.destroy))sym("nvrtcDestroyProgram");
+    N.err = (decltype(N.err))sym("nvrtcGetErrorString");
+    N.ok = ok;
+    if (!ok) N.why = "libnvrtc lacks a required symbol";
+    return N;
+}
+
+const Nvrtc& nvrtc() {
+    static Nvrtc N = load_nvrtc();
+    return N;
+}
+
+// The translation unit NVRTC compiles: the library's own device headers, the user source, and
+// the adapter the kernel templates are instantiated on.
+std::string program_tu(const ipregel_program_desc& d) {
+    const char* vt = d.value_type == IPREGEL_VALUE_F64 ? "double" : "unsigned int";
+    std::string s;
+    s += "#include \"program.cuh\"\n";
+    s += "typedef ipr::ProgCtx ipr_ctx;\n";
+    s += std::string("typedef ") + vt + " ipr_value_t;\n";
+    s += "#define IPR_BROADCAST 1u\n#define IPR_STAY_ACTIVE 2u\n#define IPR_INF_U32 0xFFFFFFFFu\n";
+    s += "__device__ __forceinline__ unsigned ipr_sat_add(unsigned a, unsigned b) "
+         "{ return ipr::sat_add(a, b); }\n";
+    s += "#line 1 \"user_program.cu\"\n";
+    s += d.source;
+    s += "\n#line 1 \"ipregel_program_adapter\"\n";
+    s += "struct UserProgram {\n  typedef ipr_value_t V;\n";
+    s += "  static constexpr int kCombiner = " + std::to_string(d.combiner) + ";\n";
+    s += "  static __device__ __forceinline__ unsigned init(const ipr::ProgCtx& c, V* v, V* m) "
+         "{ return ipr_init(c, v, m); }\n";
+    s += "  static __device__ __forceinline__ unsigned compute(const ipr::ProgCtx& c, V* v, V mb, "
+         "V* m) { return ipr_compute(c, v, mb, m); }\n";
+    s += "  static __device__ __forceinline__ V edge(V m, unsigned w) { return ipr_edge(m, w); }\n";
+    s += "};\n";
+    return s;
+}
+
+void compile_program(ipregel_program* pr, const ipregel_program_desc& d) {
+    const Nvrtc& N = nvrtc();
+    if (!N.ok) fail(IPREGEL_ERR_UNSUPPORTED, "NVRTC unavailable: %s", N.why.c_str());
+    const std::string tu = program_tu(d);
+    nvrtcProgram prog;
+    nvrtcResult r = N.create(&prog, tu.c_str(), "ipregel_program.cu", kJitHeaderCount,
+                             kJitHeaderBodies, kJitHeaderNames);
+    if (r != NVRTC_SUCCESS) fail(IPREGEL_ERR_CUDA, "nvrtcCreateProgram: %s", N.err(r));
+    for (int i = 0; i < PK_COUNT; ++i) N.add_name(prog, kProgKernelNames[i]);
+    // IEEE arithmetic as written (no FMA contraction), the oracle's convention (R7)
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
+                          "-default-device",
+                          "-DIPREGEL_JIT=1"};
+    r = N.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+    size_t ls = 0;
+    N.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) N.log(prog, &log[0]);
+    while (!log.empty() && (log.back() == '\0' || log.back() == '\n')) log.pop_back();
+    pr->log = log;
+    if (r != NVRTC_SUCCESS) {
+        N.destroy(&prog);
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "vertex program does not compile (%s):\n%.3500s",
+             N.err(r), log.c_str());
+    }
+    size_t cs = 0;
+    N.cubin_size(prog, &cs);
+    pr->cubin.resize(cs);
+    N.cubin(prog, pr->cubin.data());
+    for (int i = 0; i < PK_COUNT; ++i) {
+        const char* low = nullptr;
+        if (N.lowered(prog, kProgKernelNames[i], &low) != NVRTC_SUCCESS || !low) {
+            N.destroy(&prog);
+            fail(IPREGEL_ERR_CUDA, "nvrtcGetLoweredName(%s) failed", kProgKernelNames[i]);
+        }
+        pr->lowered[i] = low;
+    }
+    N.destroy(&prog);
+}
+
+void ensure_program_loaded(ipregel_program* pr) {
+    if (pr->lib) return;
+    CU(cudaLibraryLoadData(&pr->lib, pr->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    for (int i = 0; i < PK_COUNT; ++i)
+        CU(cudaLibraryGetKernel(&pr->k[i], pr->lib, pr->lowered[i].c_str()));
+}
+
+void launch_jit(cudaKernel_t k, unsigned grid, unsigned block, void** args, cudaStream_t s) {
+    if (grid == 0) return;
+    CU(cudaLaunchKernel((const void*)k, dim3(grid), dim3(block), args, 0, s));
+    LAUNCH_CHECK();
+}
+
+// One pull pass of a program over one adjacency (the ProgPull<P, pass> instantiation).
+template <class V>
+void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, ProgArgs<V>& a,
+                         const TilePlan& P, const int32_t* off, const int32_t* idx,
+                         const uint32_t* w, PullCounters* cnt) {
+    if (P.num_tiles == 0) return;
+    RangeArgs A = range_args(P, off, idx, w, cnt, g->stream, a.out_cur, g->n, sizeof(V),
+                             g->gather_policy, g->degree_ordered);
+    void* args[] = {&a, &A};
+    launch_jit(pr->k[PK_PULL0 + pass], (unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads,
+               args, g->stream);
+    if (P.num_groups) {
+        const int4* groups = P.groups;
+        int32_t ng = P.num_groups;
+        const V* carry = static_cast<const V*>(P.carry);
+        const V* head = static_cast<const V*>(P.head);
+        void* fargs[] = {&a, &groups, &ng, &carry, &head, &cnt};
+        launch_jit(pr->k[PK_FIX0 + pass], grid_for((int64_t)ng * 32, 256), 256, fargs, g->stream);
+    }
+}
+
+template <class V>
+ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max_steps,
+                             const ipregel_run_params& P, const double* params, int nparams) {
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    const int app = kAppProgram;
+    const bool sym = pr->sym != 0;
+    const bool multi = g->parts.size() > 1 || multi_rank(g);
+    const uint64_t pull_edges = sym ? 2ull * (uint64_t)g->e : (uint64_t)g->e;
+    ensure_program_loaded(pr);
+    const bool fused = use_fused_exchange(g, app, P.flags);
+    g->last_exchange = exchange_kind(g, fused);
+    if (P.mode != IPREGEL_MODE_PULL)
+        for (auto& p : g->parts) ensure_push_view(g, p);
+    double hp[kProgParams] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < nparams; ++i) hp[i] = params[i];
+    auto args_for = [&](Partition& p, uint32_t step, int cur) {
+        AppState& S = p.st[app];
+        ProgArgs<V> a;
+        a.value = static_cast<V*>(S.pv_value);
+        a.out_cur = static_cast<const V*>(S.pv_out[cur]);
+        a.out_next = static_cast<V*>(S.pv_out[1 - cur]);
+        a.peers = peer_slots<V>(S, 1 - cur, fused);
+        a.mbox = static_cast<V*>(S.pv_mbox);
+        a.bits = S.bits;
+        a.recv = S.pv_recv;
+        a.active = S.pv_active;
+        a.out_off = p.csr_off;
+        a.in_off = p.csc_off;
+        a.ids = g->vertex_ids;
+        a.params = S.pv_params;
+        a.vbase = p.vb;
+        a.rows = p.rows;
+        a.n = n;
+        a.superstep = step;
+        a.sym = sym ? 1 : 0;
+        return a;
+    };
+    auto exchange = [&](int w) {
+        if (!fused)
+            exchange_owned<V>(g, [app, w](Partition& p) { return static_cast<V*>(p.st[app].pv_out[w]); });
+    };
+
+    // ---------------- superstep 0: init writes outbox buffer 0 (read by superstep 1)
+    g->steps.assign(1, StepRecord{});
+    StepTimer T0{g, 0};
+    T0.begin();
+    for (auto& p : g->parts) {
+        AppState& S = p.st[app];
+        CU(cudaMemcpyAsync(S.pv_params, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
+        CU(cudaMemsetAsync(S.bits, 0, words_of(p.rows) * 4, s));
+        CU(cudaMemsetAsync(S.pv_recv, 0, words_of(p.rows) * 4, s));
+    }
+    T0.kbegin();
+    for (auto& p : g->parts) {
+        ProgArgs<V> a = args_for(p, 0, 1);   // out_next = buffer 0
+        PullCounters* cnt = p.pull_cnt;
+        void* args[] = {&a, &cnt};
+        launch_jit(pr->k[PK_INIT], grid_for(p.rows, 256), 256, args, s);
+    }
+    T0.kend();
+    exchange(0);
+    unsigned long long c[4];
+    reduce_counters(g, false, c, 4);
+    T0.end();
+    uint64_t changed = c[0], messages = c[1], active = c[3];
+    g->steps[0].mode = 0;
+    g->steps[0].changed = changed;
+    g->steps[0].messages = messages;
+    g->steps[0].model_bytes = (uint64_t)n * sizeof(V);
+    int cur = 0;
+    ipregel_status status = IPREGEL_OK;
+
+    for (uint32_t step = 1; messages > 0 || active > 0; ++step) {
+        if (step == max_steps) { status = IPREGEL_ERR_MAX_SUPERSTEPS; break; }
+        int mode;
+        if (P.mode == IPREGEL_MODE_PULL) mode = 1;
+        else if (P.mode == IPREGEL_MODE_PUSH) mode = 2;
+        else mode = (double)messages < (double)P.push_fraction * (double)pull_edges ? 2 : 1;
+        g->steps.push_back(StepRecord{});
+        StepTimer T{g, step};
+        T.begin();
+        const uint64_t frontier_len = changed;
+        for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
+        if (mode == 2) {
+            // frontier = the broadcasters of superstep s-1 (their bits; compaction clears them)
+            for (auto& p : g->parts) compact_bitmap(g, p, p.st[app], nullptr, sym);
+            if (multi) exchange_frontier(g, app, frontier_counts(g), cur);
+            T.kbegin();
+            for (auto& p : g->parts) {
+                AppState& S = p.st[app];
+                const PushAdj& adj = sym ? p.push_cc : p.push_sssp;
+                build_expand_list(g, p, S, adj, S.g_id, nullptr, S.g_len, (int64_t)frontier_len);
+                ProgArgs<V> a = args_for(p, step, cur);
+                const unsigned grid = (unsigned)std::min<int64_t>(
+                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), 148 * 8);
+                PushAdj ad = adj;
+                const int32_t* eid = S.e_id;
+                const long long* epre = S.e_pre;
+                const unsigned long long* len = &p.front_cnt->list_len;
+                const unsigned long long* ecnt = &p.front_cnt->list_edges;
+                void* eargs[] = {&ad, &eid, &epre, &len, &ecnt, &a};
+                launch_jit(pr->k[PK_EXPAND], grid, kExpandThreads, eargs, s);
+            }
+            for (auto& p : g->parts) {
+                ProgArgs<V> a = args_for(p, step, cur);
+                PullCounters* cnt = p.pull_cnt;
+                void* args[] = {&a, &cnt};
+                launch_jit(pr->k[PK_APPLY], grid_for(p.rows, 256), 256, args, s);
+            }
+            T.kend();
+        } else {
+            for (auto& p : g->parts) CU(cudaMemsetAsync(p.st[app].bits, 0, words_of(p.rows) * 4, s));
+            T.kbegin();
+            for (auto& p : g->parts) {
+                if (p.rows == 0) continue;
+                ProgArgs<V> a = args_for(p, step, cur);
+                if (sym) {
+                    launch_pull_program<V>(g, pr, 1, a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w,
+                                           p.pull_cnt);
+                    launch_pull_program<V>(g, pr, 2, a, p.plan_csr, p.csr_off, p.csr_idx, p.csr_w,
+                                           p.pull_cnt);
+                } else {
+                    launch_pull_program<V>(g, pr, 0, a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w,
+                                           p.pull_cnt);
+                }
+            }
+            T.kend();
+        }
+        exchange(1 - cur);
+        reduce_counters(g, false, c, 4);
+        T.end();
+        StepRecord& R = g->steps.back();
+        R.mode = (uint8_t)mode;
+        R.edges_scanned = mode == 1 ? pull_edges : messages;
+        R.model_bytes = mode == 1
+            ? (uint64_t)(4 + sizeof(V) + (g->parts[0].csc_w ? 4 : 0)) * pull_edges +
+                  (uint64_t)(8 + 3 * sizeof(V)) * (uint64_t)n
+            : (uint64_t)(8 + sizeof(V) + (g->parts[0].csc_w ? 4 : 0)) * messages +
+                  (uint64_t)(16 + 3 * sizeof(V)) * (uint64_t)n;
+        changed = c[0];
+        messages = c[1];
+        active = c[3];
+        R.changed = changed;
+        R.messages = messages;
+        cur = 1 - cur;
+    }
+    g->cur = cur;
+    finalize_times(g);
+    return status;
+}
+
+}  // namespace
+
+// =============================================================================================
 // C ABI
 // =============================================================================================
 #define ABI_BEGIN try {
@@ -1525,6 +1915,90 @@ ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner c
         throw;
     }
     g->last_app = app;
+    g->last_vsz = app == IPREGEL_APP_PAGERANK ? 8 : 4;
+    g->last_status = st;
+    if (st != IPREGEL_OK) g_last_error = "superstep guard reached with work remaining";
+    return st;
+    ABI_END
+}
+
+ipregel_status ipregel_program_create(const ipregel_program_desc* desc, ipregel_program** out) {
+    ABI_BEGIN
+    if (!out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!desc || !desc->source) fail(IPREGEL_ERR_INVALID_ARGUMENT, "desc or source is NULL");
+    if (desc->value_type != IPREGEL_VALUE_U32 && desc->value_type != IPREGEL_VALUE_F64)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown value_type %d", desc->value_type);
+    if (desc->combiner < IPREGEL_COMBINE_SUM || desc->combiner > IPREGEL_COMBINE_MAX)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown combiner %d", desc->combiner);
+    if (desc->symmetric != 0 && desc->symmetric != 1)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "symmetric must be 0 or 1");
+    if (desc->reserved != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "reserved must be 0");
+    ipregel_program* pr = new ipregel_program;
+    pr->value_type = desc->value_type;
+    pr->combiner = desc->combiner;
+    pr->sym = desc->symmetric;
+    try {
+        compile_program(pr, *desc);
+    } catch (...) {
+        delete pr;
+        throw;
+    }
+    *out = pr;
+    return IPREGEL_OK;
+    ABI_END
+}
+
+const char* ipregel_program_log(const ipregel_program* program) {
+    return program ? program->log.c_str() : "";
+}
+
+uint64_t ipregel_program_cubin_bytes(const ipregel_program* program) {
+    return program ? (uint64_t)program->cubin.size() : 0;
+}
+
+void ipregel_program_destroy(ipregel_program* program) {
+    if (!program) return;
+    if (program->lib) cudaLibraryUnload(program->lib);
+    delete program;
+}
+
+ipregel_status ipregel_run_program(ipregel_graph* g, ipregel_program* program,
+                                   uint32_t max_supersteps, const ipregel_run_params* params,
+                                   const double* program_params, int num_program_params) {
+    ABI_BEGIN
+    if (!g || !program) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or program is NULL");
+    if (g->poisoned) fail(IPREGEL_ERR_STATE, "graph handle was poisoned by an earlier failure");
+    if (max_supersteps == 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "max_supersteps must be >= 1");
+    if (num_program_params < 0 || num_program_params > kProgParams ||
+        (num_program_params > 0 && !program_params))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "program parameters: 0..%d values", kProgParams);
+    ipregel_run_params P;
+    ipregel_run_params_default(&P);
+    if (params) P = *params;
+    if (P.mode < IPREGEL_MODE_AUTO || P.mode > IPREGEL_MODE_PUSH)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown mode %d", P.mode);
+    if (P.flags & ~(uint32_t)(IPREGEL_RUN_EXCHANGE_COLLECTIVE | IPREGEL_RUN_EXCHANGE_FUSED))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", P.flags);
+    if ((P.flags & IPREGEL_RUN_EXCHANGE_COLLECTIVE) && (P.flags & IPREGEL_RUN_EXCHANGE_FUSED))
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "EXCHANGE_COLLECTIVE and EXCHANGE_FUSED are exclusive");
+    if (!(P.push_fraction >= 0.0f)) fail(IPREGEL_ERR_INVALID_ARGUMENT, "push_fraction < 0");
+    g->last_status = -1;
+    g->last_app = -1;
+    ipregel_status st;
+    try {
+        ensure_state(g, kAppProgram);
+        st = program->value_type == IPREGEL_VALUE_F64
+                 ? run_program_t<double>(g, program, max_supersteps, P, program_params,
+                                         num_program_params)
+                 : run_program_t<uint32_t>(g, program, max_supersteps, P, program_params,
+                                           num_program_params);
+    } catch (const Failure& f) {
+        if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
+        throw;
+    }
+    g->last_app = kAppProgram;
+    g->last_vsz = program->value_type == IPREGEL_VALUE_F64 ? 8 : 4;
     g->last_status = st;
     if (st != IPREGEL_OK) g_last_error = "superstep guard reached with work remaining";
     return st;
@@ -1537,8 +2011,10 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
     if (!g || !out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or out is NULL");
     if (g->poisoned) fail(IPREGEL_ERR_STATE, "graph handle was poisoned");
     if (g->last_app < 0) fail(IPREGEL_ERR_STATE, "no completed run");
-    const bool pr = g->last_app == IPREGEL_APP_PAGERANK;
-    const size_t esz = pr ? 8 : 4;
+    // owned value arrays (PageRank ranks, program values) are assembled into a full vector;
+    // CC/SSSP values are already full replicas
+    const bool owned = g->last_app == IPREGEL_APP_PAGERANK || g->last_app == kAppProgram;
+    const size_t esz = (size_t)g->last_vsz;
     if (out_bytes != (size_t)g->n * esz)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "out_bytes %zu != N * %zu", out_bytes, esz);
     cudaStream_t s = g->stream;
@@ -1546,18 +2022,23 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
     try {
         // full N-vector in internal order (device)
         const void* full = nullptr;
-        if (pr) {
+        if (owned) {
             if (!g->gather_tmp) CU(cudaMalloc(&g->gather_tmp, g->n * sizeof(double)));
-            for (auto& p : g->parts)
+            uint8_t* base = reinterpret_cast<uint8_t*>(g->gather_tmp);
+            for (auto& p : g->parts) {
+                const void* src = g->last_app == IPREGEL_APP_PAGERANK ? (const void*)p.st[0].rank
+                                                                      : p.st[kAppProgram].pv_value;
                 if (p.rows)
-                    CU(cudaMemcpyAsync(g->gather_tmp + p.vb, p.st[0].rank, p.rows * 8,
+                    CU(cudaMemcpyAsync(base + p.vb * esz, src, p.rows * esz,
                                        cudaMemcpyDeviceToDevice, s));
+            }
             if (multi_rank(g)) {
                 NC(ncclGroupStart());
                 for (int r = 0; r < g->comm->world; ++r)
                     if (g->rank_rows[r])
-                        NC(ncclBroadcast(g->gather_tmp + g->rank_vb[r], g->gather_tmp + g->rank_vb[r],
-                                         (size_t)g->rank_rows[r], ncclFloat64, r, g->comm->nccl, s));
+                        NC(ncclBroadcast(base + g->rank_vb[r] * esz, base + g->rank_vb[r] * esz,
+                                         (size_t)g->rank_rows[r] * esz, ncclUint8, r,
+                                         g->comm->nccl, s));
                 NC(ncclGroupEnd());
             }
             full = g->gather_tmp;
@@ -1566,7 +2047,7 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
         }
         if (g->vertex_ids) {
             if (!g->gather_tmp2) CU(cudaMalloc(&g->gather_tmp2, g->n * sizeof(double)));
-            if (pr)
+            if (esz == 8)
                 k_to_original<double><<<grid_for(g->n, 256), 256, 0, s>>>(
                     (const double*)full, g->vertex_ids, g->n, g->gather_tmp2);
             else

@@ -24,7 +24,6 @@
 // multiples of 128 GLOBAL edge positions, so every row's combine tree depends on global positions
 // only: PageRank is bit-identical for any destination partition.
 #pragma once
-#include <climits>
 #include "common.cuh"
 
 namespace ipr {
@@ -44,6 +43,7 @@ struct PullCounters {
     unsigned long long changed;
     unsigned long long messages;
     unsigned long long dmax;   // PageRank to convergence: max |r_s - r_{s-1}| as f64 bits (>= 0)
+    unsigned long long active; // user programs: vertices that did not vote to halt
 };
 
 // Range plan for one adjacency of one partition.
@@ -316,24 +316,27 @@ struct RangeArgs {
 __device__ __forceinline__ void flush_counters(const PullCounters& cnt, unsigned long long* s_cnt,
                                                PullCounters* counters) {
     const int lane = threadIdx.x & 31;
-    unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax;
+    unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax, c3 = cnt.active;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         c0 += __shfl_xor_sync(kFull, c0, d);
         c1 += __shfl_xor_sync(kFull, c1, d);
         const unsigned long long o = __shfl_xor_sync(kFull, c2, d);
         c2 = o > c2 ? o : c2;
+        c3 += __shfl_xor_sync(kFull, c3, d);
     }
-    if (lane == 0 && (c0 | c1 | c2)) {
+    if (lane == 0 && (c0 | c1 | c2 | c3)) {
         atomicAdd(&s_cnt[0], c0);
         atomicAdd(&s_cnt[1], c1);
         atomicMax(&s_cnt[2], c2);
+        atomicAdd(&s_cnt[3], c3);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1] | s_cnt[2])) {
+    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1] | s_cnt[2] | s_cnt[3])) {
         atomicAdd(&counters->changed, s_cnt[0]);
         atomicAdd(&counters->messages, s_cnt[1]);
         atomicMax(&counters->dmax, s_cnt[2]);
+        atomicAdd(&counters->active, s_cnt[3]);
     }
 }
 
@@ -523,12 +526,12 @@ template <class Op>
 __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_ranges(Op op, RangeArgs A) {
     using T = typename Op::T;
     __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums by position (conflict-free)
-    __shared__ unsigned long long s_cnt[3];
+    __shared__ unsigned long long s_cnt[4];
     const int wid = threadIdx.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    PullCounters cnt{0, 0, 0};
+    PullCounters cnt{0, 0, 0, 0};
     if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
     flush_counters(cnt, s_cnt, A.counters);
 }
@@ -555,12 +558,13 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     }
     if (lane == 0) {
         acc = Op::combine(acc, head[G.z]);
-        PullCounters c{0, 0, 0};
+        PullCounters c{0, 0, 0, 0};
         op.finish(G.x, acc, c);
-        if (counters && (c.changed | c.messages | c.dmax)) {
+        if (counters && (c.changed | c.messages | c.dmax | c.active)) {
             atomicAdd(&counters->changed, c.changed);
             atomicAdd(&counters->messages, c.messages);
             atomicMax(&counters->dmax, c.dmax);
+            atomicAdd(&counters->active, c.active);
         }
     }
 }

@@ -41,6 +41,7 @@ struct PushAdj {
     const uint32_t* w1 = nullptr;
     const int32_t* off2 = nullptr;
     const int32_t* idx2 = nullptr;
+    const uint32_t* w2 = nullptr;   // weights of the second part (generic symmetric programs)
     int64_t src_base = 0;           // off arrays cover sources [src_base, src_base + src_rows)
     int64_t src_rows = 0;
     __device__ __forceinline__ int64_t degree(int64_t u) const {
@@ -177,7 +178,7 @@ k_bitmap_write(uint32_t* __restrict__ bits, int64_t nwords, int64_t vbase,
                 b &= b - 1;
                 int64_t v = vbase + w * 32 + i;
                 f_id[pos] = (int32_t)v;
-                f_val[pos] = vals[v];
+                f_val[pos] = vals ? vals[v] : 0u;
                 ++pos;
             }
         }
@@ -241,19 +242,17 @@ k_list_write(const int32_t* __restrict__ f_id, const uint32_t* __restrict__ f_va
 }
 
 // ---- expansion: one message per out-edge of every frontier vertex ---------------------------
-// Min programs (CC, SSSP): msg = snapshot (CC) or sat(snapshot + w) (SSSP); atomicMin into the
-// live value of the recipient; a successful decrease marks the recipient in the next bitmap.
-// Sum program (PageRank push): atomicAdd of the sender's contribution into the accumulator.
-template <int kProgram>  // 0 PageRank (sum), 1 CC (min, no weight), 2 SSSP (min + weight)
-__global__ void __launch_bounds__(kExpandThreads)
-k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restrict__ e_val,
-         const long long* __restrict__ e_pre, const unsigned long long* __restrict__ counters_len,
-         const unsigned long long* __restrict__ counters_edges, int64_t dst_base,
-         uint32_t* __restrict__ val, uint32_t* __restrict__ bits,
-         const double* __restrict__ contrib, double* __restrict__ acc) {
-    // per chunk of kExpandItems edges: the frontier entries it touches, each with its adjacency
-    // bases resolved once, and an owner table (edge slot -> entry) from a block scan of the
-    // entries' start flags -- no per-edge search, no per-edge offset loads
+// Edge-balanced over the expand list: per chunk of kExpandItems edges, the frontier entries it
+// touches, each with its adjacency bases resolved once, and an owner table (edge slot -> entry)
+// from a block scan of the entries' start flags -- no per-edge search, no per-edge offset loads.
+// `deliver(u, snapshot, v, w)` folds the message of edge (u -> v, w) into v's slot.
+template <class Deliver>
+__device__ __forceinline__ void expand_edges(const PushAdj& adj, const int32_t* __restrict__ e_id,
+                                             const uint32_t* __restrict__ e_val,
+                                             const long long* __restrict__ e_pre,
+                                             const unsigned long long* __restrict__ counters_len,
+                                             const unsigned long long* __restrict__ counters_edges,
+                                             const Deliver& deliver) {
     constexpr int kPer = kExpandItems / kExpandThreads;
     __shared__ int32_t s_start[kExpandItems + 1];   // entry start relative to the chunk
     __shared__ int32_t s_b1[kExpandItems + 1], s_d1[kExpandItems + 1], s_b2[kExpandItems + 1];
@@ -287,7 +286,7 @@ k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restri
             s_start[i] = (int32_t)st;
             const int32_t u = e_id[f0 + i];
             s_id[i] = u;
-            s_val[i] = e_val[f0 + i];
+            s_val[i] = e_val ? e_val[f0 + i] : 0u;
             const int64_t r = (int64_t)u - adj.src_base;
             const int32_t b1 = adj.off1[r];
             s_b1[i] = b1;
@@ -327,23 +326,54 @@ k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restri
             uint32_t w = 1u;
             if (pos < s_d1[o]) {
                 v = adj.idx1[s_b1[o] + pos];
-                if (kProgram == 2 && adj.w1) w = adj.w1[s_b1[o] + pos];
+                if (adj.w1) w = adj.w1[s_b1[o] + pos];
             } else {
                 v = adj.idx2[s_b2[o] + (pos - s_d1[o])];
+                if (adj.w2) w = adj.w2[s_b2[o] + (pos - s_d1[o])];
             }
-            const int64_t lv = (int64_t)v - dst_base;
-            if (kProgram == 0) {
-                atomicAdd(acc + lv, contrib[s_id[o]]);
-            } else {
-                const uint32_t msg = kProgram == 2 ? sat_add(s_val[o], w) : s_val[o];
-                if (msg < val[v]) {  // cheap filter; the atomic decides
-                    const uint32_t old = atomicMin(val + v, msg);
-                    if (msg < old) atomicOr(bits + (lv >> 5), 1u << (lv & 31));
-                }
-            }
+            deliver(s_id[o], s_val[o], v, w);
         }
         __syncthreads();
     }
+}
+
+// The paper's programs.  Min programs (CC, SSSP): msg = snapshot (CC) or sat(snapshot + w)
+// (SSSP); atomicMin into the live value of the recipient; a successful decrease marks the
+// recipient in the next bitmap.  Sum program (PageRank push): atomicAdd of the sender's
+// contribution into the accumulator.
+template <int kProgram>
+struct BuiltinDeliver {
+    int64_t dst_base;
+    uint32_t* val;
+    uint32_t* bits;
+    const double* contrib;
+    double* acc;
+    __device__ __forceinline__ void operator()(int32_t u, uint32_t snap, int32_t v,
+                                               uint32_t w) const {
+        const int64_t lv = (int64_t)v - dst_base;
+        if (kProgram == 0) {
+            atomicAdd(acc + lv, contrib[u]);
+        } else {
+            const uint32_t msg = kProgram == 2 ? sat_add(snap, w) : snap;
+            if (msg < val[v]) {  // cheap filter; the atomic decides
+                const uint32_t old = atomicMin(val + v, msg);
+                if (msg < old) atomicOr(bits + (lv >> 5), 1u << (lv & 31));
+            }
+        }
+    }
+};
+
+template <int kProgram>  // 0 PageRank (sum), 1 CC (min, no weight), 2 SSSP (min + weight)
+__global__ void __launch_bounds__(kExpandThreads)
+k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restrict__ e_val,
+         const long long* __restrict__ e_pre, const unsigned long long* __restrict__ counters_len,
+         const unsigned long long* __restrict__ counters_edges, int64_t dst_base,
+         uint32_t* __restrict__ val, uint32_t* __restrict__ bits,
+         const double* __restrict__ contrib, double* __restrict__ acc) {
+    if (kProgram != 2) adj.w1 = nullptr;   // weights only matter to SSSP
+    adj.w2 = nullptr;
+    expand_edges(adj, e_id, e_val, e_pre, counters_len, counters_edges,
+                 BuiltinDeliver<kProgram>{dst_base, val, bits, contrib, acc});
 }
 
 // Pull -> push switch: the broadcasters of a pull superstep are the vertices whose value

@@ -17,7 +17,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IPREGEL_LIB") or os.path.join(_HERE, "libipregel.so")
 
 APP_PAGERANK, APP_HASHMIN_CC, APP_SSSP = 0, 1, 2
-COMBINE_SUM, COMBINE_MIN = 0, 1
+COMBINE_SUM, COMBINE_MIN, COMBINE_MAX = 0, 1, 2
+VALUE_U32, VALUE_F64 = 0, 1
+COMBINERS = {"sum": COMBINE_SUM, "min": COMBINE_MIN, "max": COMBINE_MAX}
+VALUE_TYPES = {"u32": VALUE_U32, "f64": VALUE_F64}
+APP_PROGRAM = 3   # last run was a user program
 MODE_AUTO, MODE_PULL, MODE_PUSH = 0, 1, 2
 MEMORY_DEVICE, MEMORY_HOST = 0, 1
 INF = 0xFFFFFFFF
@@ -76,6 +80,12 @@ class Stats(ctypes.Structure):
                 ("model_bytes", ctypes.c_void_p), ("pagerank_delta", ctypes.c_void_p)]
 
 
+class ProgramDesc(ctypes.Structure):
+    _fields_ = [("source", ctypes.c_char_p), ("value_type", ctypes.c_int32),
+                ("combiner", ctypes.c_int32), ("symmetric", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 # every symbol include/ipregel.h declares (tests check the library exports all of them)
 EXPORTS = [
     "ipregel_status_string", "ipregel_last_error", "ipregel_abi_version",
@@ -84,6 +94,8 @@ EXPORTS = [
     "ipregel_comm_destroy", "ipregel_partition", "ipregel_graph_create",
     "ipregel_graph_create_partitioned", "ipregel_graph_destroy", "ipregel_memory_footprint",
     "ipregel_run", "ipregel_get_values", "ipregel_get_stats",
+    "ipregel_program_create", "ipregel_program_log", "ipregel_program_cubin_bytes",
+    "ipregel_program_destroy", "ipregel_run_program",
 ]
 
 _lib = None
@@ -119,6 +131,12 @@ def load() -> ctypes.CDLL:
         "ipregel_run": (I, [P, I, I, ctypes.c_uint32, ctypes.POINTER(RunParams)]),
         "ipregel_get_values": (I, [P, P, ctypes.c_size_t, I]),
         "ipregel_get_stats": (I, [P, ctypes.POINTER(Stats)]),
+        "ipregel_program_create": (I, [ctypes.POINTER(ProgramDesc), ctypes.POINTER(P)]),
+        "ipregel_program_log": (ctypes.c_char_p, [P]),
+        "ipregel_program_cubin_bytes": (ctypes.c_uint64, [P]),
+        "ipregel_program_destroy": (None, [P]),
+        "ipregel_run_program": (I, [P, P, ctypes.c_uint32, ctypes.POINTER(RunParams),
+                                    ctypes.POINTER(ctypes.c_double), I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -200,6 +218,47 @@ class Comm:
     def close(self):
         if self.handle:
             load().ipregel_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Program:
+    """A user vertex program (ipregel_program_create): CUDA C++ source defining ipr_init,
+    ipr_compute and ipr_edge (include/ipregel.h), compiled by NVRTC for sm_100a."""
+
+    def __init__(self, source: str, value_type: str = "u32", combiner: str = "min",
+                 symmetric: bool = False):
+        d = ProgramDesc()
+        self._src = source.encode()
+        d.source = self._src
+        d.value_type = VALUE_TYPES[value_type]
+        d.combiner = COMBINERS[combiner]
+        d.symmetric = 1 if symmetric else 0
+        d.reserved = 0
+        h = ctypes.c_void_p()
+        _check(load().ipregel_program_create(ctypes.byref(d), ctypes.byref(h)),
+               "ipregel_program_create")
+        self.handle = h
+        self.value_type = value_type
+        self.combiner = combiner
+        self.symmetric = symmetric
+
+    @property
+    def log(self) -> str:
+        return load().ipregel_program_log(self.handle).decode()
+
+    @property
+    def cubin_bytes(self) -> int:
+        return int(load().ipregel_program_cubin_bytes(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().ipregel_program_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -313,12 +372,28 @@ class Graph:
         self.last_app = app
         return st
 
+    def run_program(self, program: "Program", params=(), max_supersteps: int = 1 << 30,
+                    mode="auto", push_fraction: float = 0.04, exchange: str = "auto",
+                    allow_guard: bool = False) -> int:
+        """Run a user vertex program (ipregel_run_program); params: up to 8 floats."""
+        p = run_params_default()
+        p.mode = MODES[mode] if isinstance(mode, str) else int(mode)
+        p.push_fraction = push_fraction
+        p.flags = EXCHANGES[exchange]
+        vals = (ctypes.c_double * 8)(*[float(x) for x in params])
+        st = load().ipregel_run_program(self.handle, program.handle, max_supersteps,
+                                        ctypes.byref(p), vals, len(params))
+        _check(st, "ipregel_run_program", allow=(ERR_MAX_SUPERSTEPS,) if allow_guard else ())
+        self.last_app = APP_PROGRAM
+        self._last_f64 = program.value_type == "f64"
+        return st
+
     def values(self, out=None, host: bool = False):
         """Full N-vector of the last run: torch CUDA tensor (default) or numpy (host=True)."""
         import torch
         if self.last_app is None:
             raise IpregelError(ERR_STATE, "values", "no completed run")
-        pr = self.last_app == APP_PAGERANK
+        pr = self.last_app == APP_PAGERANK or (self.last_app == APP_PROGRAM and self._last_f64)
         if host:
             out = np.empty(self.n, np.float64 if pr else np.uint32)
             _check(load().ipregel_get_values(self.handle, out.ctypes.data, out.nbytes, 0),

@@ -1,0 +1,175 @@
+"""Vertex programs written against the user-program API (include/ipregel.h, csrc/program.cuh).
+
+The paper's three benchmark programs (Sec. 6) transcribed from Figs. 8-10 into the
+ipr_init / ipr_compute / ipr_edge form, plus a few more programs of the same model.  Each entry
+is (source, value_type, combiner, symmetric); `compile(name)` builds the Program.
+"""
+from __future__ import annotations
+
+from .ipregel import Program
+
+# Fig. 8: params[0] = k, the supersteps that broadcast (Fig. 8's 10).
+PAGERANK = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, double* value, double* message) {
+    const unsigned k = (unsigned)c.params[0];
+    *value = 1.0 / (double)c.num_vertices;                 // initial_value (PAPER.md:322)
+    if (k == 0) return 0;                                  // ip_vote_to_halt
+    if (c.out_degree == 0) return IPR_STAY_ACTIVE;         // no out-neighbour: nothing to send
+    *message = *value / (double)c.out_degree;              // ip_broadcast(value / outdeg)
+    return IPR_BROADCAST | IPR_STAY_ACTIVE;
+}
+__device__ unsigned ipr_compute(const ipr_ctx& c, double* value, double mailbox, double* message) {
+    const unsigned k = (unsigned)c.params[0];
+    const double ratio = 0.15 / (double)c.num_vertices;    // Pregel's 0.15 / N (PAPER.md:521)
+    *value = ratio + 0.85 * mailbox;                       // sum of the messages (combined)
+    if (c.superstep >= k) return 0;                        // ip_vote_to_halt
+    if (c.out_degree == 0) return IPR_STAY_ACTIVE;
+    *message = *value / (double)c.out_degree;
+    return IPR_BROADCAST | IPR_STAY_ACTIVE;
+}
+__device__ double ipr_edge(double message, unsigned) { return message; }
+"""
+
+# Fig. 9: Hash-Min on the symmetrised graph.
+HASHMIN_CC = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned* message) {
+    *value = (unsigned)c.id;
+    *message = *value;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox,
+                                unsigned* message) {
+    if (mailbox < *value) {                                // min of the messages improves
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;                                              // ip_vote_to_halt
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned) { return message; }
+"""
+
+# Fig. 10 with u32 edge weights (reading R8): params[0] = source.
+SSSP = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned* message) {
+    if (c.id == (long long)c.params[0]) {
+        *value = 0;
+        *message = 0;
+        return IPR_BROADCAST;
+    }
+    *value = IPR_INF_U32;
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox,
+                                unsigned* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned weight) {
+    return ipr_sat_add(message, weight);                   // value + w, saturating (R9)
+}
+"""
+
+# Breadth-first levels from params[0]: Fig. 10 exactly (every edge adds 1, weights ignored).
+BFS = SSSP.replace("return ipr_sat_add(message, weight);", "return ipr_sat_add(message, 1u);")
+
+# Widest (maximum-bottleneck) path from params[0]: max over paths of the min edge weight.
+WIDEST_PATH = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned* message) {
+    if (c.id == (long long)c.params[0]) {
+        *value = IPR_INF_U32;
+        *message = IPR_INF_U32;
+        return IPR_BROADCAST;
+    }
+    *value = 0;
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox,
+                                unsigned* message) {
+    if (mailbox > *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned weight) {
+    return message < weight ? message : weight;            // identity 0 stays 0
+}
+"""
+
+# Max-label propagation on the symmetrised graph: every vertex ends with the largest id of its
+# component (Hash-Min with the order reversed).
+MAX_LABEL = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned* message) {
+    *value = (unsigned)c.id;
+    *message = *value;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox,
+                                unsigned* message) {
+    if (mailbox > *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned) { return message; }
+"""
+
+# One-superstep sum: every vertex broadcasts 1, the value becomes the number of in-edges.
+IN_DEGREE = r"""
+__device__ unsigned ipr_init(const ipr_ctx&, unsigned* value, unsigned* message) {
+    *value = 0;
+    *message = 1;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox, unsigned*) {
+    *value = mailbox;
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned) { return message; }
+"""
+
+# Shortest paths with f64 distances (MIN over doubles, +inf = unreached).
+SSSP_F64 = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, double* value, double* message) {
+    if (c.id == (long long)c.params[0]) {
+        *value = 0.0;
+        *message = 0.0;
+        return IPR_BROADCAST;
+    }
+    *value = __longlong_as_double(0x7FF0000000000000LL);
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, double* value, double mailbox, double* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ double ipr_edge(double message, unsigned weight) { return message + (double)weight; }
+"""
+
+CATALOG = {
+    "pagerank": (PAGERANK, "f64", "sum", False),
+    "hashmin_cc": (HASHMIN_CC, "u32", "min", True),
+    "sssp": (SSSP, "u32", "min", False),
+    "bfs": (BFS, "u32", "min", False),
+    "widest_path": (WIDEST_PATH, "u32", "max", False),
+    "max_label": (MAX_LABEL, "u32", "max", True),
+    "in_degree": (IN_DEGREE, "u32", "sum", False),
+    "sssp_f64": (SSSP_F64, "f64", "min", False),
+}
+
+
+def compile(name: str) -> Program:  # noqa: A001 - mirrors the catalog verb
+    src, vt, comb, sym = CATALOG[name]
+    return Program(src, value_type=vt, combiner=comb, symmetric=sym)

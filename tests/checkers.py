@@ -170,3 +170,34 @@ def random_graph(rng, n, m, weighted=False, self_loops=False):
         src, dst = src[keep], dst[keep]
     w = rng.integers(1, 65, len(src)).astype(np.uint32) if weighted else None
     return src, dst, w
+
+
+def widest_path(n, edges, source):
+    """max over paths source ~> v of the min edge weight (bottleneck Dijkstra); the source gets
+    INF (empty path), unreachable vertices 0."""
+    adj = defaultdict(list)
+    for u, v, w in edges:
+        adj[u].append((v, w))
+    best = [0] * n
+    best[source] = INF
+    pq = [(-INF, source)]
+    while pq:
+        b, u = heapq.heappop(pq)
+        b = -b
+        if b != best[u]:
+            continue
+        for v, w in adj[u]:
+            nb = min(b, w)
+            if nb > best[v]:
+                best[v] = nb
+                heapq.heappush(pq, (-nb, v))
+    return best
+
+
+def cc_max_label(n, edges):
+    """label(v) = max vertex id of v's component in the undirected graph (union-find)."""
+    mn = cc_union_find(n, edges)
+    top = {}
+    for v in range(n):
+        top[mn[v]] = max(top.get(mn[v], v), v)
+    return [top[mn[v]] for v in range(n)]

@@ -51,7 +51,7 @@ def test_struct_layouts_match_header(tmp_path):
     """sizeof/offsetof of every ABI struct from the C compiler equal the ctypes binding's."""
     import subprocess
     structs = {"ipregel_graph_desc": ipr.ipregel.GraphDesc, "ipregel_run_params": ipr.RunParams,
-               "ipregel_stats": ipr.ipregel.Stats}
+               "ipregel_stats": ipr.ipregel.Stats, "ipregel_program_desc": ipr.ipregel.ProgramDesc}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.abspath(HEADER)}"',
              "int main(void) {"]
     for cname, cls in structs.items():
