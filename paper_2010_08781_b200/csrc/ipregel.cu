@@ -168,7 +168,7 @@ struct AppState {
     void* pv_value = nullptr;                  // owned values [rows]
     void* pv_out[2] = {nullptr, nullptr};      // outbox replicas [N] (identity = no broadcast)
     void* pv_mbox = nullptr;                   // owned mailboxes [rows]
-    uint8_t* pv_active = nullptr;              // owned: did not vote to halt
+    uint8_t* pv_flags = nullptr;               // owned: bit 0 broadcast, bit 1 active
     uint32_t* pv_recv = nullptr;               // owned recipient bitmap (push)
     double* pv_params = nullptr;               // program parameters [8]
     DeviceBuffers mem;
@@ -440,7 +440,7 @@ void ensure_state(ipregel_graph* g, int app) {
             S.pv_out[0] = S.mem.alloc<uint64_t>(n, s, true);
             S.pv_out[1] = S.mem.alloc<uint64_t>(n, s, true);
             S.pv_mbox = S.mem.alloc<uint64_t>(p.rows, s, true);
-            S.pv_active = S.mem.alloc<uint8_t>(p.rows, s, true);
+            S.pv_flags = S.mem.alloc<uint8_t>(p.rows, s, true);
             S.pv_recv = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.pv_params = S.mem.alloc<double>(kProgParams, s, true);
             S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
@@ -1386,7 +1386,7 @@ void compile_program(ipregel_program* pr, const ipregel_program_desc& d) {
     for (int i = 0; i < PK_COUNT; ++i) N.add_name(prog, kProgKernelNames[i]);
     // IEEE arithmetic as written (no FMA contraction), the oracle's convention (R7)
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                          "-default-device",
+                          "-default-device", "--ptxas-options=-v",
                           "-DIPREGEL_JIT=1"};
     r = N.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
     size_t ls = 0;
@@ -1473,9 +1473,8 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         a.out_next = static_cast<V*>(S.pv_out[1 - cur]);
         a.peers = peer_slots<V>(S, 1 - cur, fused);
         a.mbox = static_cast<V*>(S.pv_mbox);
-        a.bits = S.bits;
+        a.flags = S.pv_flags;
         a.recv = S.pv_recv;
-        a.active = S.pv_active;
         a.out_off = p.csr_off;
         a.in_off = p.csc_off;
         a.ids = g->vertex_ids;
@@ -1500,7 +1499,6 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         AppState& S = p.st[app];
         CU(cudaMemcpyAsync(S.pv_params, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
-        CU(cudaMemsetAsync(S.bits, 0, words_of(p.rows) * 4, s));
         CU(cudaMemsetAsync(S.pv_recv, 0, words_of(p.rows) * 4, s));
     }
     T0.kbegin();
@@ -1535,8 +1533,15 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         const uint64_t frontier_len = changed;
         for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
         if (mode == 2) {
-            // frontier = the broadcasters of superstep s-1 (their bits; compaction clears them)
-            for (auto& p : g->parts) compact_bitmap(g, p, p.st[app], nullptr, sym);
+            // frontier = the broadcasters of superstep s-1 (flag bytes -> bitmap -> ids)
+            for (auto& p : g->parts) {
+                if (p.rows) {
+                    k_bits_from_flags<<<grid_for(p.rows, 256), 256, 0, s>>>(p.st[app].pv_flags,
+                                                                           p.rows, p.st[app].bits);
+                    LAUNCH_CHECK();
+                }
+                compact_bitmap(g, p, p.st[app], nullptr, sym);
+            }
             if (multi) exchange_frontier(g, app, frontier_counts(g), cur);
             T.kbegin();
             for (auto& p : g->parts) {
@@ -1562,7 +1567,6 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             }
             T.kend();
         } else {
-            for (auto& p : g->parts) CU(cudaMemsetAsync(p.st[app].bits, 0, words_of(p.rows) * 4, s));
             T.kbegin();
             for (auto& p : g->parts) {
                 if (p.rows == 0) continue;

@@ -55,9 +55,8 @@ struct ProgArgs {
     V* out_next;           // outbox replica written this superstep [N]
     PeerSlots<V> peers;    // fused exchange of out_next
     V* mbox;               // owned mailboxes [rows] (push accumulators; symmetric pull part 1)
-    uint32_t* bits;        // owned broadcaster bitmap
+    uint8_t* flags;        // owned, per vertex: bit 0 broadcast this superstep, bit 1 active
     uint32_t* recv;        // owned recipient bitmap (push)
-    uint8_t* active;       // owned: did not vote to halt
     const int32_t* out_off;
     const int32_t* in_off;
     const int32_t* ids;    // internal -> original id, or NULL
@@ -130,26 +129,25 @@ __device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
 template <class P>
 __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int64_t row,
                                           const ProgCtx& x, unsigned f, typename P::V msg,
-                                          PullCounters& c) {
+                                          LaneCounters& c) {
     using V = typename P::V;
     using C = ProgComb<V, P::kCombiner>;
     const bool b = (f & kProgBroadcast) != 0;
     const V ob = b ? msg : C::identity();
     A.out_next[A.vbase + row] = ob;
     A.peers.store(A.vbase + row, ob);
-    if (b) {
-        atomicOr(A.bits + (row >> 5), 1u << (row & 31));
-        c.changed += 1;
-        c.messages += (unsigned long long)x.out_degree + (A.sym ? (unsigned long long)x.in_degree : 0ull);
-    }
     const bool act = (f & kProgStayActive) != 0;
-    A.active[row] = act ? 1 : 0;
+    A.flags[row] = (uint8_t)((b ? 1u : 0u) | (act ? 2u : 0u));   // plain store, no atomics
+    if (b) {
+        c.changed += 1;
+        c.messages += (uint32_t)x.out_degree + (A.sym ? (uint32_t)x.in_degree : 0u);
+    }
     c.active += act ? 1ull : 0ull;
 }
 
 template <class P>
 __device__ __forceinline__ void prog_vertex(const ProgArgs<typename P::V>& A, int64_t row,
-                                            typename P::V mailbox, PullCounters& c) {
+                                            typename P::V mailbox, LaneCounters& c) {
     using V = typename P::V;
     using C = ProgComb<V, P::kCombiner>;
     const ProgCtx x = prog_ctx(A, row);
@@ -169,7 +167,7 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
     __shared__ unsigned long long s_cnt[4];
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    PullCounters c{0, 0, 0, 0};
+    LaneCounters c{};
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row < A.rows) {
         const ProgCtx x = prog_ctx(A, row);
@@ -197,7 +195,7 @@ struct ProgPull : ProgArgs<typename P::V> {
     __device__ const T* gptr() const { return this->out_cur; }
     __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t w) { return P::edge(g, w); }
-    __device__ void finish(int32_t row, T m, PullCounters& c) const {
+    __device__ void finish(int32_t row, T m, LaneCounters& c) const {
         if (kPass == 1) {
             this->mbox[row] = m;
             return;
@@ -245,18 +243,19 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     __shared__ unsigned long long s_cnt[4];
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    PullCounters c{0, 0, 0, 0};
+    LaneCounters c{};
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool got = false;
     if (row < A.rows) {
         got = (A.recv[row >> 5] >> (row & 31)) & 1u;
-        if (got || A.active[row]) {
+        if (got || (A.flags[row] & 2u)) {
             const V m = A.mbox[row];
             A.mbox[row] = C::identity();
             prog_vertex<P>(A, row, m, c);
         } else {
             A.out_next[A.vbase + row] = C::identity();
             A.peers.store(A.vbase + row, C::identity());
+            A.flags[row] = 0;
         }
     }
     __syncwarp();

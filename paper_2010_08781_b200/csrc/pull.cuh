@@ -46,6 +46,16 @@ struct PullCounters {
     unsigned long long active; // user programs: vertices that did not vote to halt
 };
 
+// A thread's share of the counters while it runs, 32-bit (fewer live registers in the range
+// kernels' epilogue): a thread counts rows it finishes (< 2^31) and the sum of their degrees,
+// at most 2E < 2^32 for the symmetrised graph since E <= INT32_MAX (validated at create).
+struct LaneCounters {
+    uint32_t changed;
+    uint32_t active;
+    uint32_t messages;
+    unsigned long long dmax;
+};
+
 // Range plan for one adjacency of one partition.
 struct TilePlan {
     int32_t rows = 0;
@@ -145,7 +155,7 @@ struct PageRankPull : SumF64 {
     __device__ const T* gptr() const { return contrib_cur; }
     __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t) { return g; }
-    __device__ void finish(int32_t row, T sum, PullCounters& c) const {
+    __device__ void finish(int32_t row, T sum, LaneCounters& c) const {
         const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
         if (track) {   // max aggregator of the per-vertex change (reading R27)
             const unsigned long long d =
@@ -173,7 +183,7 @@ struct CCPullIn : MinU32 {
     // label 0 is the smallest id: a row already at 0 cannot change (skip its gathers)
     __device__ bool absorbed(int32_t row) const { return cur[vbase + row] == 0u; }
     __device__ static T message(T g, uint32_t) { return g; }
-    __device__ void finish(int32_t row, T m, PullCounters&) const {
+    __device__ void finish(int32_t row, T m, LaneCounters&) const {
         const uint32_t c = cur[vbase + row];
         next[vbase + row] = m < c ? m : c;
     }
@@ -193,7 +203,7 @@ struct CCPullOut : MinU32 {
     __device__ const T* gptr() const { return cur; }
     __device__ bool absorbed(int32_t row) const { return next[vbase + row] == 0u; }
     __device__ static T message(T g, uint32_t) { return g; }
-    __device__ void finish(int32_t row, T m, PullCounters& c) const {
+    __device__ void finish(int32_t row, T m, LaneCounters& c) const {
         const uint32_t old = cur[vbase + row];
         uint32_t v = next[vbase + row];
         v = m < v ? m : v;
@@ -201,8 +211,8 @@ struct CCPullOut : MinU32 {
         peers.store(vbase + row, v);
         if (v < old) {
             c.changed += 1;
-            c.messages += (unsigned long long)(in_off[row + 1] - in_off[row]) +
-                          (unsigned long long)(out_off[row + 1] - out_off[row]);
+            c.messages += (uint32_t)(in_off[row + 1] - in_off[row]) +
+                          (uint32_t)(out_off[row + 1] - out_off[row]);
         }
     }
 };
@@ -220,14 +230,14 @@ struct SSSPPull : MinU32 {
     __device__ const T* gptr() const { return cur; }
     __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t w) { return sat_add(g, w); }
-    __device__ void finish(int32_t row, T m, PullCounters& c) const {
+    __device__ void finish(int32_t row, T m, LaneCounters& c) const {
         const uint32_t old = cur[vbase + row];
         const uint32_t v = m < old ? m : old;
         next[vbase + row] = v;
         peers.store(vbase + row, v);
         if (v < old) {
             c.changed += 1;
-            c.messages += (unsigned long long)(out_off[row + 1] - out_off[row]);
+            c.messages += (uint32_t)(out_off[row + 1] - out_off[row]);
         }
     }
 };
@@ -313,7 +323,7 @@ struct RangeArgs {
 };
 
 // counters: warp reduce, one shared atomic per warp, one global atomic per CTA
-__device__ __forceinline__ void flush_counters(const PullCounters& cnt, unsigned long long* s_cnt,
+__device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned long long* s_cnt,
                                                PullCounters* counters) {
     const int lane = threadIdx.x & 31;
     unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax, c3 = cnt.active;
@@ -355,7 +365,7 @@ __device__ __forceinline__ typename Op::T warp_fold(typename Op::T x) {
 // One warp, one range q (see the file header).  `my_sum` is the warp's 128-slot sum array.
 template <class Op>
 __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int64_t q,
-                                           typename Op::T* my_sum, PullCounters& cnt) {
+                                           typename Op::T* my_sum, LaneCounters& cnt) {
     using T = typename Op::T;
     const int lane = threadIdx.x & 31;
     const uint64_t pol_s = policy_evict_first();
@@ -531,7 +541,7 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_r
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    PullCounters cnt{0, 0, 0, 0};
+    LaneCounters cnt{0u, 0u, 0u, 0ull};
     if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
     flush_counters(cnt, s_cnt, A.counters);
 }
@@ -558,7 +568,7 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     }
     if (lane == 0) {
         acc = Op::combine(acc, head[G.z]);
-        PullCounters c{0, 0, 0, 0};
+        LaneCounters c{0u, 0u, 0u, 0ull};
         op.finish(G.x, acc, c);
         if (counters && (c.changed | c.messages | c.dmax | c.active)) {
             atomicAdd(&counters->changed, c.changed);

@@ -20,6 +20,16 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
     }
 }
 
+// User programs: broadcaster bitmap of the owned rows from the per-vertex flag bytes (bit 0),
+// for the frontier compaction of a push superstep (ballot per warp).
+__global__ void k_bits_from_flags(const uint8_t* __restrict__ flags, int64_t rows,
+                                  uint32_t* __restrict__ bits) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool pred = i < rows && (flags[i] & 1u);
+    const uint32_t b = __ballot_sync(kFull, pred);
+    if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
+}
+
 // Hash-Min CC, Fig. 9: value = id, the ORIGINAL id under a relabelled layout (every replica
 // initialises all N locally -- no exchange).
 __global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n, const int32_t* __restrict__ ids) {
