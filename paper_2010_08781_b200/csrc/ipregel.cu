@@ -95,6 +95,8 @@ uint64_t g_hot_bytes = read_hot_bytes();
 // persisting access-policy window over the hot prefix (IPREGEL_PERSIST_BYTES, 0 = off).
 // -1 (default): 64 KiB worth of the hottest vertices for degree-ordered layouts, else off.
 int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -2;
+// Tuning knob: PageRank update split out of the range kernel (IPREGEL_PR_SPLIT=1).
+int g_pr_split = getenv("IPREGEL_PR_SPLIT") ? atoi(getenv("IPREGEL_PR_SPLIT")) : 1;
 uint64_t g_persist_bytes =
     getenv("IPREGEL_PERSIST_BYTES") ? strtoull(getenv("IPREGEL_PERSIST_BYTES"), nullptr, 10) : 0;
 
@@ -913,9 +915,21 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
                 op.track = track;
-                launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr,
-                            track ? p.pull_cnt : nullptr, s, n, g->gather_policy,
-                            g->degree_ordered);
+                if (g_pr_split) {
+                    PageRankSum sop;
+                    sop.contrib_cur = op.contrib_cur;
+                    sop.sum_out = op.contrib_next;
+                    sop.vbase = p.vb;
+                    launch_pull(sop, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
+                                g->gather_policy, g->degree_ordered);
+                    k_pr_finish<<<grid_for(p.rows, 256), 256, 0, s>>>(op, p.rows,
+                                                                      track ? p.pull_cnt : nullptr);
+                    LAUNCH_CHECK();
+                } else {
+                    launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr,
+                                track ? p.pull_cnt : nullptr, s, n, g->gather_policy,
+                                g->degree_ordered);
+                }
             } else {
                 k_expand<0><<<1184, kExpandThreads, 0, s>>>(
                     p.push_sssp, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -1100,18 +1114,21 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 if (cc) {
                     CCPullIn a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
+                                g->gather_policy, g->degree_ordered);
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
                     b.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
-                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
+                    launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n,
+                                g->gather_policy, g->degree_ordered);
                 } else {
                     SSSPPull a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
                     a.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n, g->gather_policy, g->degree_ordered);
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n,
+                                g->gather_policy, g->degree_ordered);
                 }
             }
             T.kend();

@@ -31,9 +31,6 @@ namespace ipr {
 #ifndef IPREGEL_PULL_MINBLOCKS
 #define IPREGEL_PULL_MINBLOCKS 4
 #endif
-#ifndef IPREGEL_GATHER_AHEAD
-#define IPREGEL_GATHER_AHEAD 1   // chunks of gathers in flight ahead of the one being folded
-#endif
 constexpr int kPullThreads = 256;                 // 8 warps per CTA
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
@@ -170,6 +167,21 @@ struct PageRankPull : SumF64 {
             peers.store(vbase + row, c);
         }
     }
+};
+
+// PageRank with the update split out of the range kernel (IPREGEL_PR_SPLIT=1): the range kernel
+// only stores each row's combined sum into its next-outbox slot, and k_pr_finish applies Fig. 8's
+// update row-parallel (same operations, same result).
+struct PageRankSum : SumF64 {
+    static constexpr bool kWeighted = false;
+    const double* __restrict__ contrib_cur;
+    double* __restrict__ sum_out;             // = contrib_next of the superstep (global ids)
+    int64_t vbase;
+    const void* gather_base() const { return contrib_cur; }
+    __device__ const T* gptr() const { return contrib_cur; }
+    __device__ bool absorbed(int32_t) const { return false; }
+    __device__ static T message(T g, uint32_t) { return g; }
+    __device__ void finish(int32_t row, T sum, LaneCounters&) const { sum_out[vbase + row] = sum; }
 };
 
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
@@ -382,33 +394,6 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
     // chunks on the global 128-edge grid covering [y0, y1)
     const int32_t c0 = y0 - ((y0 + A.cphase) & (kChunk - 1));
 
-#if IPREGEL_GATHER_AHEAD == 2
-    // software pipeline: indices three chunks ahead, gathered values two chunks ahead
-    ChunkLoad L0 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
-    ChunkLoad L1 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
-    ChunkLoad L2 = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + 2 * kChunk, y0, y1, lane, pol_s);
-    T g0[4], g1[4];
-    gather_chunk(op, L0, g0, pol_g, A.l1hot);
-    gather_chunk(op, L1, g1, pol_g, A.l1hot);
-
-#pragma unroll 1
-    for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
-        T g2[4];
-        gather_chunk(op, L2, g2, pol_g, A.l1hot);
-        uint32_t wc[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) wc[k] = L0.w[k];
-        L0 = L1;
-        L1 = L2;
-        L2 = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 3 * kChunk, y0, y1, lane, pol_s);
-        T v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            v[k] = Op::message(g0[k], wc[k]);
-            g0[k] = g1[k];
-            g1[k] = g2[k];
-        }
-#else
     // software pipeline: indices two chunks ahead, gathered values one chunk ahead
     ChunkLoad Lc = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
     ChunkLoad Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
@@ -432,7 +417,6 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
             v[k] = Op::message(gc[k], wc[k]);
             gc[k] = gn[k];
         }
-#endif
 
         // The partition's first chunk when its first edge is not on the 128-edge grid: on one
         // GPU the previous partition's last row ends there, so it takes the slow path with a
@@ -544,6 +528,18 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_r
     LaneCounters cnt{0u, 0u, 0u, 0ull};
     if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
     flush_counters(cnt, s_cnt, A.counters);
+}
+
+// Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.
+__global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
+                                                   PullCounters* counters) {
+    __shared__ unsigned long long s_cnt[4];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    LaneCounters c{0u, 0u, 0u, 0ull};
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row < rows) op.finish((int32_t)row, op.contrib_next[op.vbase + row], c);
+    flush_counters(c, s_cnt, counters);
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
