@@ -324,7 +324,7 @@ def main():
             achieved = float(np.mean(mb) / (float(t.item()) * 1e-3) / 1e9)  # per-rank bytes
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(),
-                "kernel": "k_pull_ranges<PageRankPull> + k_pull_fixup",
+                "kernel": "k_pull_ranges<PageRankSum> + k_pull_fixup + k_pr_finish",
                 "bytes_per_launch": float(np.mean(mb)),
                 "model": "12 B/edge (4 B index + 8 B gathered f64 outbox) + 16 B/vertex",
                 "avg_launch_ms": float(np.mean(k_ms)), "peak_source": peak_src,
