@@ -311,7 +311,7 @@ def main():
         d = delivered_messages(sts[0])
         apps_out[app] = {"gteps": d / (t_app * 1e-3) / 1e9, "ms": t_app,
                          "supersteps": int(sts[0]["supersteps"]),
-                         "modes": "".join("ilp"[m] for m in sts[0]["mode"])}
+                         "modes": "".join("ilpr"[m] for m in sts[0]["mode"])}
     roof = None
     if "pagerank" in args.apps:
         sts = [step["pagerank"] for step in per_step]

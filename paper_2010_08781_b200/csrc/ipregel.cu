@@ -97,6 +97,9 @@ uint64_t g_hot_bytes = read_hot_bytes();
 int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -2;
 // Tuning knob: PageRank update split out of the range kernel (IPREGEL_PR_SPLIT=1).
 int g_pr_split = getenv("IPREGEL_PR_SPLIT") ? atoi(getenv("IPREGEL_PR_SPLIT")) : 1;
+// Hash-Min row-list pull when the rows not yet at label 0 hold fewer than this fraction of the
+// symmetrised edges (IPREGEL_ROWLIST; 0 = never).
+double g_rowlist = getenv("IPREGEL_ROWLIST") ? atof(getenv("IPREGEL_ROWLIST")) : 0.05;
 uint64_t g_persist_bytes =
     getenv("IPREGEL_PERSIST_BYTES") ? strtoull(getenv("IPREGEL_PERSIST_BYTES"), nullptr, 10) : 0;
 
@@ -221,6 +224,7 @@ struct ipregel_graph {
     int last_vsz = 0;              // value bytes of the last run (8 PageRank / f64, 4 u32)
     int last_status = -1;
     int last_exchange = 0;         // 0 none, 1 collective, 2 fused
+    int64_t last_rowlist_edges = 0;
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
@@ -972,6 +976,34 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
 // =============================================================================================
 // Hash-Min CC (Fig. 9) and SSSP (Fig. 10)
 // =============================================================================================
+// Hash-Min row-list pull: compact every partition's owned rows whose label is not 0 into its
+// f_id list (front_cnt: count, symmetrised degree sum; host_cnt[4], [5]) and return the total
+// degree over all partitions / ranks (the edges a row-list superstep would touch).
+double rowlist_edges(ipregel_graph* g, int app, int cur) {
+    cudaStream_t s = g->stream;
+    for (auto& p : g->parts) {
+        AppState& S = p.st[app];
+        if (p.rows)
+            k_bits_ne<<<grid_for(p.rows, 256), 256, 0, s>>>(S.val[cur] + p.vb, p.rows, 0u, S.bits);
+        LAUNCH_CHECK();
+        compact_bitmap(g, p, S, S.val[cur], true);
+        CU(cudaMemcpyAsync(p.host_cnt + 4, p.front_cnt, 16, cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    double total = 0;
+    for (auto& p : g->parts) total += (double)p.host_cnt[5];
+    if (multi_rank(g)) {
+        Partition& p = g->parts[0];
+        CU(cudaMemcpyAsync(p.dscratch + 60, &p.front_cnt->messages, 8, cudaMemcpyDeviceToDevice, s));
+        NC(ncclAllReduce(p.dscratch + 60, p.dscratch + 61, 1, ncclUint64, ncclSum, g->comm->nccl, s));
+        CU(cudaMemcpyAsync(p.host_cnt + 6, p.dscratch + 61, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        total = (double)p.host_cnt[6];
+    }
+    g->last_rowlist_edges = (int64_t)total;
+    return total;
+}
+
 ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipregel_run_params& P) {
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
@@ -1040,6 +1072,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     g->steps[0].model_bytes = 4ull * (uint64_t)n;
     int cur = 0;
     int prev_mode = 0;
+    uint64_t zero_edges = 0;   // Hash-Min: symmetrised degree of the rows at label 0 (last pull)
     ipregel_status status = IPREGEL_OK;
 
     for (uint32_t step = 1; messages > 0; ++step) {
@@ -1104,6 +1137,52 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             changed = c[0];
             messages = c[1];
             lists_ready = true;
+        } else if (cc && g_rowlist > 0.0 &&
+                   (prev_mode == 3 || (prev_mode == 1 && (double)(pull_edges - zero_edges) <
+                                                             g_rowlist * (double)pull_edges))) {
+            // ---- row-list pull (Hash-Min): only the rows not at label 0 gather (once a row is
+            // at 0 it stays there, so the list only shrinks)
+            rowlist_edges(g, app, cur);   // their list in f_id / front_cnt
+            T.kbegin();
+            for (auto& p : g->parts) {
+                AppState& S = p.st[app];
+                if (p.rows == 0) continue;
+                CU(cudaMemcpyAsync(S.val[1 - cur] + p.vb, S.val[cur] + p.vb, p.rows * 4,
+                                   cudaMemcpyDeviceToDevice, s));
+                const PushAdj own{p.csc_off, p.csc_idx, nullptr, p.csr_off, p.csr_idx, nullptr,
+                                  p.vb, p.rows};
+                build_expand_list(g, p, S, own, S.f_id, nullptr, &p.front_cnt->changed,
+                                  (int64_t)p.host_cnt[4]);
+                const unsigned grid = (unsigned)std::min<int64_t>(
+                    std::max<int64_t>(ceil_div((int64_t)p.host_cnt[5], kExpandItems), 1), 148 * 8);
+                k_rowlist_min<<<grid, kExpandThreads, 0, s>>>(
+                    own, S.e_id, S.e_pre, &p.front_cnt->list_len, &p.front_cnt->list_edges,
+                    S.val[cur], S.val[1 - cur]);
+                LAUNCH_CHECK();
+            }
+            T.kend();
+            // broadcasters = rows whose label decreased; their count and symmetrised degrees
+            for (auto& p : g->parts) {
+                AppState& S = p.st[app];
+                k_bitmap_from_diff<<<grid_for(std::max<int64_t>(p.rows, 1), 256), 256, 0, s>>>(
+                    S.val[cur], S.val[1 - cur], p.vb, p.rows, S.bits);
+                LAUNCH_CHECK();
+                compact_bitmap(g, p, S, S.val[1 - cur], true);
+            }
+            const int nx = 1 - cur;
+            exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
+            unsigned long long c[2];
+            reduce_counters(g, true, c, 2);
+            T.end();
+            StepRecord& R = g->steps.back();
+            R.mode = 3;
+            mode = 3;
+            R.edges_scanned = (uint64_t)g->last_rowlist_edges;
+            R.model_bytes = 12ull * (uint64_t)g->last_rowlist_edges + 16ull * (uint64_t)n;
+            changed = c[0];
+            messages = c[1];
+            cur = 1 - cur;
+            lists_ready = false;
         } else {
             // ---- pull: gather over CSC (and CSR for CC), value[next] = min(value, gathered)
             for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
@@ -1137,8 +1216,9 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             // AllReduce below is the superstep barrier
             if (!fused)
                 exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
-            unsigned long long c[2];
-            reduce_counters(g, false, c, 2);
+            unsigned long long c[4];
+            reduce_counters(g, false, c, 4);
+            zero_edges = c[3];
             T.end();
             StepRecord& R = g->steps.back();
             R.mode = 1;

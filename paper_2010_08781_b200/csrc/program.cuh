@@ -142,7 +142,7 @@ __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int6
         c.changed += 1;
         c.messages += (uint32_t)x.out_degree + (A.sym ? (uint32_t)x.in_degree : 0u);
     }
-    c.active += act ? 1ull : 0ull;
+    c.aux += act ? 1ull : 0ull;
 }
 
 template <class P>
@@ -190,6 +190,7 @@ struct ProgPull : ProgArgs<typename P::V> {
     using T = typename P::V;
     using C = ProgComb<T, P::kCombiner>;
     static constexpr bool kWeighted = true;
+    static constexpr bool kAbsorbing = false;
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }

@@ -40,7 +40,8 @@ struct PullCounters {
     unsigned long long changed;
     unsigned long long messages;
     unsigned long long dmax;   // PageRank to convergence: max |r_s - r_{s-1}| as f64 bits (>= 0)
-    unsigned long long active; // user programs: vertices that did not vote to halt
+    unsigned long long aux;    // user programs: vertices that did not vote to halt; Hash-Min:
+                               // symmetrised degree of the rows at label 0 after the superstep
 };
 
 // A thread's share of the counters while it runs, 32-bit (fewer live registers in the range
@@ -48,7 +49,7 @@ struct PullCounters {
 // at most 2E < 2^32 for the symmetrised graph since E <= INT32_MAX (validated at create).
 struct LaneCounters {
     uint32_t changed;
-    uint32_t active;
+    uint32_t aux;
     uint32_t messages;
     unsigned long long dmax;
 };
@@ -114,6 +115,12 @@ struct MinU32 {
     __device__ static T combine(T a, T b) { return a > b ? b : a; }   // Fig. 5 ip_combine
 };
 
+// Ops whose result is settled once a row's partial reaches an absorbing value (Hash-Min: label
+// 0, the smallest id, cannot be lowered) stop gathering the rest of that row.
+struct NotAbsorbing {
+    static constexpr bool kAbsorbing = false;
+};
+
 // ---- fused exchange ---------------------------------------------------------
 // Every OTHER replica of the broadcast array that must receive this partition's owned slice: peer
 // GPUs' replicas mapped over NVLink (CUDA IPC) for ranks of a communicator, or the other
@@ -136,7 +143,7 @@ struct PeerSlots {
 // finish = recipient compute --------------------------------------------------------------------
 // PageRank, Fig. 8: the message of u is contrib[u] = r_u / outdeg(u); recipient compute is
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
-struct PageRankPull : SumF64 {
+struct PageRankPull : SumF64, NotAbsorbing {
     static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
@@ -172,7 +179,7 @@ struct PageRankPull : SumF64 {
 // PageRank with the update split out of the range kernel (IPREGEL_PR_SPLIT=1): the range kernel
 // only stores each row's combined sum into its next-outbox slot, and k_pr_finish applies Fig. 8's
 // update row-parallel (same operations, same result).
-struct PageRankSum : SumF64 {
+struct PageRankSum : SumF64, NotAbsorbing {
     static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;
     double* __restrict__ sum_out;             // = contrib_next of the superstep (global ids)
@@ -187,6 +194,8 @@ struct PageRankSum : SumF64 {
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
 struct CCPullIn : MinU32 {
     static constexpr bool kWeighted = false;
+    static constexpr bool kAbsorbing = true;
+    __device__ static bool absorbing(T x) { return x == 0u; }
     const uint32_t* __restrict__ cur;   // replica, global ids
     uint32_t* __restrict__ next;        // replica, global ids (owned slice written)
     int64_t vbase;
@@ -205,6 +214,8 @@ struct CCPullIn : MinU32 {
 // "if value < old: broadcast" -> changed / messages counters (degree in the symmetrised graph).
 struct CCPullOut : MinU32 {
     static constexpr bool kWeighted = false;
+    static constexpr bool kAbsorbing = true;
+    __device__ static bool absorbing(T x) { return x == 0u; }
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
     const int32_t* __restrict__ in_off;   // owned CSC offsets
@@ -221,17 +232,19 @@ struct CCPullOut : MinU32 {
         v = m < v ? m : v;
         next[vbase + row] = v;
         peers.store(vbase + row, v);
+        const uint32_t deg = (uint32_t)(in_off[row + 1] - in_off[row]) +
+                             (uint32_t)(out_off[row + 1] - out_off[row]);
         if (v < old) {
             c.changed += 1;
-            c.messages += (uint32_t)(in_off[row + 1] - in_off[row]) +
-                          (uint32_t)(out_off[row + 1] - out_off[row]);
+            c.messages += deg;
         }
+        if (v == 0u) c.aux += deg;   // absorbed rows (row-list pull decision)
     }
 };
 
 // SSSP, Fig. 10 with weights: message on edge (u -> v, w) is sat(dist_u + w), applied at the
 // recipient from the CSC weight (reading R8); "if mindist < value: broadcast".
-struct SSSPPull : MinU32 {
+struct SSSPPull : MinU32, NotAbsorbing {
     static constexpr bool kWeighted = true;
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
@@ -338,7 +351,7 @@ struct RangeArgs {
 __device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned long long* s_cnt,
                                                PullCounters* counters) {
     const int lane = threadIdx.x & 31;
-    unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax, c3 = cnt.active;
+    unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax, c3 = cnt.aux;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         c0 += __shfl_xor_sync(kFull, c0, d);
@@ -358,7 +371,7 @@ __device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned
         atomicAdd(&counters->changed, s_cnt[0]);
         atomicAdd(&counters->messages, s_cnt[1]);
         atomicMax(&counters->dmax, s_cnt[2]);
-        atomicAdd(&counters->active, s_cnt[3]);
+        atomicAdd(&counters->aux, s_cnt[3]);
     }
 }
 
@@ -425,6 +438,10 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         if (!part_head && (r >= x1 || Ec > e0 + kChunk)) {
             // fast path: the whole chunk belongs to row r (no row ends here)
             la = Op::combine(la, Op::combine(Op::combine(v[0], v[1]), Op::combine(v[2], v[3])));
+            if constexpr (Op::kAbsorbing) {
+                // the open row's partial reached the absorbing value: skip its remaining gathers
+                if (!absorbed) absorbed = __any_sync(kFull, Op::absorbing(la));
+            }
             continue;
         }
         // slow path: rows end in this chunk.  Fold the lane partials of row r first.
@@ -504,6 +521,9 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         absorbed = r < x1 && op.absorbed(r);
         if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
         carry = next_carry;
+        if constexpr (Op::kAbsorbing) {
+            if (!absorbed && r < x1) absorbed = Op::absorbing(carry);   // carry is warp-uniform
+        }
         __syncwarp();
     }
     // rows finished after the last edge of the range (rows without in-edges)
@@ -566,11 +586,11 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
         acc = Op::combine(acc, head[G.z]);
         LaneCounters c{0u, 0u, 0u, 0ull};
         op.finish(G.x, acc, c);
-        if (counters && (c.changed | c.messages | c.dmax | c.active)) {
+        if (counters && (c.changed | c.messages | c.dmax | c.aux)) {
             atomicAdd(&counters->changed, c.changed);
             atomicAdd(&counters->messages, c.messages);
             atomicMax(&counters->dmax, c.dmax);
-            atomicAdd(&counters->active, c.active);
+            atomicAdd(&counters->aux, c.aux);
         }
     }
 }

@@ -376,6 +376,41 @@ k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restri
                  BuiltinDeliver<kProgram>{dst_base, val, bits, contrib, acc});
 }
 
+// ---- Hash-Min row-list pull -----------------------------------------------------------------
+// Once most rows hold label 0 (the smallest id, absorbing for min: PAPER.md:341-344 never lowers
+// it further), a dense pull superstep spends its time streaming rows whose result is already
+// known.  The row-list pull runs the same gather-combine only over the rows NOT at 0: the owned
+// rows are compacted into a list (the frontier machinery above), and the edges of the listed rows
+// (CSC row + CSR row: the symmetrised neighbourhood) are expanded edge-balanced, each folding its
+// neighbour's label into the row's next value with atomicMin (min is exact in any order).
+struct RowMinDeliver {
+    const uint32_t* cur;   // labels after superstep s-1 (replica, global ids)
+    uint32_t* next;        // next[u] = cur[u] on entry (owned rows), min over neighbours on exit
+    __device__ __forceinline__ void operator()(int32_t u, uint32_t, int32_t v, uint32_t) const {
+        const uint32_t m = cur[v];
+        if (m < next[u]) atomicMin(next + u, m);
+    }
+};
+
+__global__ void __launch_bounds__(kExpandThreads)
+k_rowlist_min(PushAdj adj, const int32_t* __restrict__ e_id, const long long* __restrict__ e_pre,
+              const unsigned long long* __restrict__ len,
+              const unsigned long long* __restrict__ edges, const uint32_t* __restrict__ cur,
+              uint32_t* __restrict__ next) {
+    adj.w1 = nullptr;
+    adj.w2 = nullptr;
+    expand_edges(adj, e_id, nullptr, e_pre, len, edges, RowMinDeliver{cur, next});
+}
+
+// Owned rows whose value is not `v0` (ballot per warp).
+__global__ void k_bits_ne(const uint32_t* __restrict__ vals, int64_t rows, uint32_t v0,
+                          uint32_t* __restrict__ bits) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool pred = i < rows && vals[i] != v0;
+    const uint32_t b = __ballot_sync(kFull, pred);
+    if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
+}
+
 // Pull -> push switch: the broadcasters of a pull superstep are the vertices whose value
 // decreased; mark them in the bitmap (owned range, ballot per warp).
 __global__ void k_bitmap_from_diff(const uint32_t* __restrict__ before,

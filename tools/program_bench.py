@@ -61,8 +61,8 @@ for parts in [int(x) for x in a.parts.split(",")]:
             row = {"parts": parts, "exchange": ex, "app": app, "builtin_ms": round(t_b, 3),
                    "program_ms": round(t_p, 3), "supersteps": int(s_b["supersteps"]),
                    "program_supersteps": int(s_p["supersteps"]),
-                   "builtin_modes": "".join("ilp"[m] for m in s_b["mode"]),
-                   "program_modes": "".join("ilp"[m] for m in s_p["mode"])}
+                   "builtin_modes": "".join("ilpr"[m] for m in s_b["mode"]),
+                   "program_modes": "".join("ilpr"[m] for m in s_p["mode"])}
             out["rows"].append(row)
             print(json.dumps(row), flush=True)
     G.close()
