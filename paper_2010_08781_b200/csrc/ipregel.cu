@@ -104,6 +104,10 @@ uint64_t g_persist_bytes =
     getenv("IPREGEL_PERSIST_BYTES") ? strtoull(getenv("IPREGEL_PERSIST_BYTES"), nullptr, 10) : 0;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline uint32_t sat_add_host(uint32_t a, uint32_t b) {
+    const uint64_t s = (uint64_t)a + b;
+    return s >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)s;
+}
 inline unsigned grid_for(int64_t n, int threads) {
     int64_t g = ceil_div(std::max<int64_t>(n, 1), threads);
     return (unsigned)std::min<int64_t>(g, 0x7FFFFFFF);
@@ -225,6 +229,7 @@ struct ipregel_graph {
     int last_status = -1;
     int last_exchange = 0;         // 0 none, 1 collective, 2 fused
     int64_t last_rowlist_edges = 0;
+    int64_t w_min = -1;            // smallest edge weight (SSSP absorption bound), lazily
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
@@ -976,6 +981,33 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
 // =============================================================================================
 // Hash-Min CC (Fig. 9) and SSSP (Fig. 10)
 // =============================================================================================
+// Smallest edge weight of the graph (1 without weights), over partitions / ranks; computed once.
+uint32_t min_weight(ipregel_graph* g) {
+    if (g->w_min >= 0) return (uint32_t)g->w_min;
+    cudaStream_t s = g->stream;
+    Partition& p0 = g->parts[0];
+    unsigned long long m = 1;
+    if (p0.csc_w) {
+        DeviceBuffers tmp;
+        unsigned* d = tmp.alloc<unsigned>(2, s);
+        CU(cudaMemsetAsync(d, 0xFF, 8, s));
+        for (auto& p : g->parts)
+            if (p.csc_edges)
+                k_min_u32<<<std::min<unsigned>(grid_for(p.csc_edges, 256), 4096), 256, 0, s>>>(
+                    p.csc_w, p.csc_edges, d);
+        LAUNCH_CHECK();
+        if (multi_rank(g))
+            NC(ncclAllReduce(d, d + 1, 1, ncclUint32, ncclMin, g->comm->nccl, s));
+        unsigned h[2] = {0, 0};
+        CU(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        tmp.release();
+        m = multi_rank(g) ? h[1] : h[0];
+    }
+    g->w_min = (int64_t)m;
+    return (uint32_t)m;
+}
+
 // Hash-Min row-list pull: compact every partition's owned rows whose label is not 0 into its
 // f_id list (front_cnt: count, symmetrised degree sum; host_cnt[4], [5]) and return the total
 // degree over all partitions / ranks (the edges a row-list superstep would touch).
@@ -1073,6 +1105,10 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     int cur = 0;
     int prev_mode = 0;
     uint64_t zero_edges = 0;   // Hash-Min: symmetrised degree of the rows at label 0 (last pull)
+    // SSSP absorption bound: smallest distance that changed in the last superstep (the source's
+    // 0 after superstep 0) plus the smallest edge weight
+    const uint32_t w_min = cc ? 0u : min_weight(g);
+    uint32_t m_prev = 0;
     ipregel_status status = IPREGEL_OK;
 
     for (uint32_t step = 1; messages > 0; ++step) {
@@ -1125,6 +1161,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             T.kend();
             // broadcasters of this superstep -> next frontier (+ counters)
             for (auto& p : g->parts) compact_bitmap(g, p, p.st[app], p.st[app].val[cur], cc);
+
             if (multi) exchange_frontier(g, app, frontier_counts(g), cur);
             unsigned long long c[2];
             reduce_counters(g, true, c, 2);
@@ -1185,6 +1222,20 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             lists_ready = false;
         } else {
             // ---- pull: gather over CSC (and CSR for CC), value[next] = min(value, gathered)
+            if (!cc && prev_mode == 2) {
+                // absorption bound after a push superstep: the smallest distance among its
+                // broadcasters (the owned frontier lists still hold their snapshots)
+                for (auto& p : g->parts) {
+                    CU(cudaMemsetAsync(&p.pull_cnt->dmax, 0, 8, s));
+                    k_list_max_inv<<<std::max<unsigned>(1u, std::min<unsigned>(
+                                         grid_for((int64_t)std::max<uint64_t>(changed, 1), 256),
+                                         1024)),
+                                     256, 0, s>>>(p.st[app].f_val, &p.front_cnt->changed,
+                                                  &p.pull_cnt->dmax);
+                    LAUNCH_CHECK();
+                }
+                m_prev = (uint32_t)(kInf - (uint32_t)reduce_max_delta(g));
+            }
             for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
             T.kbegin();
             for (auto& p : g->parts) {
@@ -1206,6 +1257,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                     a.cur = S.val[cur]; a.next = S.val[1 - cur];
                     a.out_off = p.csr_off; a.vbase = p.vb;
                     a.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
+                    a.thr = sat_add_host(m_prev, w_min);
                     launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.pull_cnt, s, n,
                                 g->gather_policy, g->degree_ordered);
                 }
@@ -1219,6 +1271,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             unsigned long long c[4];
             reduce_counters(g, false, c, 4);
             zero_edges = c[3];
+            if (!cc) m_prev = (uint32_t)(kInf - (uint32_t)reduce_max_delta(g));
             T.end();
             StepRecord& R = g->steps.back();
             R.mode = 1;

@@ -244,16 +244,25 @@ struct CCPullOut : MinU32 {
 
 // SSSP, Fig. 10 with weights: message on edge (u -> v, w) is sat(dist_u + w), applied at the
 // recipient from the CSC weight (reading R8); "if mindist < value: broadcast".
-struct SSSPPull : MinU32, NotAbsorbing {
+//
+// Absorption bound: every message of superstep s comes from a vertex that changed in s-1 (E1), so
+// it is >= thr = sat(m + w_min), m the smallest distance that changed in s-1 and w_min the
+// smallest edge weight; a row already at or below thr -- or whose partial reaches thr -- cannot
+// change, and its remaining gathers are skipped.  finish() reports m for the next superstep (as
+// INF - dist in the max-reduced dmax counter).
+struct SSSPPull : MinU32 {
     static constexpr bool kWeighted = true;
+    static constexpr bool kAbsorbing = true;
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
     PeerSlots<uint32_t> peers;            // fused exchange: other replicas of `next`
+    uint32_t thr;                         // absorption bound (0: none below the source)
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
-    __device__ bool absorbed(int32_t) const { return false; }
+    __device__ bool absorbed(int32_t row) const { return cur[vbase + row] <= thr; }
+    __device__ bool absorbing(T x) const { return x <= thr; }
     __device__ static T message(T g, uint32_t w) { return sat_add(g, w); }
     __device__ void finish(int32_t row, T m, LaneCounters& c) const {
         const uint32_t old = cur[vbase + row];
@@ -263,6 +272,8 @@ struct SSSPPull : MinU32, NotAbsorbing {
         if (v < old) {
             c.changed += 1;
             c.messages += (uint32_t)(out_off[row + 1] - out_off[row]);
+            const unsigned long long inv = (unsigned long long)(kInf - v);
+            c.dmax = inv > c.dmax ? inv : c.dmax;
         }
     }
 };
@@ -440,7 +451,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
             la = Op::combine(la, Op::combine(Op::combine(v[0], v[1]), Op::combine(v[2], v[3])));
             if constexpr (Op::kAbsorbing) {
                 // the open row's partial reached the absorbing value: skip its remaining gathers
-                if (!absorbed) absorbed = __any_sync(kFull, Op::absorbing(la));
+                if (!absorbed) absorbed = __any_sync(kFull, op.absorbing(la));
             }
             continue;
         }
@@ -522,7 +533,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
         carry = next_carry;
         if constexpr (Op::kAbsorbing) {
-            if (!absorbed && r < x1) absorbed = Op::absorbing(carry);   // carry is warp-uniform
+            if (!absorbed && r < x1) absorbed = op.absorbing(carry);   // carry is warp-uniform
         }
         __syncwarp();
     }

@@ -30,6 +30,40 @@ __global__ void k_bits_from_flags(const uint8_t* __restrict__ flags, int64_t row
     if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
 }
 
+// Max of (INF - value) over a device list of values (SSSP: the smallest distance among a push
+// superstep's broadcasters, for the absorption bound of SSSPPull).
+__global__ void k_list_max_inv(const uint32_t* __restrict__ vals,
+                               const unsigned long long* __restrict__ len,
+                               unsigned long long* __restrict__ out) {
+    const int64_t n = (int64_t)*len;
+    unsigned long long m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = (unsigned long long)(kInf - vals[i]);
+        m = x > m ? x : m;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// Min of a u32 array (SSSP: the smallest edge weight), into *out (initialised to INF).
+__global__ void k_min_u32(const uint32_t* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
+    unsigned m = kInf;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = a[i] < m ? a[i] : m;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned o = __shfl_xor_sync(kFull, m, d);
+        m = o < m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
 // Hash-Min CC, Fig. 9: value = id, the ORIGINAL id under a relabelled layout (every replica
 // initialises all N locally -- no exchange).
 __global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n, const int32_t* __restrict__ ids) {

@@ -560,3 +560,24 @@ def test_pagerank_to_convergence_cfg3_scale():
     # deltas are differences of f64 sums taken in another order: equal up to ~1e-16 absolute
     np.testing.assert_allclose(s["pagerank_delta"], d, rtol=1e-9, atol=1e-15)
     G.close()
+
+
+# ------------------------------------------------------------------ Hash-Min row-list pull
+
+@pytest.mark.parametrize("parts,mode", [(1, "pull"), (3, "pull"), (1, "auto"), (2, "auto")])
+def test_cc_rowlist_pull_matches_oracle(parts, mode):
+    """Once the rows not at label 0 hold < 5 % of the symmetrised edges, pull supersteps gather
+    only over those rows (mode 3 in the stats); values and every counter stay the oracle's."""
+    import inputs
+    src, dst, _ = inputs.rmat_coo(14, 16, 33)
+    n = 1 << 14
+    o = oracle.hashmin_cc(n, src, dst)
+    G = make_graph(csr_csc(n, src, dst), partitions=parts, weighted=False)
+    G.run("cc", mode=mode, push_fraction=0.0 if mode == "pull" else 0.001)
+    s = G.stats()
+    np.testing.assert_array_equal(G.values(host=True), o["values"])
+    assert s["supersteps"] == o["supersteps"]
+    np.testing.assert_array_equal(s["changed"], o["changed"])
+    np.testing.assert_array_equal(s["messages"], o["messages"])
+    assert 3 in list(s["mode"]), list(s["mode"])
+    G.close()
