@@ -110,9 +110,13 @@ typedef struct ipregel_comm ipregel_comm;   /* opaque; NULL means a single GPU *
  *   csc_*: in-edges of the owned vertices ("CSC", the in-adjacency of PAPER.md:123).  Row r
  *          lists the sources u of edges (u -> vertex_begin + r).  Required.
  *   csr_*: out-edges of the owned vertices (the out-adjacency).  Row r lists the destinations v
- *          of edges (vertex_begin + r -> v).  Required: out-degrees come from it (PageRank's
- *          r/outdeg, messages counters), Hash-Min CC gathers over it (the reverse direction of
- *          the symmetrised graph) and push mode expands over it.
+ *          of edges (vertex_begin + r -> v).  Out-degrees come from it (PageRank's r/outdeg,
+ *          messages counters), Hash-Min CC gathers over it (the reverse direction of the
+ *          symmetrised graph) and push mode expands over it.  If csr_offsets, csr_indices and
+ *          csr_weights are ALL NULL, the library derives the out-adjacency (and its weights) by
+ *          transposing the CSC on the device during create (library-owned memory; the order of
+ *          neighbours inside a derived row is unspecified).  Only for a graph held whole in one
+ *          partition (vertex range [0, N), csc_edges == num_edges), else UNSUPPORTED.
  *   *_weights: uint32 weight per stored edge, aligned with *_indices, used by SSSP only; NULL
  *          means every weight is 1.  csc_weights and csr_weights must both be NULL or both set.
  */

@@ -125,22 +125,50 @@ struct ipregel_comm {
 
 namespace {
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync), which keeps up to
+// IPREGEL_POOL_RETAIN_BYTES (default 64 GiB) of freed memory for the next graph instead of
+// returning it to the driver: creating and destroying a graph handle per job stays cheap (a
+// plain cudaMalloc/cudaFree of the 7.5 GB adjacency copies costs ~100 ms each).  Buffers another
+// process maps with CUDA IPC (fused-exchange replicas of a rank) use cudaMalloc.
+void configure_pool(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    done[device] = true;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    const char* e = getenv("IPREGEL_POOL_RETAIN_BYTES");
+    uint64_t keep = e ? strtoull(e, nullptr, 10) : (64ull << 30);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
 struct DeviceBuffers {
-    std::vector<void*> ptrs;
+    struct Block {
+        void* p;
+        cudaStream_t s;   // pooled: freed on this stream; nullptr with ipc = cudaFree
+        bool ipc;
+    };
+    std::vector<Block> blocks;
     uint64_t bytes = 0;
     template <class T>
-    T* alloc(int64_t count, cudaStream_t s, bool zero = false) {
+    T* alloc(int64_t count, cudaStream_t s, bool zero = false, bool ipc = false) {
         void* p = nullptr;
         size_t b = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
-        CU(cudaMalloc(&p, b));
-        ptrs.push_back(p);
+        if (ipc) CU(cudaMalloc(&p, b));
+        else CU(cudaMallocAsync(&p, b, s));
+        blocks.push_back(Block{p, s, ipc});
         bytes += b;
         if (zero) CU(cudaMemsetAsync(p, 0, b, s));
         return static_cast<T*>(p);
     }
     void release() {
-        for (void* p : ptrs) cudaFree(p);
-        ptrs.clear();
+        for (const Block& k : blocks) {
+            if (k.ipc) cudaFree(k.p);
+            else cudaFreeAsync(k.p, k.s);
+        }
+        blocks.clear();
         bytes = 0;
     }
 };
@@ -442,14 +470,15 @@ void ensure_state(ipregel_graph* g, int app) {
         if (S.ready) continue;
         cudaStream_t s = g->stream;
         const int64_t n = g->n;
+        const bool ipc = multi_rank(g);   // replicas a peer maps for the fused exchange
         if (app == IPREGEL_APP_PAGERANK) {
             S.rank = S.mem.alloc<double>(p.rows, s);
-            S.contrib[0] = S.mem.alloc<double>(n, s, true);
-            S.contrib[1] = S.mem.alloc<double>(n, s, true);
+            S.contrib[0] = S.mem.alloc<double>(n, s, true, ipc);
+            S.contrib[1] = S.mem.alloc<double>(n, s, true, ipc);
         } else if (app == kAppProgram) {
             S.pv_value = S.mem.alloc<uint64_t>(p.rows, s, true);
-            S.pv_out[0] = S.mem.alloc<uint64_t>(n, s, true);
-            S.pv_out[1] = S.mem.alloc<uint64_t>(n, s, true);
+            S.pv_out[0] = S.mem.alloc<uint64_t>(n, s, true, ipc);
+            S.pv_out[1] = S.mem.alloc<uint64_t>(n, s, true, ipc);
             S.pv_mbox = S.mem.alloc<uint64_t>(p.rows, s, true);
             S.pv_flags = S.mem.alloc<uint8_t>(p.rows, s, true);
             S.pv_recv = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
@@ -467,8 +496,8 @@ void ensure_state(ipregel_graph* g, int app) {
                 S.g_len = &p.front_cnt->changed;
             }
         } else {
-            S.val[0] = S.mem.alloc<uint32_t>(n, s);
-            S.val[1] = S.mem.alloc<uint32_t>(n, s);
+            S.val[0] = S.mem.alloc<uint32_t>(n, s, false, ipc);
+            S.val[1] = S.mem.alloc<uint32_t>(n, s, false, ipc);
             S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.f_id = S.mem.alloc<int32_t>(p.rows, s);
             S.f_val = S.mem.alloc<uint32_t>(p.rows, s);
@@ -511,6 +540,37 @@ void exscan_i32(int32_t* a, int64_t n, DeviceBuffers& tmp, cudaStream_t s) {
     LAUNCH_CHECK();
 }
 
+// Transpose of a partition's rows (row r lists neighbours u) into a source-major adjacency over all
+// N sources (u lists vb + r), allocated in the partition's graph memory.  Counting sort with an
+// atomic cursor per source: the order inside a row is not deterministic (every consumer of a
+// transposed adjacency combines with min, or with a sum that is order-nondeterministic anyway).
+void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* idx,
+                    const uint32_t* w, int64_t edges, bool want_w, cudaStream_t s,
+                    int32_t** out_off, int32_t** out_idx, uint32_t** out_w) {
+    int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+    int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
+    uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
+    if (edges > 0) {
+        k_hist_sources<<<grid_for(edges, 256) > 4096 ? 4096 : grid_for(edges, 256), 256, 0, s>>>(
+            idx, edges, o);
+        LAUNCH_CHECK();
+    }
+    DeviceBuffers tmp;
+    exscan_i32(o, n + 1, tmp, s);
+    int32_t* cursor = tmp.alloc<int32_t>(n + 1, s);
+    CU(cudaMemcpyAsync(cursor, o, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (p.rows > 0) {
+        k_transpose_rows<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, idx, w, p.rows, p.vb,
+                                                                   cursor, ix, wx);
+        LAUNCH_CHECK();
+    }
+    CU(cudaStreamSynchronize(s));
+    tmp.release();
+    *out_off = o;
+    *out_idx = ix;
+    if (out_w) *out_w = wx;
+}
+
 // Push adjacency of one partition.  One partition: the graph's own CSR (+ CSC for CC).  Several:
 // transposes of the owned CSC (and, for CC, owned CSR) rows, over all N sources.
 void ensure_push_view(ipregel_graph* g, Partition& p) {
@@ -525,28 +585,7 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     }
     auto transpose = [&](const int32_t* off, const int32_t* idx, const uint32_t* w, int64_t edges,
                          bool want_w, int32_t** out_off, int32_t** out_idx, uint32_t** out_w) {
-        int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
-        int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
-        uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
-        if (edges > 0) {
-            k_hist_sources<<<grid_for(edges, 256) > 4096 ? 4096 : grid_for(edges, 256), 256, 0, s>>>(
-                idx, edges, o);
-            LAUNCH_CHECK();
-        }
-        DeviceBuffers tmp;
-        exscan_i32(o, n + 1, tmp, s);
-        int32_t* cursor = tmp.alloc<int32_t>(n + 1, s);
-        CU(cudaMemcpyAsync(cursor, o, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        if (p.rows > 0) {
-            k_transpose_rows<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, idx, w, p.rows, p.vb,
-                                                                       cursor, ix, wx);
-            LAUNCH_CHECK();
-        }
-        CU(cudaStreamSynchronize(s));
-        tmp.release();
-        *out_off = o;
-        *out_idx = ix;
-        if (out_w) *out_w = wx;
+        transpose_rows(p, n, off, idx, w, edges, want_w, s, out_off, out_idx, out_w);
     };
     int32_t *o1, *i1, *o2, *i2;
     uint32_t *w1 = nullptr, *w2 = nullptr;
@@ -1306,11 +1345,16 @@ void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
     if (d->csc_edges < 0 || d->csr_edges < 0 || d->csc_edges > d->num_edges ||
         d->csr_edges > d->num_edges)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "csc_edges/csr_edges out of range");
-    if (!d->csc_offsets || !d->csr_offsets || (d->csc_edges > 0 && !d->csc_indices) ||
-        (d->csr_edges > 0 && !d->csr_indices))
+    const bool derive_csr = !d->csr_offsets && !d->csr_indices && !d->csr_weights;
+    if (!d->csc_offsets || (!derive_csr && !d->csr_offsets) || (d->csc_edges > 0 && !d->csc_indices) ||
+        (!derive_csr && d->csr_edges > 0 && !d->csr_indices))
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "required CSC/CSR array is NULL");
-    if ((d->csc_weights == nullptr) != (d->csr_weights == nullptr))
+    if (!derive_csr && (d->csc_weights == nullptr) != (d->csr_weights == nullptr))
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "csc_weights and csr_weights must both be set or NULL");
+    if (derive_csr && (d->vertex_begin != 0 || d->vertex_end != d->num_vertices ||
+                       d->csc_edges != d->num_edges))
+        fail(IPREGEL_ERR_UNSUPPORTED,
+             "deriving the CSR from the CSC needs the whole graph in one partition");
     if (d->memory != IPREGEL_MEMORY_DEVICE && d->memory != IPREGEL_MEMORY_HOST)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown memory kind %d", d->memory);
     if (d->reserved != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "reserved must be 0");
@@ -1345,10 +1389,12 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         p.csc_off = d.csc_offsets; p.csc_idx = d.csc_indices; p.csc_w = d.csc_weights;
         p.csr_off = d.csr_offsets; p.csr_idx = d.csr_indices; p.csr_w = d.csr_weights;
     }
+
     if (d.validate) {
         unsigned* flags = p.graph_mem.alloc<unsigned>(1, s, true);
         k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csc_off, p.rows, p.csc_edges, flags);
-        k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csr_off, p.rows, p.csr_edges, flags);
+        if (p.csr_off)
+            k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csr_off, p.rows, p.csr_edges, flags);
         LAUNCH_CHECK();
         unsigned h = 0;
         CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s));
@@ -1357,7 +1403,7 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
             if (p.csc_edges)
                 k_validate_indices<<<std::min<unsigned>(grid_for(p.csc_edges, 256), 4096), 256, 0, s>>>(
                     p.csc_idx, p.csc_edges, g->n, flags);
-            if (p.csr_edges)
+            if (p.csr_edges && p.csr_idx)
                 k_validate_indices<<<std::min<unsigned>(grid_for(p.csr_edges, 256), 4096), 256, 0, s>>>(
                     p.csr_idx, p.csr_edges, g->n, flags);
             LAUNCH_CHECK();
@@ -1368,6 +1414,19 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
             fail(IPREGEL_ERR_INVALID_GRAPH, "graph validation failed (flags 0x%x: %s%s%s)", h,
                  (h & 1) ? "offsets[0]/offsets[rows] " : "", (h & 2) ? "non-monotone offsets " : "",
                  (h & 4) ? "index out of range" : "");
+    }
+    if (!d.csr_offsets && !d.csr_indices) {
+        // out-adjacency (and its weights) derived from the CSC on the device: the transpose of
+        // the whole graph's in-edges (single partition, checked by validate_desc;
+        // after the validation: the transpose indexes by the CSC sources)
+        int32_t *o, *ix;
+        uint32_t* wx = nullptr;
+        transpose_rows(p, g->n, p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, s,
+                       &o, &ix, &wx);
+        p.csr_off = o;
+        p.csr_idx = ix;
+        p.csr_w = wx;
+        p.csr_edges = p.csc_edges;
     }
     p.pull_cnt = p.graph_mem.alloc<PullCounters>(1, s, true);
     p.dscratch = p.graph_mem.alloc<unsigned long long>(64, s, true);
@@ -1409,9 +1468,8 @@ void destroy_graph(ipregel_graph* g) {
         p.host_cnt = nullptr;
     }
     for (auto e : g->events) cudaEventDestroy(e);
-    if (g->gather_tmp) cudaFree(g->gather_tmp);
-    if (g->gather_tmp2) cudaFree(g->gather_tmp2);
     g->graph_mem.release();
+    cudaStreamSynchronize(g->stream);
     delete g;
 }
 
@@ -1912,6 +1970,7 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
     int device = 0;
     CU(cudaGetDevice(&device));
     check_device(device);
+    configure_pool(device);
     ipregel_graph* g = new ipregel_graph;
     g->n = n;
     g->e = descs[0].num_edges;
@@ -2177,7 +2236,7 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
         // full N-vector in internal order (device)
         const void* full = nullptr;
         if (owned) {
-            if (!g->gather_tmp) CU(cudaMalloc(&g->gather_tmp, g->n * sizeof(double)));
+            if (!g->gather_tmp) g->gather_tmp = g->graph_mem.alloc<double>(g->n, s);
             uint8_t* base = reinterpret_cast<uint8_t*>(g->gather_tmp);
             for (auto& p : g->parts) {
                 const void* src = g->last_app == IPREGEL_APP_PAGERANK ? (const void*)p.st[0].rank
@@ -2200,7 +2259,7 @@ ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
             full = g->parts[0].st[g->last_app].val[g->cur];
         }
         if (g->vertex_ids) {
-            if (!g->gather_tmp2) CU(cudaMalloc(&g->gather_tmp2, g->n * sizeof(double)));
+            if (!g->gather_tmp2) g->gather_tmp2 = g->graph_mem.alloc<double>(g->n, s);
             if (esz == 8)
                 k_to_original<double><<<grid_for(g->n, 256), 256, 0, s>>>(
                     (const double*)full, g->vertex_ids, g->n, g->gather_tmp2);

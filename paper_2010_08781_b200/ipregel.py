@@ -289,7 +289,7 @@ class Partition:
     vertex_end: int
     csc_offsets: object
     csc_indices: object
-    csr_offsets: object
+    csr_offsets: object            # None (with csr_indices, csr_weights): derived on the device
     csr_indices: object
     csc_weights: object = None
     csr_weights: object = None
@@ -304,7 +304,7 @@ class Partition:
         d.vertex_begin = self.vertex_begin
         d.vertex_end = self.vertex_end
         d.csc_edges = int(self.csc_indices.shape[0])
-        d.csr_edges = int(self.csr_indices.shape[0])
+        d.csr_edges = 0 if self.csr_indices is None else int(self.csr_indices.shape[0])
         d.csc_offsets = _ptr(self.csc_offsets)
         d.csc_indices = _ptr(self.csc_indices)
         d.csc_weights = _ptr(self.csc_weights)

@@ -581,3 +581,55 @@ def test_cc_rowlist_pull_matches_oracle(parts, mode):
     np.testing.assert_array_equal(s["messages"], o["messages"])
     assert 3 in list(s["mode"]), list(s["mode"])
     G.close()
+
+
+# ------------------------------------------------------------------ CSR derived from the CSC
+
+@pytest.mark.parametrize("host", [False, True])
+def test_csr_derived_on_device_matches_given_csr(host):
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    rng = np.random.default_rng(31)
+    n = 2500
+    src, dst, w = checkers.random_graph(rng, n, 15000, weighted=True)
+    g = csr_csc(n, src, dst, w)
+    full = make_graph(g)
+    if host:
+        h = {k: np.ascontiguousarray(g[k]).view(np.int32) for k in ("csc_off", "csc_idx", "csc_w")}
+        part = ipr.Partition(n, g["e"], 0, n, h["csc_off"], h["csc_idx"], None, None, h["csc_w"], None)
+    else:
+        d = to_device(g)
+        part = ipr.Partition(n, g["e"], 0, n, d["csc_off"], d["csc_idx"], None, None, d["csc_w"], None)
+    derived = ipr.Graph(part, validate=True)
+    for app, mode in (("pagerank", "pull"), ("pagerank", "push"), ("cc", "pull"), ("cc", "push"),
+                      ("cc", "auto"), ("sssp", "pull"), ("sssp", "push"), ("sssp", "auto")):
+        full.run(app, mode=mode, source=3)
+        derived.run(app, mode=mode, source=3)
+        a, b = full.values(host=True), derived.values(host=True)
+        if app == "pagerank" and mode == "push":
+            assert np.abs(a - b).max() <= 1e-15
+        else:
+            np.testing.assert_array_equal(a, b)
+        sa, sb = full.stats(), derived.stats()
+        np.testing.assert_array_equal(sa["messages"], sb["messages"])
+    o = oracle.sssp(n, src, dst, w, source=3)
+    np.testing.assert_array_equal(derived.values(host=True), o["values"])
+    full.close()
+    derived.close()
+
+
+def test_csr_derivation_needs_one_whole_partition():
+    import ctypes
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    n = 100
+    src = np.arange(n - 1)
+    d = to_device(csr_csc(n, src, src + 1))
+    b = np.array([0, 50, 100])
+    parts = ipr.split_partitions(n, n - 1, b, d["csc_off"], d["csc_idx"], d["csr_off"], d["csr_idx"])
+    for p in parts:
+        p.csr_offsets = p.csr_indices = None
+    descs = (ipr.ipregel.GraphDesc * 2)(*[p.desc() for p in parts])
+    h = ctypes.c_void_p()
+    st = ipr.load().ipregel_graph_create_partitioned(descs, 2, None, ctypes.byref(h))
+    assert st == ipr.ERR_UNSUPPORTED
