@@ -288,8 +288,14 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * Flags: IPR_BROADCAST = send *message to every out-neighbour (with symmetric = 1
  * to every in- and out-neighbour); IPR_STAY_ACTIVE = do not vote to halt.
  * ipr_ctx (read-only): id (ORIGINAL vertex id under a relabelled layout), num_vertices,
- * superstep, out_degree, in_degree, params[0..7] (the run's program parameters, 0 if unset).
+ * superstep, out_degree, in_degree, params[0..7] (the run's program parameters, 0 if unset),
+ * aggregate (the aggregator after the previous superstep; its identity before any fold).
  * Helpers: ipr_sat_add(a, b) (u32, saturating at IPR_INF_U32 = 0xFFFFFFFF).
+ * Services (Fig. 2): ipr_send(c, dest, message) -- IP_send_message: a point-to-point message to
+ * the ORIGINAL vertex id dest (ignored outside [0, N)), combined into dest's mailbox with the
+ * program's combiner and delivered in the next superstep, where dest computes (it counts in
+ * `messages`; one GPU: whole graph or loopback partitions; not across ranks: UNSUPPORTED);
+ * ipr_aggregate(c, x) -- fold the f64 x into the run's aggregator (desc.aggregator).
  * The run ends when a superstep has no broadcast and no active vertex.
  * Selection (R28): push supersteps run compute on recipients and active vertices
  * only; pull supersteps run it on every vertex, the non-recipients getting the identity, so a
@@ -298,6 +304,9 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * order in pull mode and by atomics in push mode (SUM f64 in push is order-nondeterministic).
  */
 typedef enum { IPREGEL_VALUE_U32 = 0, IPREGEL_VALUE_F64 = 1 } ipregel_value_type;
+typedef enum {
+    IPREGEL_AGG_NONE = 0, IPREGEL_AGG_SUM = 1, IPREGEL_AGG_MIN = 2, IPREGEL_AGG_MAX = 3
+} ipregel_aggregator;
 
 typedef struct {
     const char* source;   /* NUL-terminated CUDA C++ source (copied; the caller keeps ownership) */
@@ -305,6 +314,10 @@ typedef struct {
     int32_t combiner;     /* ipregel_combiner                                                   */
     int32_t symmetric;    /* 1: messages travel along every edge in both directions (Hash-Min's
                              neighbourhood; the graph's CSR row U CSC row), 0: out-edges only   */
+    int32_t aggregator;   /* ipregel_aggregator: NONE (0), or SUM / MIN / MAX folding the f64
+                             values vertices pass to ipr_aggregate in a superstep; every vertex
+                             reads the result as ipr_ctx.aggregate in the next one (Pregel
+                             aggregators; SUM's rounding order is not deterministic)           */
     int32_t reserved;     /* must be 0                                                          */
 } ipregel_program_desc;
 

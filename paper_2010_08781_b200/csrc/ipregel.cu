@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -208,6 +209,11 @@ struct AppState {
     uint8_t* pv_flags = nullptr;               // owned: bit 0 broadcast, bit 1 active
     uint32_t* pv_recv = nullptr;               // owned recipient bitmap (push)
     double* pv_params = nullptr;               // program parameters [8]
+    void* pv_p2p[2] = {nullptr, nullptr};      // point-to-point mailboxes [rows] (by parity)
+    uint32_t* pv_p2p_recv[2] = {nullptr, nullptr};
+    ProgShared* pv_shared = nullptr;           // device copy of the run's ProgShared
+    unsigned long long* pv_sends = nullptr;    // point-to-point sends of the superstep
+    double* pv_agg = nullptr;                  // aggregator fold of the superstep
     DeviceBuffers mem;
 };
 
@@ -258,6 +264,7 @@ struct ipregel_graph {
     int last_exchange = 0;         // 0 none, 1 collective, 2 fused
     int64_t last_rowlist_edges = 0;
     int64_t w_min = -1;            // smallest edge weight (SSSP absorption bound), lazily
+    const int32_t* inv_ids = nullptr;   // original -> internal id (user programs' ipr_send)
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
@@ -483,6 +490,13 @@ void ensure_state(ipregel_graph* g, int app) {
             S.pv_flags = S.mem.alloc<uint8_t>(p.rows, s, true);
             S.pv_recv = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.pv_params = S.mem.alloc<double>(kProgParams, s, true);
+            for (int w = 0; w < 2; ++w) {
+                S.pv_p2p[w] = S.mem.alloc<uint64_t>(p.rows, s);
+                S.pv_p2p_recv[w] = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
+            }
+            S.pv_shared = S.mem.alloc<ProgShared>(1, s, true);
+            S.pv_sends = S.mem.alloc<unsigned long long>(1, s, true);
+            S.pv_agg = S.mem.alloc<double>(1, s, true);
             S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.f_id = S.mem.alloc<int32_t>(p.rows, s);
             S.f_val = S.mem.alloc<uint32_t>(p.rows, s);
@@ -1496,6 +1510,8 @@ struct ipregel_program {
     int value_type = 0;   // ipregel_value_type
     int combiner = 0;     // ipregel_combiner
     int sym = 0;
+    int agg_op = -1;      // aggregator (ipregel_combiner over f64), -1 none
+    bool sends = false;   // the source calls ipr_send (point-to-point messages)
     std::vector<char> cubin;
     std::string log;
     std::string lowered[PK_COUNT];
@@ -1569,11 +1585,20 @@ std::string program_tu(const ipregel_program_desc& d) {
     s += "#define IPR_BROADCAST 1u\n#define IPR_STAY_ACTIVE 2u\n#define IPR_INF_U32 0xFFFFFFFFu\n";
     s += "__device__ __forceinline__ unsigned ipr_sat_add(unsigned a, unsigned b) "
          "{ return ipr::sat_add(a, b); }\n";
+    s += "__device__ __forceinline__ void ipr_send(const ipr_ctx& c, long long dest, "
+         "ipr_value_t m) { ipr::prog_send<ipr_value_t, " + std::to_string(d.combiner) +
+         ">(c, dest, m); }\n";
+    s += "__device__ __forceinline__ void ipr_aggregate(const ipr_ctx& c, double x) "
+         "{ ipr::prog_aggregate(c, x); }\n";
     s += "#line 1 \"user_program.cu\"\n";
     s += d.source;
     s += "\n#line 1 \"ipregel_program_adapter\"\n";
     s += "struct UserProgram {\n  typedef ipr_value_t V;\n";
     s += "  static constexpr int kCombiner = " + std::to_string(d.combiner) + ";\n";
+    s += std::string("  static constexpr bool kSends = ") +
+         (strstr(d.source, "ipr_send") ? "true" : "false") + ";\n";
+    s += std::string("  static constexpr bool kAggregates = ") +
+         (d.aggregator != IPREGEL_AGG_NONE ? "true" : "false") + ";\n";
     s += "  static __device__ __forceinline__ unsigned init(const ipr::ProgCtx& c, V* v, V* m) "
          "{ return ipr_init(c, v, m); }\n";
     s += "  static __device__ __forceinline__ unsigned compute(const ipr::ProgCtx& c, V* v, V mb, "
@@ -1636,6 +1661,31 @@ void launch_jit(cudaKernel_t k, unsigned grid, unsigned block, void** args, cuda
     LAUNCH_CHECK();
 }
 
+// Bit pattern of the program combiner's identity in an 8-byte slot (u32 in the low half).
+uint64_t prog_identity_bits(const ipregel_program* pr) {
+    if (pr->value_type == IPREGEL_VALUE_F64) {
+        const double id = pr->combiner == IPREGEL_COMBINE_SUM ? 0.0
+                        : (pr->combiner == IPREGEL_COMBINE_MIN ? INFINITY : -INFINITY);
+        uint64_t b;
+        memcpy(&b, &id, 8);
+        return b;
+    }
+    return pr->combiner == IPREGEL_COMBINE_MIN ? 0xFFFFFFFFull : 0ull;
+}
+
+// original -> internal id (the inverse of vertex_ids), built once per graph; NULL without a
+// relabelled layout.
+const int32_t* inverse_ids(ipregel_graph* g) {
+    if (!g->vertex_ids) return nullptr;
+    if (!g->inv_ids) {
+        int32_t* inv = g->graph_mem.alloc<int32_t>(g->n, g->stream);
+        k_invert_ids<<<grid_for(g->n, 256), 256, 0, g->stream>>>(g->vertex_ids, g->n, inv);
+        LAUNCH_CHECK();
+        g->inv_ids = inv;
+    }
+    return g->inv_ids;
+}
+
 // One pull pass of a program over one adjacency (the ProgPull<P, pass> instantiation).
 template <class V>
 void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, ProgArgs<V>& a,
@@ -1673,6 +1723,84 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         for (auto& p : g->parts) ensure_push_view(g, p);
     double hp[kProgParams] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int i = 0; i < nparams; ++i) hp[i] = params[i];
+    // point-to-point messages and the aggregator (Fig. 2's IP_send_message; Pregel aggregators)
+    const int np = (int)g->parts.size();
+    if (pr->sends && multi_rank(g) && g->comm->world > 1)
+        fail(IPREGEL_ERR_UNSUPPORTED, "ipr_send across ranks is not supported (loopback partitions are)");
+    if (pr->sends && np > kProgMaxParts)
+        fail(IPREGEL_ERR_UNSUPPORTED, "ipr_send supports at most %d partitions", kProgMaxParts);
+    const uint64_t ident = prog_identity_bits(pr);
+    const double agg_id = pr->agg_op == 0 ? 0.0 : (pr->agg_op == 1 ? INFINITY : -INFINITY);
+    double agg_prev = agg_id;
+    if (pr->sends || pr->agg_op >= 0) {
+        const int32_t* inv = pr->sends ? inverse_ids(g) : nullptr;
+        for (int a = 0; a < np; ++a) {
+            Partition& p = g->parts[a];
+            AppState& S = p.st[app];
+            ProgShared h{};
+            h.nparts = pr->sends ? np : 0;
+            h.agg_op = pr->agg_op;
+            for (int b = 0; b < np && pr->sends; ++b) {
+                h.bounds[b] = g->parts[b].vb;
+                h.bounds[b + 1] = g->parts[b].ve;
+                for (int w = 0; w < 2; ++w) {
+                    h.p2p[w][b] = g->parts[b].st[app].pv_p2p[w];
+                    h.p2p_recv[w][b] = g->parts[b].st[app].pv_p2p_recv[w];
+                }
+            }
+            h.inv_ids = inv;
+            h.sends = S.pv_sends;
+            h.agg = S.pv_agg;
+            CU(cudaMemcpyAsync(S.pv_shared, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+            if (pr->sends && p.rows) {
+                for (int w = 0; w < 2; ++w) {
+                    k_fill_u64<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                        static_cast<uint64_t*>(S.pv_p2p[w]), p.rows, ident, (int)sizeof(V));
+                    LAUNCH_CHECK();
+                    CU(cudaMemsetAsync(S.pv_p2p_recv[w], 0, words_of(p.rows) * 4, s));
+                }
+            }
+        }
+        CU(cudaStreamSynchronize(s));   // `h` lives on the host stack
+    }
+    // per superstep: reset the send counters and aggregators; afterwards fold them
+    auto reset_extras = [&]() {
+        if (!pr->sends && pr->agg_op < 0) return;
+        for (auto& p : g->parts) {
+            AppState& S = p.st[app];
+            CU(cudaMemsetAsync(S.pv_sends, 0, 8, s));
+            CU(cudaMemcpyAsync(S.pv_agg, &agg_id, 8, cudaMemcpyHostToDevice, s));
+        }
+    };
+    auto fold_extras = [&](uint64_t* sends_out, double* agg_out) {
+        *sends_out = 0;
+        *agg_out = agg_id;
+        if (!pr->sends && pr->agg_op < 0) return;
+        std::vector<unsigned long long> hs(np);
+        std::vector<double> ha(np);
+        for (int a = 0; a < np; ++a) {
+            AppState& S = g->parts[a].st[app];
+            CU(cudaMemcpyAsync(&hs[a], S.pv_sends, 8, cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(&ha[a], S.pv_agg, 8, cudaMemcpyDeviceToHost, s));
+        }
+        CU(cudaStreamSynchronize(s));
+        double agg = agg_id;
+        for (int a = 0; a < np; ++a) {
+            *sends_out += hs[a];
+            agg = pr->agg_op == 0 ? agg + ha[a] : (pr->agg_op == 1 ? std::min(agg, ha[a])
+                                                                    : std::max(agg, ha[a]));
+        }
+        if (multi_rank(g) && pr->agg_op >= 0) {
+            Partition& p = g->parts[0];
+            double* d = reinterpret_cast<double*>(p.dscratch + 62);
+            CU(cudaMemcpyAsync(d, &agg, 8, cudaMemcpyHostToDevice, s));
+            const ncclRedOp_t op = pr->agg_op == 0 ? ncclSum : (pr->agg_op == 1 ? ncclMin : ncclMax);
+            NC(ncclAllReduce(d, d + 1, 1, ncclFloat64, op, g->comm->nccl, s));
+            CU(cudaMemcpyAsync(&agg, d + 1, 8, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+        }
+        *agg_out = agg;
+    };
     auto args_for = [&](Partition& p, uint32_t step, int cur) {
         AppState& S = p.st[app];
         ProgArgs<V> a;
@@ -1687,6 +1815,11 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         a.in_off = p.csc_off;
         a.ids = g->vertex_ids;
         a.params = S.pv_params;
+        a.shared = (pr->sends || pr->agg_op >= 0) ? S.pv_shared : nullptr;
+        a.p2p_in = pr->sends ? S.pv_p2p[(step & 1u) ^ 1u] : nullptr;
+        a.p2p_in_recv = pr->sends ? S.pv_p2p_recv[(step & 1u) ^ 1u] : nullptr;
+        a.aggregate = agg_prev;
+        a.agg_op = pr->agg_op;
         a.vbase = p.vb;
         a.rows = p.rows;
         a.n = n;
@@ -1709,6 +1842,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
         CU(cudaMemsetAsync(S.pv_recv, 0, words_of(p.rows) * 4, s));
     }
+    reset_extras();
     T0.kbegin();
     for (auto& p : g->parts) {
         ProgArgs<V> a = args_for(p, 0, 1);   // out_next = buffer 0
@@ -1720,8 +1854,10 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
     exchange(0);
     unsigned long long c[4];
     reduce_counters(g, false, c, 4);
+    uint64_t sends = 0;
+    fold_extras(&sends, &agg_prev);
     T0.end();
-    uint64_t changed = c[0], messages = c[1], active = c[3];
+    uint64_t changed = c[0], messages = c[1] + sends, active = c[3];
     g->steps[0].mode = 0;
     g->steps[0].changed = changed;
     g->steps[0].messages = messages;
@@ -1740,6 +1876,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         T.begin();
         const uint64_t frontier_len = changed;
         for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
+        reset_extras();
         if (mode == 2) {
             // frontier = the broadcasters of superstep s-1 (flag bytes -> bitmap -> ids)
             for (auto& p : g->parts) {
@@ -1793,6 +1930,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         }
         exchange(1 - cur);
         reduce_counters(g, false, c, 4);
+        fold_extras(&sends, &agg_prev);
         T.end();
         StepRecord& R = g->steps.back();
         R.mode = (uint8_t)mode;
@@ -1803,7 +1941,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             : (uint64_t)(8 + sizeof(V) + (g->parts[0].csc_w ? 4 : 0)) * messages +
                   (uint64_t)(16 + 3 * sizeof(V)) * (uint64_t)n;
         changed = c[0];
-        messages = c[1];
+        messages = c[1] + sends;
         active = c[3];
         R.changed = changed;
         R.messages = messages;
@@ -2147,10 +2285,14 @@ ipregel_status ipregel_program_create(const ipregel_program_desc* desc, ipregel_
     if (desc->symmetric != 0 && desc->symmetric != 1)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "symmetric must be 0 or 1");
     if (desc->reserved != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "reserved must be 0");
+    if (desc->aggregator < IPREGEL_AGG_NONE || desc->aggregator > IPREGEL_AGG_MAX)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown aggregator %d", desc->aggregator);
     ipregel_program* pr = new ipregel_program;
     pr->value_type = desc->value_type;
     pr->combiner = desc->combiner;
     pr->sym = desc->symmetric;
+    pr->agg_op = desc->aggregator - 1;   // -1 none, else SUM / MIN / MAX
+    pr->sends = strstr(desc->source, "ipr_send") != nullptr;
     try {
         compile_program(pr, *desc);
     } catch (...) {

@@ -36,6 +36,23 @@ constexpr unsigned kProgBroadcast = 1u;
 constexpr unsigned kProgStayActive = 2u;
 constexpr int kProgParams = 8;
 
+constexpr int kProgMaxParts = 8;
+
+// Point-to-point messages (Fig. 2's IP_send_message) and the aggregator of a run, one device copy
+// per partition.  Messages sent in superstep s go to buffer s & 1 of the OWNER partition of the
+// destination (atomic combine into its single-slot mailbox + a recipient bit) and are folded
+// into the recipient's mailbox in superstep s + 1.
+struct ProgShared {
+    int32_t nparts;
+    int32_t agg_op;                          // -1 none, else SUM / MIN / MAX (ipregel_combiner)
+    int64_t bounds[kProgMaxParts + 1];       // partition p owns [bounds[p], bounds[p + 1])
+    void* p2p[2][kProgMaxParts];             // mailboxes [rows_p] (8-byte slots)
+    uint32_t* p2p_recv[2][kProgMaxParts];    // recipient bitmaps
+    const int32_t* inv_ids;                  // original -> internal id, or NULL
+    unsigned long long* sends;               // this partition's point-to-point sends
+    double* agg;                             // this partition's aggregator (superstep's fold)
+};
+
 // What compute() sees of its vertex (Fig. 2's services).
 struct ProgCtx {
     int64_t id;            // vertex id (the ORIGINAL id under a relabelled layout)
@@ -43,8 +60,12 @@ struct ProgCtx {
     uint32_t superstep;
     int32_t out_degree;    // out-neighbours
     int32_t in_degree;     // in-neighbours
-    int32_t reserved;
+    int32_t wpar;          // point-to-point buffer written this superstep (superstep & 1)
     const double* params;  // the run's program parameters [8]
+    double aggregate;      // the aggregator's value after the previous superstep
+    const ProgShared* shared;
+    mutable double agg_acc;   // this vertex's ipr_aggregate fold (folded into the thread's)
+    mutable uint32_t agg_n;
 };
 
 // Kernel parameter block; its layout does not depend on the program.
@@ -61,6 +82,11 @@ struct ProgArgs {
     const int32_t* in_off;
     const int32_t* ids;    // internal -> original id, or NULL
     const double* params;  // device [kProgParams]
+    const ProgShared* shared;   // device, this partition's
+    void* p2p_in;          // this partition's point-to-point mailboxes read this superstep
+    uint32_t* p2p_in_recv; //   and their recipient bitmap (NULL: the program never sends)
+    double aggregate;      // the aggregator after the previous superstep
+    int32_t agg_op;        // -1 none
     int64_t vbase, rows, n;
     uint32_t superstep;
     int32_t sym;
@@ -120,9 +146,62 @@ __device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
     x.superstep = A.superstep;
     x.out_degree = A.out_off[row + 1] - A.out_off[row];
     x.in_degree = A.in_off[row + 1] - A.in_off[row];
-    x.reserved = 0;
+    x.wpar = (int32_t)(A.superstep & 1u);
     x.params = A.params;
+    x.aggregate = A.aggregate;
+    x.shared = A.shared;
+    x.agg_acc = 0.0;
+    x.agg_n = 0u;
     return x;
+}
+
+// ---- Fig. 2's IP_send_message and a Pregel aggregator ------------------------------------------
+// Point-to-point send of `m` to ORIGINAL vertex id `dest` (ignored if outside [0, N)).
+template <class V, int kComb>
+__device__ __forceinline__ void prog_send(const ProgCtx& c, long long dest, V m) {
+    const ProgShared* S = c.shared;
+    if (!S || dest < 0 || dest >= c.num_vertices) return;
+    const int64_t v = S->inv_ids ? (int64_t)S->inv_ids[dest] : (int64_t)dest;
+    int p = 0;
+    while (p + 1 < S->nparts && v >= S->bounds[p + 1]) ++p;
+    const int64_t lv = v - S->bounds[p];
+    ProgComb<V, kComb>::atomic(static_cast<V*>(S->p2p[c.wpar][p]) + lv, m);
+    uint32_t* rb = S->p2p_recv[c.wpar][p];
+    const uint32_t bit = 1u << (lv & 31);
+    if (!(rb[lv >> 5] & bit)) atomicOr(rb + (lv >> 5), bit);
+    atomicAdd(S->sends, 1ull);
+}
+
+__device__ __forceinline__ double agg_combine(int op, double a, double b) {
+    return op == 0 ? __dadd_rn(a, b) : (op == 1 ? (b < a ? b : a) : (b > a ? b : a));
+}
+
+// Fold x into this superstep's aggregator (visible to every vertex as ctx.aggregate in the next
+// superstep).
+__device__ __forceinline__ void prog_aggregate(const ProgCtx& c, double x) {
+    if (!c.shared || c.shared->agg_op < 0) return;
+    c.agg_acc = c.agg_n ? agg_combine(c.shared->agg_op, c.agg_acc, x) : x;
+    c.agg_n = 1u;
+}
+
+__device__ __forceinline__ void agg_atomic(int op, double* p, double v) {
+    if (op == 0) atomicAdd(p, v);
+    else atomic_f64_select(p, v, op == 1);
+}
+
+// End of a kernel: warp-fold the threads' aggregator values, one atomic per warp.
+__device__ __forceinline__ void flush_prog_aggregate(const LaneCounters& c, int op, double* dst) {
+    if (op < 0 || !dst) return;
+    const unsigned any = __ballot_sync(kFull, c.agg_n != 0u);
+    if (!any) return;
+    double x = c.agg;
+    const bool have = c.agg_n != 0u;
+    const double id = op == 0 ? 0.0 : (op == 1 ? __longlong_as_double(0x7FF0000000000000LL)
+                                               : __longlong_as_double((long long)0xFFF0000000000000ULL));
+    if (!have) x = id;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x = agg_combine(op, x, __shfl_xor_sync(kFull, x, d));
+    if ((threadIdx.x & 31) == 0) agg_atomic(op, dst, x);
 }
 
 // Record what one vertex did: outbox slot (identity unless it broadcast), bitmap, counters.
@@ -145,16 +224,41 @@ __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int6
     c.aux += act ? 1ull : 0ull;
 }
 
+// The point-to-point messages received for `row` (sent in the previous superstep), folded into
+// its mailbox; the slot is reset for the next use of this buffer.
+template <class P>
+__device__ __forceinline__ typename P::V prog_p2p_in(const ProgArgs<typename P::V>& A,
+                                                     int64_t row, typename P::V m) {
+    using V = typename P::V;
+    using C = ProgComb<V, P::kCombiner>;
+    if constexpr (!P::kSends) return m;
+    if (!A.p2p_in_recv) return m;
+    const uint32_t bit = 1u << (row & 31);
+    if (!(A.p2p_in_recv[row >> 5] & bit)) return m;
+    V* slot = static_cast<V*>(A.p2p_in) + row;
+    m = C::combine(m, *slot);
+    *slot = C::identity();
+    atomicAnd(A.p2p_in_recv + (row >> 5), ~bit);
+    return m;
+}
+
 template <class P>
 __device__ __forceinline__ void prog_vertex(const ProgArgs<typename P::V>& A, int64_t row,
                                             typename P::V mailbox, LaneCounters& c) {
     using V = typename P::V;
     using C = ProgComb<V, P::kCombiner>;
     const ProgCtx x = prog_ctx(A, row);
+    mailbox = prog_p2p_in<P>(A, row, mailbox);
     V val = A.value[row];
     V msg = C::identity();
     const unsigned f = P::compute(x, &val, mailbox, &msg);
     A.value[row] = val;
+    if constexpr (P::kAggregates) {
+        if (x.agg_n) {
+            c.agg = c.agg_n ? agg_combine(A.agg_op, c.agg, x.agg_acc) : x.agg_acc;
+            c.agg_n = 1u;
+        }
+    }
     prog_emit<P>(A, row, x, f, msg, c);
 }
 
@@ -176,9 +280,16 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
         const unsigned f = P::init(x, &val, &msg);
         A.value[row] = val;
         A.mbox[row] = C::identity();
+        if constexpr (P::kAggregates) {
+            if (x.agg_n) {
+                c.agg = x.agg_acc;
+                c.agg_n = 1u;
+            }
+        }
         prog_emit<P>(A, row, x, f, msg, c);
     }
     flush_counters(c, s_cnt, counters);
+    if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }
 
 // ---- pull: the op of pull.cuh's range kernels ------------------------------------------------
@@ -191,6 +302,14 @@ struct ProgPull : ProgArgs<typename P::V> {
     using C = ProgComb<T, P::kCombiner>;
     static constexpr bool kWeighted = true;
     static constexpr bool kAbsorbing = false;
+    static constexpr bool kAggregates = P::kAggregates;
+    __device__ void flush_aggregate(const LaneCounters& c) const {
+        flush_prog_aggregate(c, this->agg_op, this->shared ? this->shared->agg : nullptr);
+    }
+    __device__ void flush_aggregate_lane(const LaneCounters& c) const {   // one thread
+        if (this->agg_op >= 0 && c.agg_n && this->shared)
+            agg_atomic(this->agg_op, this->shared->agg, c.agg);
+    }
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }
@@ -249,6 +368,8 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     bool got = false;
     if (row < A.rows) {
         got = (A.recv[row >> 5] >> (row & 31)) & 1u;
+        if constexpr (P::kSends)
+            if (A.p2p_in_recv) got = got || ((A.p2p_in_recv[row >> 5] >> (row & 31)) & 1u);
         if (got || (A.flags[row] & 2u)) {
             const V m = A.mbox[row];
             A.mbox[row] = C::identity();
@@ -262,6 +383,7 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     __syncwarp();
     if (row < A.rows && (row & 31) == 0) A.recv[row >> 5] = 0u;
     flush_counters(c, s_cnt, counters);
+    if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }
 
 }  // namespace ipr

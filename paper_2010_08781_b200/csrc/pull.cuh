@@ -52,6 +52,8 @@ struct LaneCounters {
     uint32_t aux;
     uint32_t messages;
     unsigned long long dmax;
+    double agg;        // user programs: this thread's fold of ipr_aggregate values
+    uint32_t agg_n;    //   (agg_n = 0: nothing folded)
 };
 
 // Range plan for one adjacency of one partition.
@@ -139,11 +141,16 @@ struct PeerSlots {
     }
 };
 
+// Ops that fold a program aggregator flush it at the end of the kernel (kAggregates).
+struct NoAggregate {
+    static constexpr bool kAggregates = false;
+};
+
 // ---- vertex programs: gather = outbox value of the sender, message = value on the edge,
 // finish = recipient compute --------------------------------------------------------------------
 // PageRank, Fig. 8: the message of u is contrib[u] = r_u / outdeg(u); recipient compute is
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
-struct PageRankPull : SumF64, NotAbsorbing {
+struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
@@ -179,7 +186,7 @@ struct PageRankPull : SumF64, NotAbsorbing {
 // PageRank with the update split out of the range kernel (IPREGEL_PR_SPLIT=1): the range kernel
 // only stores each row's combined sum into its next-outbox slot, and k_pr_finish applies Fig. 8's
 // update row-parallel (same operations, same result).
-struct PageRankSum : SumF64, NotAbsorbing {
+struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
     const double* __restrict__ contrib_cur;
     double* __restrict__ sum_out;             // = contrib_next of the superstep (global ids)
@@ -192,7 +199,7 @@ struct PageRankSum : SumF64, NotAbsorbing {
 };
 
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
-struct CCPullIn : MinU32 {
+struct CCPullIn : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
     static constexpr bool kAbsorbing = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
@@ -212,7 +219,7 @@ struct CCPullIn : MinU32 {
 
 // Hash-Min CC, second half: min over the CSR row (the symmetrised graph's reverse edges), then
 // "if value < old: broadcast" -> changed / messages counters (degree in the symmetrised graph).
-struct CCPullOut : MinU32 {
+struct CCPullOut : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
     static constexpr bool kAbsorbing = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
@@ -250,7 +257,7 @@ struct CCPullOut : MinU32 {
 // smallest edge weight; a row already at or below thr -- or whose partial reaches thr -- cannot
 // change, and its remaining gathers are skipped.  finish() reports m for the next superstep (as
 // INF - dist in the max-reduced dmax counter).
-struct SSSPPull : MinU32 {
+struct SSSPPull : MinU32, NoAggregate {
     static constexpr bool kWeighted = true;
     static constexpr bool kAbsorbing = true;
     const uint32_t* __restrict__ cur;
@@ -556,9 +563,10 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_r
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    LaneCounters cnt{0u, 0u, 0u, 0ull};
+    LaneCounters cnt{0u, 0u, 0u, 0ull, 0.0, 0u};
     if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
     flush_counters(cnt, s_cnt, A.counters);
+    if constexpr (Op::kAggregates) op.flush_aggregate(cnt);
 }
 
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.
@@ -595,8 +603,9 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     }
     if (lane == 0) {
         acc = Op::combine(acc, head[G.z]);
-        LaneCounters c{0u, 0u, 0u, 0ull};
+        LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
         op.finish(G.x, acc, c);
+        if constexpr (Op::kAggregates) op.flush_aggregate_lane(c);
         if (counters && (c.changed | c.messages | c.dmax | c.aux)) {
             atomicAdd(&counters->changed, c.changed);
             atomicAdd(&counters->messages, c.messages);

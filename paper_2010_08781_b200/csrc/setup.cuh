@@ -64,6 +64,20 @@ __global__ void k_min_u32(const uint32_t* __restrict__ a, int64_t n, unsigned* _
     if ((threadIdx.x & 31) == 0) atomicMin(out, m);
 }
 
+// Fill 8-byte slots with a pattern (vsz 4: the low 32 bits into a u32 array of the same count).
+__global__ void k_fill_u64(uint64_t* __restrict__ a, int64_t n, uint64_t pattern, int vsz) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (vsz == 8) a[i] = pattern;
+    else reinterpret_cast<uint32_t*>(a)[i] = (uint32_t)pattern;
+}
+
+// inv[ids[v]] = v
+__global__ void k_invert_ids(const int32_t* __restrict__ ids, int64_t n, int32_t* __restrict__ inv) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) inv[ids[i]] = (int32_t)i;
+}
+
 // Hash-Min CC, Fig. 9: value = id, the ORIGINAL id under a relabelled layout (every replica
 // initialises all N locally -- no exchange).
 __global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n, const int32_t* __restrict__ ids) {

@@ -83,7 +83,7 @@ class Stats(ctypes.Structure):
 class ProgramDesc(ctypes.Structure):
     _fields_ = [("source", ctypes.c_char_p), ("value_type", ctypes.c_int32),
                 ("combiner", ctypes.c_int32), ("symmetric", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("aggregator", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 # every symbol include/ipregel.h declares (tests check the library exports all of them)
@@ -232,13 +232,14 @@ class Program:
     ipr_compute and ipr_edge (include/ipregel.h), compiled by NVRTC for sm_100a."""
 
     def __init__(self, source: str, value_type: str = "u32", combiner: str = "min",
-                 symmetric: bool = False):
+                 symmetric: bool = False, aggregator: str | None = None):
         d = ProgramDesc()
         self._src = source.encode()
         d.source = self._src
         d.value_type = VALUE_TYPES[value_type]
         d.combiner = COMBINERS[combiner]
         d.symmetric = 1 if symmetric else 0
+        d.aggregator = 0 if aggregator is None else 1 + COMBINERS[aggregator]
         d.reserved = 0
         h = ctypes.c_void_p()
         _check(load().ipregel_program_create(ctypes.byref(d), ctypes.byref(h)),

@@ -158,6 +158,62 @@ __device__ unsigned ipr_compute(const ipr_ctx&, double* value, double mailbox, d
 __device__ double ipr_edge(double message, unsigned weight) { return message + (double)weight; }
 """
 
+# PageRank to convergence with a Pregel aggregator (PAPER.md:322): every vertex folds its rank
+# change into a MAX aggregator; in the next superstep, if the largest change was <= params[1],
+# every vertex votes to halt keeping its rank (one superstep after the built-in master halt,
+# same values).  params[0] = k, the superstep cap.
+PAGERANK_CONVERGE = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, double* value, double* message) {
+    *value = 1.0 / (double)c.num_vertices;
+    if ((unsigned)c.params[0] == 0) return 0;
+    if (c.out_degree == 0) return IPR_STAY_ACTIVE;
+    *message = *value / (double)c.out_degree;
+    return IPR_BROADCAST | IPR_STAY_ACTIVE;
+}
+__device__ unsigned ipr_compute(const ipr_ctx& c, double* value, double mailbox, double* message) {
+    const unsigned k = (unsigned)c.params[0];
+    if (c.superstep >= 2 && c.aggregate <= c.params[1]) return 0;   // converged: halt, keep
+    const double old = *value;
+    *value = 0.15 / (double)c.num_vertices + 0.85 * mailbox;
+    ipr_aggregate(c, fabs(*value - old));
+    if (c.superstep >= k) return 0;
+    if (c.out_degree == 0) return IPR_STAY_ACTIVE;
+    *message = *value / (double)c.out_degree;
+    return IPR_BROADCAST | IPR_STAY_ACTIVE;
+}
+__device__ double ipr_edge(double message, unsigned) { return message; }
+"""
+
+# Point-to-point messages (Fig. 2's IP_send_message): every vertex v > 0 sends v to its parent
+# (v - 1) / 2 in the implicit binary heap over the ids; a vertex's value becomes the sum of its
+# children's ids.
+HEAP_CHILDREN_SUM = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned*) {
+    *value = 0;
+    if (c.id > 0) ipr_send(c, (c.id - 1) / 2, (unsigned)c.id);
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbox, unsigned*) {
+    *value = mailbox;
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned message, unsigned) { return message; }
+"""
+
+# Aggregators: superstep 0 folds 1 per vertex (SUM) -> every vertex reads N in superstep 1.
+COUNT_VERTICES = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, double* value, double*) {
+    *value = 0.0;
+    ipr_aggregate(c, 1.0);
+    return IPR_STAY_ACTIVE;
+}
+__device__ unsigned ipr_compute(const ipr_ctx& c, double* value, double, double*) {
+    *value = c.aggregate;
+    return 0;
+}
+__device__ double ipr_edge(double message, unsigned) { return message; }
+"""
+
 CATALOG = {
     "pagerank": (PAGERANK, "f64", "sum", False),
     "hashmin_cc": (HASHMIN_CC, "u32", "min", True),
@@ -167,9 +223,13 @@ CATALOG = {
     "max_label": (MAX_LABEL, "u32", "max", True),
     "in_degree": (IN_DEGREE, "u32", "sum", False),
     "sssp_f64": (SSSP_F64, "f64", "min", False),
+    "pagerank_converge": (PAGERANK_CONVERGE, "f64", "sum", False, "max"),
+    "heap_children_sum": (HEAP_CHILDREN_SUM, "u32", "sum", False),
+    "count_vertices": (COUNT_VERTICES, "f64", "sum", False, "sum"),
 }
 
 
 def compile(name: str) -> Program:  # noqa: A001 - mirrors the catalog verb
-    src, vt, comb, sym = CATALOG[name]
-    return Program(src, value_type=vt, combiner=comb, symmetric=sym)
+    src, vt, comb, sym, *agg = CATALOG[name]
+    return Program(src, value_type=vt, combiner=comb, symmetric=sym,
+                   aggregator=agg[0] if agg else None)

@@ -174,3 +174,71 @@ def test_program_cc_at_baseline_config1():
     assert s["supersteps"] == o["supersteps"]
     np.testing.assert_array_equal(s["messages"], o["messages"])
     G.close()
+
+
+# ------------------------------------------------------------------ Fig. 2 services
+
+@pytest.mark.parametrize("mode,parts", [("pull", 1), ("push", 1), ("auto", 3), ("push", 4)])
+def test_point_to_point_send(mode, parts):
+    """IP_send_message: every vertex v > 0 sends v to (v - 1) / 2; values = sum of children."""
+    n, src, dst, _ = graph(9, n=3000)
+    G = make_graph(csr_csc(n, src, dst), partitions=parts, weighted=False)
+    G.run_program(prog("heap_children_sum"), mode=mode)
+    v = G.values(host=True).astype(np.int64)
+    ids = np.arange(n)
+    want = np.where(2 * ids + 1 < n, 2 * ids + 1, 0) + np.where(2 * ids + 2 < n, 2 * ids + 2, 0)
+    np.testing.assert_array_equal(v, want)
+    s = G.stats()
+    assert s["supersteps"] == 2 and s["messages"][0] == n - 1
+    G.close()
+
+
+def test_point_to_point_send_original_ids_under_relabelling():
+    import torch
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    rng = np.random.default_rng(3)
+    n = 1000
+    src, dst, _ = checkers.random_graph(rng, n, 4000)
+    perm = rng.permutation(n).astype(np.int64)
+    g = csr_csc(n, perm[src], perm[dst])
+    inv = np.empty(n, np.int32)
+    inv[perm] = np.arange(n, dtype=np.int32)
+    d = to_device(g)
+    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"],
+                                     d["csr_idx"], vertex_ids=torch.from_numpy(inv).cuda()))
+    G.run_program(prog("heap_children_sum"), mode="push")
+    ids = np.arange(n)
+    want = np.where(2 * ids + 1 < n, 2 * ids + 1, 0) + np.where(2 * ids + 2 < n, 2 * ids + 2, 0)
+    np.testing.assert_array_equal(G.values(host=True).astype(np.int64), want)
+    G.close()
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_aggregator_counts_vertices(parts):
+    n, src, dst, _ = graph(5, n=2222)
+    G = make_graph(csr_csc(n, src, dst), partitions=parts, weighted=False)
+    G.run_program(prog("count_vertices"))
+    np.testing.assert_array_equal(G.values(host=True), np.full(n, float(n)))
+    G.close()
+
+
+@pytest.mark.parametrize("mode,parts", [("pull", 1), ("push", 1), ("pull", 3)])
+def test_pagerank_converge_program_equals_oracle(mode, parts):
+    """PageRank to convergence written with a MAX aggregator halts one superstep after the
+    oracle's master halt, with the same values (reading R27)."""
+    rng = np.random.default_rng(6200)
+    n = 2000
+    src, dst, _ = checkers.random_graph(rng, n, 12000)
+    full = oracle.pagerank(n, src, dst, k=60)
+    dl = full["delta"]
+    cand = [t for t in range(2, 60) if 0 < dl[t] < 0.5 * dl[t - 1] and dl[t] > 1e-13]
+    t = cand[len(cand) // 2]
+    tol = float(np.sqrt(dl[t] * dl[t - 1]))
+    o = oracle.pagerank(n, src, dst, k=60, tol=tol)
+    G = make_graph(csr_csc(n, src, dst), partitions=parts, weighted=False)
+    G.run_program(prog("pagerank_converge"), params=[60, tol], mode=mode)
+    v = G.values(host=True)
+    assert np.abs(v - o["values"]).max() <= PR_ABS
+    assert G.stats()["supersteps"] == o["supersteps"] + 1
+    G.close()
