@@ -257,8 +257,8 @@ ipregel_status ipregel_run(ipregel_graph* graph, ipregel_app app, ipregel_combin
                            uint32_t max_supersteps, const ipregel_run_params* params);
 
 /* Copies the full N-vertex result of the last run into `out` (host or device memory per
- * out_is_device).  out_bytes must be N * 8 (PageRank, f64 programs) or N * 4 (CC, SSSP, u32
- * programs).  Multi-GPU: every
+ * out_is_device).  out_bytes must be N * 8 (PageRank, 8-byte program values) or N * 4 (CC,
+ * SSSP, 4-byte program values).  Multi-GPU: every
  * rank receives all N values (collective). */
 ipregel_status ipregel_get_values(ipregel_graph* graph, void* out, size_t out_bytes,
                                   int out_is_device);
@@ -303,7 +303,11 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * The combiner (SUM, MIN, MAX) must be what the program folds with: it is applied in a fixed
  * order in pull mode and by atomics in push mode (SUM f64 in push is order-nondeterministic).
  */
-typedef enum { IPREGEL_VALUE_U32 = 0, IPREGEL_VALUE_F64 = 1 } ipregel_value_type;
+typedef enum {
+    IPREGEL_VALUE_U32 = 0, IPREGEL_VALUE_F64 = 1, IPREGEL_VALUE_F32 = 2, IPREGEL_VALUE_I32 = 3,
+    IPREGEL_VALUE_U64 = 4, IPREGEL_VALUE_I64 = 5
+} ipregel_value_type;   /* ipr_value_t: unsigned int, double, float, int, unsigned long long,
+                           long long; values returned as 4- or 8-byte elements */
 typedef enum {
     IPREGEL_AGG_NONE = 0, IPREGEL_AGG_SUM = 1, IPREGEL_AGG_MIN = 2, IPREGEL_AGG_MAX = 3
 } ipregel_aggregator;

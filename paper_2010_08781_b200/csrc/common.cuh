@@ -157,6 +157,45 @@ __device__ __forceinline__ uint32_t ld_gather_l1(const uint32_t* p, uint64_t pol
     return r;
 }
 
+// Same-size bit reinterpretation (no <cstring> under NVRTC).
+template <class To, class From>
+__device__ __forceinline__ To bit_cast(From f) {
+    static_assert(sizeof(To) == sizeof(From), "same size");
+    union {
+        From f;
+        To t;
+    } u;
+    u.f = f;
+    return u.t;
+}
+template <bool B, class X, class Y> struct cond_type { using type = X; };
+template <class X, class Y> struct cond_type<false, X, Y> { using type = Y; };
+
+// Any other 4- or 8-byte value type (user programs: f32, i32, u64, i64) through the u32 / f64
+// paths by bit pattern.
+template <class T>
+__device__ __forceinline__ T ld_gather(const T* p, uint64_t pol) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte values");
+    T r;
+    if constexpr (sizeof(T) == 8) {
+        r = bit_cast<T>(ld_gather(reinterpret_cast<const double*>(p), pol));
+    } else {
+        r = bit_cast<T>(ld_gather(reinterpret_cast<const uint32_t*>(p), pol));
+    }
+    return r;
+}
+template <class T>
+__device__ __forceinline__ T ld_gather_l1(const T* p, uint64_t pol, int hot) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte values");
+    T r;
+    if constexpr (sizeof(T) == 8) {
+        r = bit_cast<T>(ld_gather_l1(reinterpret_cast<const double*>(p), pol, hot));
+    } else {
+        r = bit_cast<T>(ld_gather_l1(reinterpret_cast<const uint32_t*>(p), pol, hot));
+    }
+    return r;
+}
+
 // Predicated gather (no branch): returns `fallback` bits when pred == 0.
 __device__ __forceinline__ double ld_gather_pred(const double* p, uint64_t pol, int pred) {
     double r;

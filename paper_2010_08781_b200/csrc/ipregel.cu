@@ -397,6 +397,14 @@ template <>
 ncclDataType_t nccl_type<double>() { return ncclFloat64; }
 template <>
 ncclDataType_t nccl_type<uint32_t>() { return ncclUint32; }
+template <>
+ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+template <>
+ncclDataType_t nccl_type<int32_t>() { return ncclInt32; }
+template <>
+ncclDataType_t nccl_type<uint64_t>() { return ncclUint64; }
+template <>
+ncclDataType_t nccl_type<int64_t>() { return ncclInt64; }
 
 // Replicate every partition's owned slice of a replica array into every other replica
 // (multi-GPU: in-place AllGatherv as grouped ncclBroadcast, one root per rank range).
@@ -1577,7 +1585,12 @@ const Nvrtc& nvrtc() {
 // The translation unit NVRTC compiles: the library's own device headers, the user source, and
 // the adapter the kernel templates are instantiated on.
 std::string program_tu(const ipregel_program_desc& d) {
-    const char* vt = d.value_type == IPREGEL_VALUE_F64 ? "double" : "unsigned int";
+    const char* vt = d.value_type == IPREGEL_VALUE_F64   ? "double"
+                   : d.value_type == IPREGEL_VALUE_F32 ? "float"
+                   : d.value_type == IPREGEL_VALUE_I32 ? "int"
+                   : d.value_type == IPREGEL_VALUE_U64 ? "unsigned long long"
+                   : d.value_type == IPREGEL_VALUE_I64 ? "long long"
+                                                       : "unsigned int";
     std::string s;
     s += "#include \"program.cuh\"\n";
     s += "typedef ipr::ProgCtx ipr_ctx;\n";
@@ -1663,14 +1676,35 @@ void launch_jit(cudaKernel_t k, unsigned grid, unsigned block, void** args, cuda
 
 // Bit pattern of the program combiner's identity in an 8-byte slot (u32 in the low half).
 uint64_t prog_identity_bits(const ipregel_program* pr) {
-    if (pr->value_type == IPREGEL_VALUE_F64) {
-        const double id = pr->combiner == IPREGEL_COMBINE_SUM ? 0.0
-                        : (pr->combiner == IPREGEL_COMBINE_MIN ? INFINITY : -INFINITY);
-        uint64_t b;
-        memcpy(&b, &id, 8);
-        return b;
+    const int c = pr->combiner;
+    switch (pr->value_type) {
+        case IPREGEL_VALUE_F64: {
+            const double id = c == IPREGEL_COMBINE_SUM ? 0.0 : (c == IPREGEL_COMBINE_MIN ? INFINITY : -INFINITY);
+            uint64_t b;
+            memcpy(&b, &id, 8);
+            return b;
+        }
+        case IPREGEL_VALUE_F32: {
+            const float id = c == IPREGEL_COMBINE_SUM ? 0.0f : (c == IPREGEL_COMBINE_MIN ? INFINITY : -INFINITY);
+            uint32_t b;
+            memcpy(&b, &id, 4);
+            return b;
+        }
+        case IPREGEL_VALUE_I32:
+            return c == IPREGEL_COMBINE_SUM ? 0ull : (c == IPREGEL_COMBINE_MIN ? 0x7FFFFFFFull : 0x80000000ull);
+        case IPREGEL_VALUE_U64:
+            return c == IPREGEL_COMBINE_MIN ? ~0ull : 0ull;
+        case IPREGEL_VALUE_I64:
+            return c == IPREGEL_COMBINE_SUM ? 0ull
+                 : (c == IPREGEL_COMBINE_MIN ? 0x7FFFFFFFFFFFFFFFull : 0x8000000000000000ull);
+        default:
+            return c == IPREGEL_COMBINE_MIN ? 0xFFFFFFFFull : 0ull;
     }
-    return pr->combiner == IPREGEL_COMBINE_MIN ? 0xFFFFFFFFull : 0ull;
+}
+
+size_t value_bytes(int value_type) {
+    return (value_type == IPREGEL_VALUE_F64 || value_type == IPREGEL_VALUE_U64 ||
+            value_type == IPREGEL_VALUE_I64) ? 8 : 4;
 }
 
 // original -> internal id (the inverse of vertex_ids), built once per graph; NULL without a
@@ -2278,7 +2312,7 @@ ipregel_status ipregel_program_create(const ipregel_program_desc* desc, ipregel_
     if (!out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (!desc || !desc->source) fail(IPREGEL_ERR_INVALID_ARGUMENT, "desc or source is NULL");
-    if (desc->value_type != IPREGEL_VALUE_U32 && desc->value_type != IPREGEL_VALUE_F64)
+    if (desc->value_type < IPREGEL_VALUE_U32 || desc->value_type > IPREGEL_VALUE_I64)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown value_type %d", desc->value_type);
     if (desc->combiner < IPREGEL_COMBINE_SUM || desc->combiner > IPREGEL_COMBINE_MAX)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown combiner %d", desc->combiner);
@@ -2343,17 +2377,37 @@ ipregel_status ipregel_run_program(ipregel_graph* g, ipregel_program* program,
     ipregel_status st;
     try {
         ensure_state(g, kAppProgram);
-        st = program->value_type == IPREGEL_VALUE_F64
-                 ? run_program_t<double>(g, program, max_supersteps, P, program_params,
-                                         num_program_params)
-                 : run_program_t<uint32_t>(g, program, max_supersteps, P, program_params,
+        switch (program->value_type) {
+            case IPREGEL_VALUE_F64:
+                st = run_program_t<double>(g, program, max_supersteps, P, program_params,
                                            num_program_params);
+                break;
+            case IPREGEL_VALUE_F32:
+                st = run_program_t<float>(g, program, max_supersteps, P, program_params,
+                                          num_program_params);
+                break;
+            case IPREGEL_VALUE_I32:
+                st = run_program_t<int32_t>(g, program, max_supersteps, P, program_params,
+                                            num_program_params);
+                break;
+            case IPREGEL_VALUE_U64:
+                st = run_program_t<uint64_t>(g, program, max_supersteps, P, program_params,
+                                             num_program_params);
+                break;
+            case IPREGEL_VALUE_I64:
+                st = run_program_t<int64_t>(g, program, max_supersteps, P, program_params,
+                                            num_program_params);
+                break;
+            default:
+                st = run_program_t<uint32_t>(g, program, max_supersteps, P, program_params,
+                                             num_program_params);
+        }
     } catch (const Failure& f) {
         if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
         throw;
     }
     g->last_app = kAppProgram;
-    g->last_vsz = program->value_type == IPREGEL_VALUE_F64 ? 8 : 4;
+    g->last_vsz = (int)value_bytes(program->value_type);
     g->last_status = st;
     if (st != IPREGEL_OK) g_last_error = "superstep guard reached with work remaining";
     return st;

@@ -137,6 +137,94 @@ template <> struct ProgComb<double, 2> {     // MAX
     __device__ static void atomic(double* p, double v) { atomic_f64_select(p, v, false); }
 };
 
+// f32 / i32 / u64 / i64 values (ipregel_value_type F32, I32, U64, I64)
+template <class T>
+__device__ __forceinline__ void atomic_select_cas(T* p, T v, bool want_min) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte values");
+    using U = typename cond_type<sizeof(T) == 8, unsigned long long, unsigned int>::type;
+    U* q = reinterpret_cast<U*>(p);
+    U old = *q;
+    while (true) {
+        const T cur = bit_cast<T>(old);
+        if (want_min ? !(v < cur) : !(v > cur)) return;
+        const U seen = atomicCAS(q, old, bit_cast<U>(v));
+        if (seen == old) return;
+        old = seen;
+    }
+}
+template <> struct ProgComb<float, 0> {
+    __device__ static float identity() { return 0.0f; }
+    __device__ static float combine(float a, float b) { return __fadd_rn(a, b); }
+    __device__ static void atomic(float* p, float v) { atomicAdd(p, v); }
+};
+template <> struct ProgComb<float, 1> {
+    __device__ static float identity() { return __int_as_float(0x7F800000); }
+    __device__ static float combine(float a, float b) { return b < a ? b : a; }
+    __device__ static void atomic(float* p, float v) { atomic_select_cas(p, v, true); }
+};
+template <> struct ProgComb<float, 2> {
+    __device__ static float identity() { return __int_as_float((int)0xFF800000u); }
+    __device__ static float combine(float a, float b) { return b > a ? b : a; }
+    __device__ static void atomic(float* p, float v) { atomic_select_cas(p, v, false); }
+};
+template <> struct ProgComb<int32_t, 0> {
+    __device__ static int32_t identity() { return 0; }
+    __device__ static int32_t combine(int32_t a, int32_t b) { return (int32_t)((uint32_t)a + (uint32_t)b); }
+    __device__ static void atomic(int32_t* p, int32_t v) { atomicAdd(p, v); }
+};
+template <> struct ProgComb<int32_t, 1> {
+    __device__ static int32_t identity() { return 0x7FFFFFFF; }
+    __device__ static int32_t combine(int32_t a, int32_t b) { return b < a ? b : a; }
+    __device__ static void atomic(int32_t* p, int32_t v) { if (v < *p) atomicMin(p, v); }
+};
+template <> struct ProgComb<int32_t, 2> {
+    __device__ static int32_t identity() { return (int32_t)0x80000000u; }
+    __device__ static int32_t combine(int32_t a, int32_t b) { return b > a ? b : a; }
+    __device__ static void atomic(int32_t* p, int32_t v) { if (v > *p) atomicMax(p, v); }
+};
+template <> struct ProgComb<uint64_t, 0> {
+    __device__ static uint64_t identity() { return 0ull; }
+    __device__ static uint64_t combine(uint64_t a, uint64_t b) { return a + b; }
+    __device__ static void atomic(uint64_t* p, uint64_t v) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    }
+};
+template <> struct ProgComb<uint64_t, 1> {
+    __device__ static uint64_t identity() { return ~0ull; }
+    __device__ static uint64_t combine(uint64_t a, uint64_t b) { return b < a ? b : a; }
+    __device__ static void atomic(uint64_t* p, uint64_t v) {
+        if (v < *p) atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    }
+};
+template <> struct ProgComb<uint64_t, 2> {
+    __device__ static uint64_t identity() { return 0ull; }
+    __device__ static uint64_t combine(uint64_t a, uint64_t b) { return b > a ? b : a; }
+    __device__ static void atomic(uint64_t* p, uint64_t v) {
+        if (v > *p) atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    }
+};
+template <> struct ProgComb<int64_t, 0> {
+    __device__ static int64_t identity() { return 0; }
+    __device__ static int64_t combine(int64_t a, int64_t b) { return (int64_t)((uint64_t)a + (uint64_t)b); }
+    __device__ static void atomic(int64_t* p, int64_t v) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    }
+};
+template <> struct ProgComb<int64_t, 1> {
+    __device__ static int64_t identity() { return 0x7FFFFFFFFFFFFFFFLL; }
+    __device__ static int64_t combine(int64_t a, int64_t b) { return b < a ? b : a; }
+    __device__ static void atomic(int64_t* p, int64_t v) {
+        if (v < *p) atomicMin(reinterpret_cast<long long*>(p), (long long)v);
+    }
+};
+template <> struct ProgComb<int64_t, 2> {
+    __device__ static int64_t identity() { return (int64_t)0x8000000000000000ULL; }
+    __device__ static int64_t combine(int64_t a, int64_t b) { return b > a ? b : a; }
+    __device__ static void atomic(int64_t* p, int64_t v) {
+        if (v > *p) atomicMax(reinterpret_cast<long long*>(p), (long long)v);
+    }
+};
+
 template <class V>
 __device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
     ProgCtx x;

@@ -18,9 +18,12 @@ LIB_PATH = os.environ.get("IPREGEL_LIB") or os.path.join(_HERE, "libipregel.so")
 
 APP_PAGERANK, APP_HASHMIN_CC, APP_SSSP = 0, 1, 2
 COMBINE_SUM, COMBINE_MIN, COMBINE_MAX = 0, 1, 2
-VALUE_U32, VALUE_F64 = 0, 1
+VALUE_U32, VALUE_F64, VALUE_F32, VALUE_I32, VALUE_U64, VALUE_I64 = 0, 1, 2, 3, 4, 5
 COMBINERS = {"sum": COMBINE_SUM, "min": COMBINE_MIN, "max": COMBINE_MAX}
-VALUE_TYPES = {"u32": VALUE_U32, "f64": VALUE_F64}
+VALUE_TYPES = {"u32": VALUE_U32, "f64": VALUE_F64, "f32": VALUE_F32, "i32": VALUE_I32,
+               "u64": VALUE_U64, "i64": VALUE_I64}
+_NP_DTYPES = {"u32": np.uint32, "f64": np.float64, "f32": np.float32, "i32": np.int32,
+              "u64": np.uint64, "i64": np.int64}
 APP_PROGRAM = 3   # last run was a user program
 MODE_AUTO, MODE_PULL, MODE_PUSH = 0, 1, 2
 MEMORY_DEVICE, MEMORY_HOST = 0, 1
@@ -386,7 +389,7 @@ class Graph:
                                         ctypes.byref(p), vals, len(params))
         _check(st, "ipregel_run_program", allow=(ERR_MAX_SUPERSTEPS,) if allow_guard else ())
         self.last_app = APP_PROGRAM
-        self._last_f64 = program.value_type == "f64"
+        self._last_vt = program.value_type
         return st
 
     def values(self, out=None, host: bool = False):
@@ -394,14 +397,20 @@ class Graph:
         import torch
         if self.last_app is None:
             raise IpregelError(ERR_STATE, "values", "no completed run")
-        pr = self.last_app == APP_PAGERANK or (self.last_app == APP_PROGRAM and self._last_f64)
+        if self.last_app == APP_PROGRAM:
+            dt = _NP_DTYPES[self._last_vt]
+        else:
+            dt = np.float64 if self.last_app == APP_PAGERANK else np.uint32
         if host:
-            out = np.empty(self.n, np.float64 if pr else np.uint32)
+            out = np.empty(self.n, dt)
             _check(load().ipregel_get_values(self.handle, out.ctypes.data, out.nbytes, 0),
                    "ipregel_get_values")
             return out
         if out is None:
-            out = torch.empty(self.n, dtype=torch.float64 if pr else torch.int32, device="cuda")
+            tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+                   np.dtype(np.uint64): torch.int64, np.dtype(np.int64): torch.int64}.get(
+                       np.dtype(dt), torch.int32)
+            out = torch.empty(self.n, dtype=tdt, device="cuda")
         _check(load().ipregel_get_values(self.handle, out.data_ptr(),
                                          out.numel() * out.element_size(), 1),
                "ipregel_get_values")

@@ -214,6 +214,89 @@ __device__ unsigned ipr_compute(const ipr_ctx& c, double* value, double, double*
 __device__ double ipr_edge(double message, unsigned) { return message; }
 """
 
+# The same Fig. 10 / Fig. 9 programs over other value types (ipregel_value_type).
+SSSP_F32 = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, float* value, float* message) {
+    if (c.id == (long long)c.params[0]) {
+        *value = 0.0f;
+        *message = 0.0f;
+        return IPR_BROADCAST;
+    }
+    *value = __int_as_float(0x7F800000);                   // +inf: unreached
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, float* value, float mailbox, float* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ float ipr_edge(float message, unsigned weight) { return message + (float)weight; }
+"""
+
+SSSP_I32 = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, int* value, int* message) {
+    if (c.id == (long long)c.params[0]) {
+        *value = 0;
+        *message = 0;
+        return IPR_BROADCAST;
+    }
+    *value = 0x7FFFFFFF;                                   // INT_MAX: unreached
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, int* value, int mailbox, int* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ int ipr_edge(int message, unsigned weight) {
+    return message == 0x7FFFFFFF ? message : message + (int)weight;
+}
+"""
+
+HASHMIN_U64 = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned long long* value,
+                             unsigned long long* message) {
+    *value = (unsigned long long)c.id;
+    *message = *value;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, unsigned long long* value,
+                                unsigned long long mailbox, unsigned long long* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ unsigned long long ipr_edge(unsigned long long message, unsigned) { return message; }
+"""
+
+# Hash-Min over negated ids (signed 64-bit): every vertex ends with -(largest id of its component).
+MIN_NEG_LABEL_I64 = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, long long* value, long long* message) {
+    *value = -(long long)c.id;
+    *message = *value;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx&, long long* value, long long mailbox,
+                                long long* message) {
+    if (mailbox < *value) {
+        *value = mailbox;
+        *message = mailbox;
+        return IPR_BROADCAST;
+    }
+    return 0;
+}
+__device__ long long ipr_edge(long long message, unsigned) { return message; }
+"""
+
 CATALOG = {
     "pagerank": (PAGERANK, "f64", "sum", False),
     "hashmin_cc": (HASHMIN_CC, "u32", "min", True),
@@ -226,6 +309,10 @@ CATALOG = {
     "pagerank_converge": (PAGERANK_CONVERGE, "f64", "sum", False, "max"),
     "heap_children_sum": (HEAP_CHILDREN_SUM, "u32", "sum", False),
     "count_vertices": (COUNT_VERTICES, "f64", "sum", False, "sum"),
+    "sssp_f32": (SSSP_F32, "f32", "min", False),
+    "sssp_i32": (SSSP_I32, "i32", "min", False),
+    "hashmin_u64": (HASHMIN_U64, "u64", "min", True),
+    "min_neg_label_i64": (MIN_NEG_LABEL_I64, "i64", "min", True),
 }
 
 

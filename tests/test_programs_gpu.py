@@ -242,3 +242,27 @@ def test_pagerank_converge_program_equals_oracle(mode, parts):
     assert np.abs(v - o["values"]).max() <= PR_ABS
     assert G.stats()["supersteps"] == o["supersteps"] + 1
     G.close()
+
+
+# ------------------------------------------------------------------ other value types
+
+@pytest.mark.parametrize("mode,parts", [("pull", 1), ("push", 1), ("auto", 3)])
+def test_typed_programs(mode, parts):
+    """f32 / i32 / u64 / i64 values: the same programs, pinned to brute force."""
+    n, src, dst, w = graph(77, n=1800)
+    G = make_graph(csr_csc(n, src, dst, w), partitions=parts)
+    e3 = list(zip(src.tolist(), dst.tolist(), w.tolist()))
+    e2 = list(zip(src.tolist(), dst.tolist()))
+    d = np.array(checkers.dijkstra(n, e3, 4), dtype=np.int64)
+    G.run_program(prog("sssp_i32"), params=[4], mode=mode)
+    want = np.where(d == checkers.INF, 0x7FFFFFFF, d).astype(np.int32)
+    np.testing.assert_array_equal(G.values(host=True), want)
+    G.run_program(prog("sssp_f32"), params=[4], mode=mode)
+    want = np.where(d == checkers.INF, np.inf, d).astype(np.float32)   # integer sums < 2^24
+    np.testing.assert_array_equal(G.values(host=True), want)
+    lab = np.array(checkers.cc_union_find(n, e2), dtype=np.uint64)
+    G.run_program(prog("hashmin_u64"), mode=mode)
+    np.testing.assert_array_equal(G.values(host=True), lab)
+    G.run_program(prog("min_neg_label_i64"), mode=mode)
+    np.testing.assert_array_equal(G.values(host=True), -np.array(checkers.cc_max_label(n, e2), np.int64))
+    G.close()
