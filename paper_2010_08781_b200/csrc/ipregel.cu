@@ -7,6 +7,7 @@
 // same kernels, counts broadcasters and messages on the device, exchanges owned values between
 // partitions, and the host reads the counters to decide termination ("every active vertex has
 // been processed and every outgoing message delivered").
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -127,7 +128,7 @@ struct ipregel_comm {
 namespace {
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync), which keeps up to
-// IPREGEL_POOL_RETAIN_BYTES (default 64 GiB) of freed memory for the next graph instead of
+// IPREGEL_POOL_RETAIN_BYTES (default 96 GiB) of freed memory for the next graph instead of
 // returning it to the driver: creating and destroying a graph handle per job stays cheap (a
 // plain cudaMalloc/cudaFree of the 7.5 GB adjacency copies costs ~100 ms each).  Buffers another
 // process maps with CUDA IPC (fused-exchange replicas of a rank) use cudaMalloc.
@@ -141,7 +142,7 @@ void configure_pool(int device) {
         return;
     }
     const char* e = getenv("IPREGEL_POOL_RETAIN_BYTES");
-    uint64_t keep = e ? strtoull(e, nullptr, 10) : (64ull << 30);
+    uint64_t keep = e ? strtoull(e, nullptr, 10) : (96ull << 30);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
 }
 
@@ -572,19 +573,36 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
     int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
     int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
     uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
-    if (edges > 0) {
-        k_hist_sources<<<grid_for(edges, 256) > 4096 ? 4096 : grid_for(edges, 256), 256, 0, s>>>(
-            idx, edges, o);
-        LAUNCH_CHECK();
-    }
     DeviceBuffers tmp;
-    exscan_i32(o, n + 1, tmp, s);
-    int32_t* cursor = tmp.alloc<int32_t>(n + 1, s);
-    CU(cudaMemcpyAsync(cursor, o, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    if (p.rows > 0) {
-        k_transpose_rows<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, idx, w, p.rows, p.vb,
-                                                                   cursor, ix, wx);
+    if (p.rows == 0 || edges == 0) CU(cudaMemsetAsync(o, 0, (n + 1) * sizeof(int32_t), s));
+    if (p.rows > 0 && edges > 0) {
+        // stable radix sort of (source, row | weight << 32) by source: coalesced, and each
+        // transposed row lists its destinations in ascending order
+        int32_t* k0 = tmp.alloc<int32_t>(edges, s);
+        int32_t* k1 = tmp.alloc<int32_t>(edges, s);
+        unsigned long long* v0 = tmp.alloc<unsigned long long>(edges, s);
+        unsigned long long* v1 = tmp.alloc<unsigned long long>(edges, s);
+        CU(cudaMemcpyAsync(k0, idx, edges * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        k_transpose_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, w, p.rows, p.vb, v0);
         LAUNCH_CHECK();
+        cub::DoubleBuffer<int32_t> keys(k0, k1);
+        cub::DoubleBuffer<unsigned long long> vals(v0, v1);
+        int bits = 1;
+        while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+        size_t temp_bytes = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, vals, edges, 0, bits, s));
+        void* temp = tmp.alloc<uint8_t>((int64_t)temp_bytes, s);
+        CU(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, edges, 0, bits, s));
+        k_transpose_unpack<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
+            vals.Current(), edges, ix, wx);
+        LAUNCH_CHECK();
+        // offsets from the sorted sources: run lengths, then an exclusive scan
+        int32_t* st = tmp.alloc<int32_t>(n, s, true);
+        k_run_bounds<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
+            keys.Current(), edges, st, o);
+        k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, o);
+        LAUNCH_CHECK();
+        exscan_i32(o, n + 1, tmp, s);
     }
     CU(cudaStreamSynchronize(s));
     tmp.release();

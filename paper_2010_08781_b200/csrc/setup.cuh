@@ -195,6 +195,48 @@ __global__ void k_transpose_rows(const int32_t* __restrict__ off, const int32_t*
     }
 }
 
+// Sort-based transpose (coalesced writes; the atomic-cursor scatter above writes 4-byte words
+// at random, which costs ~7x the bytes in DRAM read-modify-write): every edge becomes a
+// (source, row | weight << 32) pair, a stable LSD radix sort by source groups the pairs into
+// the transposed rows with their destinations ascending (the input is in row order), and the
+// unpack writes indices and weights contiguously.
+__global__ void k_transpose_pack(const int32_t* __restrict__ off, const uint32_t* __restrict__ w,
+                                 int64_t rows, int64_t vbase, unsigned long long* __restrict__ vals) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const unsigned long long v = (unsigned long long)(uint32_t)(vbase + r);
+    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32)
+        vals[e] = v | ((unsigned long long)(w ? w[e] : 1u) << 32);
+}
+
+// Run boundaries of the sorted sources: start[k] = first position of source k, end[k] = one past
+// its last (both 0 for sources without edges); then count[k] = end[k] - start[k] in place.
+__global__ void k_run_bounds(const int32_t* __restrict__ keys, int64_t edges,
+                             int32_t* __restrict__ start, int32_t* __restrict__ end) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k) start[k] = (int32_t)i;
+        if (i + 1 == edges || keys[i + 1] != k) end[k] = (int32_t)(i + 1);
+    }
+}
+__global__ void k_run_counts(const int32_t* __restrict__ start, int64_t n,
+                             int32_t* __restrict__ end_to_count) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) end_to_count[u] = end_to_count[u] ? end_to_count[u] - start[u] : 0;
+}
+
+__global__ void k_transpose_unpack(const unsigned long long* __restrict__ vals, int64_t edges,
+                                   int32_t* __restrict__ out_idx, uint32_t* __restrict__ out_w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = vals[i];
+        out_idx[i] = (int32_t)(uint32_t)x;
+        if (out_w) out_w[i] = (uint32_t)(x >> 32);
+    }
+}
+
 // Device-wide exclusive scan of int32 counts (in place), 3 passes with a u64 block scratch.
 constexpr int kScanChunk = 2048;
 __global__ void __launch_bounds__(256)
