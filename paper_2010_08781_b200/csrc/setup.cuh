@@ -173,28 +173,6 @@ __global__ void k_validate_indices(const int32_t* __restrict__ idx, int64_t edge
 // ---- push view for a destination partition (multi-GPU push mode) ---------------------------
 // Source-major list of the edges whose destination is owned: built by transposing the owned
 // CSC rows (u -> v) and, for CC, the owned CSR rows reversed (u <- v taken as u -> v).
-__global__ void k_hist_sources(const int32_t* __restrict__ idx, int64_t edges,
-                               int32_t* __restrict__ cnt /* [n+1]; exclusive-scanned after */) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
-         i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(cnt + idx[i], 1);
-}
-
-__global__ void k_transpose_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                                 const uint32_t* __restrict__ w, int64_t rows, int64_t vbase,
-                                 int32_t* __restrict__ cursor, int32_t* __restrict__ out_idx,
-                                 uint32_t* __restrict__ out_w) {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (r >= rows) return;
-    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32) {
-        const int32_t u = idx[e];
-        const int32_t pos = atomicAdd(cursor + u, 1);
-        out_idx[pos] = (int32_t)(vbase + r);
-        if (out_w) out_w[pos] = w ? w[e] : 1u;
-    }
-}
-
 // Sort-based transpose (coalesced writes; the atomic-cursor scatter above writes 4-byte words
 // at random, which costs ~7x the bytes in DRAM read-modify-write): every edge becomes a
 // (source, row | weight << 32) pair, a stable LSD radix sort by source groups the pairs into
