@@ -173,8 +173,8 @@ __global__ void k_validate_indices(const int32_t* __restrict__ idx, int64_t edge
 // ---- push view for a destination partition (multi-GPU push mode) ---------------------------
 // Source-major list of the edges whose destination is owned: built by transposing the owned
 // CSC rows (u -> v) and, for CC, the owned CSR rows reversed (u <- v taken as u -> v).
-// Sort-based transpose (coalesced writes; the atomic-cursor scatter above writes 4-byte words
-// at random, which costs ~7x the bytes in DRAM read-modify-write): every edge becomes a
+// Sort-based transpose (coalesced writes; an atomic-cursor scatter writes 4-byte words at
+// random, which costs ~7x the bytes in DRAM read-modify-write): every edge becomes a
 // (source, row | weight << 32) pair, a stable LSD radix sort by source groups the pairs into
 // the transposed rows with their destinations ascending (the input is in row order), and the
 // unpack writes indices and weights contiguously.
