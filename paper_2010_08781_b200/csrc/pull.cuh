@@ -425,6 +425,23 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
     // chunks on the global 128-edge grid covering [y0, y1)
     const int32_t c0 = y0 - ((y0 + A.cphase) & (kChunk - 1));
 
+    if constexpr (Op::kAbsorbing) {
+        // every row of the range (and the one leaving it) is settled: no gather can change any
+        // of them, so finish them straight away (runs of short rows the chunk skip cannot catch)
+        const int32_t last = y1 > (x1 < A.rows ? A.off[x1] : y1) ? x1 : x1 - 1;
+        bool all = true;
+        for (int32_t row = r + lane; row <= last && all; row += 32)
+            all = op.absorbed(row);
+        if (__all_sync(kFull, all)) {
+            for (int32_t row = r + lane; row < x1; row += 32) {
+                if (row == defer) static_cast<T*>(A.head_out)[q] = Op::identity();
+                else op.finish(row, Op::identity(), cnt);
+            }
+            if (lane == 0) static_cast<T*>(A.carry_out)[q] = Op::identity();
+            return;
+        }
+    }
+
     // software pipeline: indices two chunks ahead, gathered values one chunk ahead
     ChunkLoad Lc = load_chunk<Op::kWeighted>(A.idx, A.wts, c0, y0, y1, lane, pol_s);
     ChunkLoad Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
