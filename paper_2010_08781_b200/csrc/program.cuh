@@ -394,10 +394,6 @@ struct ProgPull : ProgArgs<typename P::V> {
     __device__ void flush_aggregate(const LaneCounters& c) const {
         flush_prog_aggregate(c, this->agg_op, this->shared ? this->shared->agg : nullptr);
     }
-    __device__ void flush_aggregate_lane(const LaneCounters& c) const {   // one thread
-        if (this->agg_op >= 0 && c.agg_n && this->shared)
-            agg_atomic(this->agg_op, this->shared->agg, c.agg);
-    }
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }

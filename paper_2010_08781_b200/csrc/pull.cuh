@@ -607,29 +607,29 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
                              const typename Op::T* __restrict__ head,
                              PullCounters* __restrict__ counters) {
     using T = typename Op::T;
+    __shared__ unsigned long long s_cnt[4];
     const int lane = threadIdx.x & 31;
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= num_groups) return;
-    const int4 G = groups[g];
-    T acc = Op::identity();
-    for (int t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
+    if (g < num_groups) {
+        const int4 G = groups[g];
+        T acc = Op::identity();
+        for (int t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const T o = shfl_xor(acc, d);
-        acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
-    }
-    if (lane == 0) {
-        acc = Op::combine(acc, head[G.z]);
-        LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
-        op.finish(G.x, acc, c);
-        if constexpr (Op::kAggregates) op.flush_aggregate_lane(c);
-        if (counters && (c.changed | c.messages | c.dmax | c.aux)) {
-            atomicAdd(&counters->changed, c.changed);
-            atomicAdd(&counters->messages, c.messages);
-            atomicMax(&counters->dmax, c.dmax);
-            atomicAdd(&counters->aux, c.aux);
+        for (int d = 1; d < 32; d <<= 1) {
+            const T o = shfl_xor(acc, d);
+            acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
+        }
+        if (lane == 0) {
+            acc = Op::combine(acc, head[G.z]);
+            op.finish(G.x, acc, c);
         }
     }
+    // one global atomic per CTA (not per group: the counters are shared by every group)
+    flush_counters(c, s_cnt, counters);
+    if constexpr (Op::kAggregates) op.flush_aggregate(c);
 }
 
 }  // namespace ipr
