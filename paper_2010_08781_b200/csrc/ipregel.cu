@@ -266,6 +266,18 @@ struct ipregel_graph {
     int64_t last_rowlist_edges = 0;
     int64_t w_min = -1;            // smallest edge weight (SSSP absorption bound), lazily
     const int32_t* inv_ids = nullptr;   // original -> internal id (user programs' ipr_send)
+    cudaStream_t capture_stream = nullptr;   // private stream for CUDA-graph capture
+    // PageRank (fixed k, pull) captured once as a CUDA graph and replayed: one launch per run
+    struct {
+        bool valid = false;
+        uint32_t k = 0, max_steps = 0, flags = 0;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<StepRecord> steps;
+        int cur = 0;
+        int exchange = 0;
+        ipregel_status status = IPREGEL_OK;
+        unsigned long long launches = 0;
+    } pr_graph;
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
@@ -886,13 +898,23 @@ cudaEvent_t ev(ipregel_graph* g, size_t i) {
     return g->events[i];
 }
 
+// Per-superstep CUDA events on the run stream.  Inside a CUDA-graph capture they are recorded as
+// external event nodes, so they still time the superstep when the graph is replayed.
 struct StepTimer {
     ipregel_graph* g;
     size_t step;
-    void begin() { CU(cudaEventRecord(ev(g, 4 * step + 0), g->stream)); }
-    void kbegin() { CU(cudaEventRecord(ev(g, 4 * step + 1), g->stream)); }
-    void kend() { CU(cudaEventRecord(ev(g, 4 * step + 2), g->stream)); }
-    void end() { CU(cudaEventRecord(ev(g, 4 * step + 3), g->stream)); }
+    void rec(size_t i) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CU(cudaStreamIsCapturing(g->stream, &cs));
+        if (cs == cudaStreamCaptureStatusActive)
+            CU(cudaEventRecordWithFlags(ev(g, i), g->stream, cudaEventRecordExternal));
+        else
+            CU(cudaEventRecord(ev(g, i), g->stream));
+    }
+    void begin() { rec(4 * step + 0); }
+    void kbegin() { rec(4 * step + 1); }
+    void kend() { rec(4 * step + 2); }
+    void end() { rec(4 * step + 3); }
 };
 
 void finalize_times(ipregel_graph* g) {
@@ -911,6 +933,7 @@ void finalize_times(ipregel_graph* g) {
 // =============================================================================================
 ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_run_params& P) {
     cudaStream_t s = g->stream;
+    const cudaStream_t user_stream = g->stream;
     const int64_t n = g->n;
     const uint32_t k = P.pagerank_iterations;
     const double ratio = 0.15 / (double)n;   // Pregel's 0.15 / NumVertices()
@@ -934,6 +957,32 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         CU(cudaMemcpyAsync(p.host_cnt + 1, p.dscratch + 1, 8, cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         nondangling = (int64_t)p.host_cnt[1];
+    }
+
+    // Fixed-k pull runs have no host synchronisation between supersteps: the whole run (superstep
+    // 0 .. k, exchanges and per-superstep timing events included) is captured once as a CUDA
+    // graph and replayed by every later run with the same parameters (IPREGEL_NO_GRAPHS=1: off).
+    static const bool no_graphs = getenv("IPREGEL_NO_GRAPHS") != nullptr;
+    const bool graphable = !track && !push && !g_persist_bytes && !no_graphs;
+    auto& G = g->pr_graph;
+    if (graphable && G.valid && G.k == k && G.max_steps == max_steps && G.flags == P.flags) {
+        CU(cudaGraphLaunch(G.exec, s));
+        g_launches.fetch_add(G.launches, std::memory_order_relaxed);
+        g->steps = G.steps;
+        g->cur = G.cur;
+        g->last_exchange = G.exchange;
+        finalize_times(g);
+        return G.status;
+    }
+    const unsigned long long launches0 = g_launches.load(std::memory_order_relaxed);
+    if (graphable) {
+        for (uint32_t i = 0; i <= 4 * (k + 1); ++i) ev(g, i);   // events exist before capture
+        // capture on a private stream (the caller's may be the legacy default stream, which
+        // cannot be captured); the graph is then launched on the caller's stream
+        if (!g->capture_stream)
+            CU(cudaStreamCreateWithFlags(&g->capture_stream, cudaStreamNonBlocking));
+        g->stream = s = g->capture_stream;
+        CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     }
 
     // superstep 0
@@ -1053,6 +1102,28 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         }
     }
     g->cur = cur;
+    if (graphable) {
+        cudaGraph_t graph = nullptr;
+        g->stream = user_stream;
+        CU(cudaStreamEndCapture(s, &graph));
+        s = user_stream;
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+        G.valid = false;
+        const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CU(ie);
+        G.valid = true;
+        G.k = k;
+        G.max_steps = max_steps;
+        G.flags = P.flags;
+        G.steps = g->steps;
+        G.cur = cur;
+        G.exchange = g->last_exchange;
+        G.status = status;
+        G.launches = g_launches.load(std::memory_order_relaxed) - launches0;
+        CU(cudaGraphLaunch(G.exec, s));
+    }
     finalize_times(g);
     return status;
 }
@@ -1507,6 +1578,8 @@ void destroy_graph(ipregel_graph* g) {
         if (p.host_cnt) cudaFreeHost(p.host_cnt);
         p.host_cnt = nullptr;
     }
+    if (g->pr_graph.exec) cudaGraphExecDestroy(g->pr_graph.exec);
+    if (g->capture_stream) cudaStreamDestroy(g->capture_stream);
     for (auto e : g->events) cudaEventDestroy(e);
     g->graph_mem.release();
     cudaStreamSynchronize(g->stream);
@@ -2309,11 +2382,24 @@ ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner c
     g->last_status = -1;
     g->last_app = -1;
     ipregel_status st;
+    const cudaStream_t caller_stream = g->stream;
     try {
         ensure_state(g, app);
         st = app == IPREGEL_APP_PAGERANK ? run_pagerank(g, max_supersteps, P)
                                          : run_min(g, app, max_supersteps, P);
     } catch (const Failure& f) {
+        // a failure inside a CUDA-graph capture: close the capture, back to the caller's stream
+        if (g->capture_stream) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (cudaStreamIsCapturing(g->capture_stream, &cs) == cudaSuccess &&
+                cs != cudaStreamCaptureStatusNone) {
+                cudaGraph_t gr = nullptr;
+                cudaStreamEndCapture(g->capture_stream, &gr);
+                if (gr) cudaGraphDestroy(gr);
+            }
+            cudaGetLastError();
+        }
+        g->stream = caller_stream;
         if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
         throw;
     }

@@ -633,3 +633,31 @@ def test_csr_derivation_needs_one_whole_partition():
     h = ctypes.c_void_p()
     st = ipr.load().ipregel_graph_create_partitioned(descs, 2, None, ctypes.byref(h))
     assert st == ipr.ERR_UNSUPPORTED
+
+
+def test_pagerank_graph_replay_matches_first_run():
+    """Fixed-k pull PageRank is captured as a CUDA graph on its first run and replayed: replays
+    give the same values, counters and timing records; other k / max_supersteps re-capture."""
+    import paper_2010_08781_b200 as ipr
+    rng = np.random.default_rng(21)
+    n = 4000
+    src, dst, _ = checkers.random_graph(rng, n, 30000)
+    G = make_graph(csr_csc(n, src, dst), partitions=2, weighted=False)
+    launches = []
+    vals = []
+    for k in (10, 10, 10, 3, 10):
+        before = ipr.kernel_launches()
+        G.run("pagerank", mode="pull", iterations=k)
+        launches.append(ipr.kernel_launches() - before)
+        vals.append(G.values(host=True))
+        s = G.stats()
+        assert s["supersteps"] == k + 1 and (s["time_ms"] > 0).all()
+    np.testing.assert_array_equal(vals[0], vals[1])
+    np.testing.assert_array_equal(vals[0], vals[2])
+    np.testing.assert_array_equal(vals[0], vals[4])
+    assert launches[0] == launches[1] == launches[2]   # replays count the captured kernels
+    o = oracle.pagerank(n, src, dst, k=3)
+    assert np.abs(vals[3] - o["values"]).max() <= PR_ABS
+    st = G.run("pagerank", mode="pull", iterations=10, max_supersteps=5, allow_guard=True)
+    assert st == ipr.ERR_MAX_SUPERSTEPS and G.stats()["supersteps"] == 5
+    G.close()
