@@ -201,7 +201,6 @@ int64_t rmat_gpu_coo(uint64_t seed, int scale, uint64_t slots, uint32_t ta, uint
     CK(cudaMallocAsync(&blk, (nb + 1) * 8, s));
     k_block_counts<<<(unsigned)nb, kThreads, 0, s>>>(g, slots, blk);
     CK(cudaGetLastError());
-    unsigned long long* tmp_out = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, blk, blk, (int)nb + 1, s);
@@ -209,7 +208,6 @@ int64_t rmat_gpu_coo(uint64_t seed, int scale, uint64_t slots, uint32_t ta, uint
     // blk[nb] must be 0 before the scan so the total lands in blk[nb]
     CK(cudaMemsetAsync(blk + nb, 0, 8, s));
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, blk, blk, (int)nb + 1, s);
-    (void)tmp_out;
     k_block_write<<<(unsigned)nb, kThreads, 0, s>>>(g, slots, blk, src, dst, w);
     CK(cudaGetLastError());
     unsigned long long kept = 0;
