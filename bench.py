@@ -123,6 +123,14 @@ def ncu_traffic():
         return None
 
 
+def device_info(device):
+    import torch
+    p = torch.cuda.get_device_properties(device)
+    return {"name": p.name, "sms": p.multi_processor_count,
+            "l2_bytes": getattr(p, "L2_cache_size", None),
+            "hbm_bytes": p.total_memory}
+
+
 def delivered_messages(stats):
     """Messages delivered by supersteps 1..S-1 = messages sent in supersteps 0..S-2."""
     m = stats["messages"].astype(np.int64)
@@ -309,9 +317,14 @@ def main():
         sts = [step[app] for step in per_step]
         t_app = float(np.mean([s["time_ms"].sum() for s in sts]))
         d = delivered_messages(sts[0])
+        st0 = sts[0]
         apps_out[app] = {"gteps": d / (t_app * 1e-3) / 1e9, "ms": t_app,
-                         "supersteps": int(sts[0]["supersteps"]),
-                         "modes": "".join("ilpr"[m] for m in sts[0]["mode"])}
+                         "supersteps": int(st0["supersteps"]),
+                         "modes": "".join("ilpr"[m] for m in st0["mode"]),
+                         # per superstep (first timed step): device ms, messages sent, model bytes
+                         "superstep_ms": [round(float(x), 4) for x in st0["time_ms"]],
+                         "superstep_messages": [int(x) for x in st0["messages"]],
+                         "superstep_model_gb": [round(float(x) / 1e9, 3) for x in st0["model_bytes"]]}
     roof = None
     if "pagerank" in args.apps:
         sts = [step["pagerank"] for step in per_step]
@@ -348,6 +361,7 @@ def main():
                    "layout": "degree-ordered internal ids (results in original ids)",
                    "n": n, "e": e, "parallelism": f"1D destination partition x{world}",
                    "l2": "inputs larger than L2 (7.5 GB per adjacency array), no flush",
+                   "device": device_info(local),
                    "apps": apps_out},
         "roofline": roof,
         "gpu_launches": int(launches),
