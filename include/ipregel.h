@@ -296,6 +296,10 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * program's combiner and delivered in the next superstep, where dest computes (it counts in
  * `messages`; one GPU: whole graph or loopback partitions; not across ranks: UNSUPPORTED);
  * ipr_aggregate(c, x) -- fold the f64 x into the run's aggregator (desc.aggregator).
+ * Optional hint: __device__ bool ipr_absorbing(ipr_value_t value) -- true when a vertex holding
+ * `value` ignores every message (e.g. Hash-Min's label 0): pull supersteps then skip gathering
+ * its in-edges, and whole merge-path ranges of such vertices (compute still runs, with the
+ * identity as mailbox).
  * The run ends when a superstep has no broadcast and no active vertex.
  * Selection (R28): push supersteps run compute on recipients and active vertices
  * only; pull supersteps run it on every vertex, the non-recipients getting the identity, so a

@@ -1703,6 +1703,12 @@ std::string program_tu(const ipregel_program_desc& d) {
          (strstr(d.source, "ipr_send") ? "true" : "false") + ";\n";
     s += std::string("  static constexpr bool kAggregates = ") +
          (d.aggregator != IPREGEL_AGG_NONE ? "true" : "false") + ";\n";
+    const bool absorbing = strstr(d.source, "ipr_absorbing") != nullptr;
+    s += std::string("  static constexpr bool kAbsorbing = ") + (absorbing ? "true" : "false") + ";\n";
+    if (absorbing)
+        s += "  static __device__ __forceinline__ bool absorbing(V v) { return ipr_absorbing(v); }\n";
+    else
+        s += "  static __device__ __forceinline__ bool absorbing(V) { return false; }\n";
     s += "  static __device__ __forceinline__ unsigned init(const ipr::ProgCtx& c, V* v, V* m) "
          "{ return ipr_init(c, v, m); }\n";
     s += "  static __device__ __forceinline__ unsigned compute(const ipr::ProgCtx& c, V* v, V mb, "

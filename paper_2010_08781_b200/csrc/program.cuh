@@ -389,7 +389,10 @@ struct ProgPull : ProgArgs<typename P::V> {
     using T = typename P::V;
     using C = ProgComb<T, P::kCombiner>;
     static constexpr bool kWeighted = true;
-    static constexpr bool kAbsorbing = false;
+    // optional ipr_absorbing(value): a vertex holding such a value ignores its messages, so its
+    // row need not be gathered (and whole ranges of such rows are skipped)
+    static constexpr bool kAbsorbing = P::kAbsorbing;
+    static constexpr bool kAbsorbingPartial = false;
     static constexpr bool kAggregates = P::kAggregates;
     __device__ void flush_aggregate(const LaneCounters& c) const {
         flush_prog_aggregate(c, this->agg_op, this->shared ? this->shared->agg : nullptr);
@@ -397,7 +400,11 @@ struct ProgPull : ProgArgs<typename P::V> {
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }
-    __device__ bool absorbed(int32_t) const { return false; }
+    __device__ bool absorbed(int32_t row) const {
+        if constexpr (P::kAbsorbing) return P::absorbing(this->value[row]);
+        return false;
+    }
+    __device__ bool absorbing(T) const { return false; }
     __device__ static T message(T g, uint32_t w) { return P::edge(g, w); }
     __device__ void finish(int32_t row, T m, LaneCounters& c) const {
         if (kPass == 1) {

@@ -120,7 +120,9 @@ struct MinU32 {
 // Ops whose result is settled once a row's partial reaches an absorbing value (Hash-Min: label
 // 0, the smallest id, cannot be lowered) stop gathering the rest of that row.
 struct NotAbsorbing {
-    static constexpr bool kAbsorbing = false;
+    static constexpr bool kAbsorbing = false;          // absorbed(row): the row is settled
+    static constexpr bool kAbsorbingPartial = false;   // absorbing(partial): so is a row whose
+                                                       // partial combine reaches this value
 };
 
 // ---- fused exchange ---------------------------------------------------------
@@ -202,6 +204,7 @@ struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
 struct CCPullIn : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
     static constexpr bool kAbsorbing = true;
+    static constexpr bool kAbsorbingPartial = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
     const uint32_t* __restrict__ cur;   // replica, global ids
     uint32_t* __restrict__ next;        // replica, global ids (owned slice written)
@@ -222,6 +225,7 @@ struct CCPullIn : MinU32, NoAggregate {
 struct CCPullOut : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
     static constexpr bool kAbsorbing = true;
+    static constexpr bool kAbsorbingPartial = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
@@ -260,6 +264,7 @@ struct CCPullOut : MinU32, NoAggregate {
 struct SSSPPull : MinU32, NoAggregate {
     static constexpr bool kWeighted = true;
     static constexpr bool kAbsorbing = true;
+    static constexpr bool kAbsorbingPartial = true;
     const uint32_t* __restrict__ cur;
     uint32_t* __restrict__ next;
     const int32_t* __restrict__ out_off;  // owned CSR offsets
@@ -473,7 +478,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         if (!part_head && (r >= x1 || Ec > e0 + kChunk)) {
             // fast path: the whole chunk belongs to row r (no row ends here)
             la = Op::combine(la, Op::combine(Op::combine(v[0], v[1]), Op::combine(v[2], v[3])));
-            if constexpr (Op::kAbsorbing) {
+            if constexpr (Op::kAbsorbingPartial) {
                 // the open row's partial reached the absorbing value: skip its remaining gathers
                 if (!absorbed) absorbed = __any_sync(kFull, op.absorbing(la));
             }
@@ -556,7 +561,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         absorbed = r < x1 && op.absorbed(r);
         if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
         carry = next_carry;
-        if constexpr (Op::kAbsorbing) {
+        if constexpr (Op::kAbsorbingPartial) {
             if (!absorbed && r < x1) absorbed = op.absorbing(carry);   // carry is warp-uniform
         }
         __syncwarp();

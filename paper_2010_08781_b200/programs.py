@@ -47,6 +47,8 @@ __device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbo
     return 0;                                              // ip_vote_to_halt
 }
 __device__ unsigned ipr_edge(unsigned message, unsigned) { return message; }
+// hint: label 0 (the smallest id) cannot be lowered, so such vertices need not gather
+__device__ bool ipr_absorbing(unsigned value) { return value == 0u; }
 """
 
 # Fig. 10 (PAPER.md:372-396) with u32 edge weights (DESIGN.md reading R8): params[0] = source.
