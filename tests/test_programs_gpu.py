@@ -266,3 +266,61 @@ def test_typed_programs(mode, parts):
     G.run_program(prog("min_neg_label_i64"), mode=mode)
     np.testing.assert_array_equal(G.values(host=True), -np.array(checkers.cc_max_label(n, e2), np.int64))
     G.close()
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("n", [1, 17])
+@pytest.mark.parametrize("parts", [1, 3])
+def test_programs_on_edgeless_graphs(n, parts):
+    if parts > n:
+        pytest.skip("more partitions than vertices")
+    e = np.zeros(0, np.int64)
+    G = make_graph(csr_csc(n, e, e), partitions=parts, weighted=False)
+    for mode in ("pull", "push", "auto"):
+        G.run_program(prog("hashmin_cc"), mode=mode)
+        np.testing.assert_array_equal(G.values(host=True), oracle.hashmin_cc(n, e, e)["values"])
+        G.run_program(prog("pagerank"), params=[10], mode=mode)
+        o = oracle.pagerank(n, e, e, k=10)
+        assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
+        assert G.stats()["supersteps"] == o["supersteps"]
+        G.run_program(prog("heap_children_sum"), mode=mode)
+        ids = np.arange(n)
+        want = np.where(2 * ids + 1 < n, 2 * ids + 1, 0) + np.where(2 * ids + 2 < n, 2 * ids + 2, 0)
+        np.testing.assert_array_equal(G.values(host=True).astype(np.int64), want)
+    G.close()
+
+
+def test_program_guard_with_sends_and_aggregate_counts():
+    # sends count as messages for termination: a chain of point-to-point hand-offs
+    import paper_2010_08781_b200 as ipr
+    src = r"""
+__device__ unsigned ipr_init(const ipr_ctx& c, unsigned* value, unsigned*) {
+    *value = 0;
+    if (c.id == 0) ipr_send(c, 1, 1u);
+    return 0;
+}
+__device__ unsigned ipr_compute(const ipr_ctx& c, unsigned* value, unsigned mailbox, unsigned*) {
+    if (mailbox) {                       // got the token: keep it, pass it on
+        *value = mailbox;
+        ipr_send(c, c.id + 1, mailbox + 1);
+        ipr_aggregate(c, 1.0);
+    }
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned m, unsigned) { return m; }
+"""
+    p = ipr.Program(src, "u32", "sum", aggregator="sum")
+    n = 50
+    e = np.zeros(0, np.int64)
+    for parts in (1, 4):
+        G = make_graph(csr_csc(n, e, e), partitions=parts, weighted=False)
+        G.run_program(p, mode="push")
+        v = G.values(host=True)
+        np.testing.assert_array_equal(v, np.concatenate([[0], np.arange(1, n)]))
+        s = G.stats()
+        assert s["supersteps"] == n            # the token visits every vertex, then stops
+        assert list(s["messages"][:-1]) == [1] * (n - 1)
+        st = G.run_program(p, mode="pull", max_supersteps=10, allow_guard=True)
+        assert st == ipr.ERR_MAX_SUPERSTEPS
+        G.close()
