@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--sample-scale", type=int, default=SAMPLE_SCALE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", action="store_true",
+                    help="use the NCCL communicator path even on one rank (tests the N>1 path)")
     args = ap.parse_args()
     args.apps = [a for a in args.apps.split(",") if a]
 
@@ -265,10 +267,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     ipr.device_check(local)
-    if world > 1:
+    use_comm = world > 1 or args.comm
+    if use_comm:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     g, part, bounds = build_graph_device(args.config, rank, world)
-    comm = ipr.Comm.from_process_group(local) if world > 1 else None
+    comm = ipr.Comm.from_process_group(local) if use_comm else None
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         G = ipr.Graph(part, comm=comm, stream=stream)
@@ -321,6 +324,7 @@ def main():
         apps_out[app] = {"gteps": d / (t_app * 1e-3) / 1e9, "ms": t_app,
                          "supersteps": int(st0["supersteps"]),
                          "modes": "".join("ilpr"[m] for m in st0["mode"]),
+                         "exchange": st0.get("exchange"),
                          # per superstep (first timed step): device ms, messages sent, model bytes
                          "superstep_ms": [round(float(x), 4) for x in st0["time_ms"]],
                          "superstep_messages": [int(x) for x in st0["messages"]],
@@ -376,7 +380,7 @@ def main():
     G.close()
     if comm:
         comm.close()
-    if world > 1:
+    if use_comm:
         dist.destroy_process_group()
 
 
