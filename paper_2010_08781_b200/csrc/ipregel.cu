@@ -235,6 +235,7 @@ struct Partition {
     bool push_view_ready = false;
     int64_t nondangling = 0;
     DeviceBuffers graph_mem;      // host copies, tile plans, push view
+    cudaEvent_t up_idx = nullptr, up_w = nullptr, up_all = nullptr;   // host-upload progress
     AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
@@ -267,6 +268,7 @@ struct ipregel_graph {
     int64_t w_min = -1;            // smallest edge weight (SSSP absorption bound), lazily
     const int32_t* inv_ids = nullptr;   // original -> internal id (user programs' ipr_send)
     cudaStream_t capture_stream = nullptr;   // private stream for CUDA-graph capture
+    cudaStream_t copy_stream = nullptr;      // host -> device uploads (MEMORY_HOST create)
     // PageRank (fixed k, pull) captured once as a CUDA graph and replayed: one launch per run
     struct {
         bool valid = false;
@@ -581,7 +583,8 @@ void exscan_i32(int32_t* a, int64_t n, DeviceBuffers& tmp, cudaStream_t s) {
 // transposed adjacency combines with min, or with a sum that is order-nondeterministic anyway).
 void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* idx,
                     const uint32_t* w, int64_t edges, bool want_w, cudaStream_t s,
-                    int32_t** out_off, int32_t** out_idx, uint32_t** out_w) {
+                    int32_t** out_off, int32_t** out_idx, uint32_t** out_w,
+                    cudaEvent_t w_ready = nullptr) {
     int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
     int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
     uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
@@ -595,7 +598,7 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
         unsigned long long* v0 = tmp.alloc<unsigned long long>(edges, s);
         unsigned long long* v1 = tmp.alloc<unsigned long long>(edges, s);
         CU(cudaMemcpyAsync(k0, idx, edges * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        k_transpose_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, w, p.rows, p.vb, v0);
+        k_transpose_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, p.rows, p.vb, v0);
         LAUNCH_CHECK();
         cub::DoubleBuffer<int32_t> keys(k0, k1);
         cub::DoubleBuffer<unsigned long long> vals(v0, v1);
@@ -605,8 +608,9 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
         CU(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, vals, edges, 0, bits, s));
         void* temp = tmp.alloc<uint8_t>((int64_t)temp_bytes, s);
         CU(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, edges, 0, bits, s));
+        if (w_ready) CU(cudaStreamWaitEvent(s, w_ready, 0));   // weights uploaded meanwhile
         k_transpose_unpack<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
-            vals.Current(), edges, ix, wx);
+            vals.Current(), edges, w, ix, wx);
         LAUNCH_CHECK();
         // offsets from the sorted sources: run lengths, then an exclusive scan
         int32_t* st = tmp.alloc<int32_t>(n, s, true);
@@ -1483,19 +1487,46 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
     p.rows = p.ve - p.vb;
     p.csc_edges = d.csc_edges;
     p.csr_edges = d.csr_edges;
+    const bool derive = !d.csr_offsets && !d.csr_indices;
     if (d.memory == IPREGEL_MEMORY_HOST) {
-        auto up = [&](const void* src, size_t bytes) -> void* {
-            if (!src) return nullptr;
-            void* dst = p.graph_mem.alloc<uint8_t>((int64_t)bytes, s);
-            CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-            return dst;
+        // uploads run on a copy stream in the order the device work needs them: the CSC
+        // offsets and indices first (the derived CSR's sort starts as soon as they land), then
+        // the weights (needed only by the sort's last pass) and the rest
+        if (!g->copy_stream) CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = g->copy_stream;
+        auto alloc = [&](const void* src, size_t bytes) -> void* {
+            return src ? (void*)p.graph_mem.alloc<uint8_t>((int64_t)bytes, s) : nullptr;
         };
-        p.csc_off = (const int32_t*)up(d.csc_offsets, (p.rows + 1) * 4);
-        p.csc_idx = (const int32_t*)up(d.csc_indices, d.csc_edges * 4);
-        p.csc_w = (const uint32_t*)up(d.csc_weights, d.csc_edges * 4);
-        p.csr_off = (const int32_t*)up(d.csr_offsets, (p.rows + 1) * 4);
-        p.csr_idx = (const int32_t*)up(d.csr_indices, d.csr_edges * 4);
-        p.csr_w = (const uint32_t*)up(d.csr_weights, d.csr_edges * 4);
+        void* off_d = alloc(d.csc_offsets, (p.rows + 1) * 4);
+        void* idx_d = alloc(d.csc_indices, d.csc_edges * 4);
+        void* w_d = alloc(d.csc_weights, d.csc_edges * 4);
+        void* roff_d = alloc(d.csr_offsets, (p.rows + 1) * 4);
+        void* ridx_d = alloc(d.csr_indices, d.csr_edges * 4);
+        void* rw_d = alloc(d.csr_weights, d.csr_edges * 4);
+        for (cudaEvent_t* e : {&p.up_idx, &p.up_w, &p.up_all})
+            if (!*e) CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CU(cudaEventRecord(p.up_all, s));              // the allocations, in stream order
+        CU(cudaStreamWaitEvent(cs, p.up_all, 0));
+        auto up = [&](void* dst, const void* src, size_t bytes) {
+            if (src) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs));
+        };
+        up(off_d, d.csc_offsets, (p.rows + 1) * 4);
+        up(idx_d, d.csc_indices, d.csc_edges * 4);
+        CU(cudaEventRecord(p.up_idx, cs));
+        up(w_d, d.csc_weights, d.csc_edges * 4);
+        CU(cudaEventRecord(p.up_w, cs));
+        up(roff_d, d.csr_offsets, (p.rows + 1) * 4);
+        up(ridx_d, d.csr_indices, d.csr_edges * 4);
+        up(rw_d, d.csr_weights, d.csr_edges * 4);
+        CU(cudaEventRecord(p.up_all, cs));
+        // validation reads every array; otherwise only a derived CSR starts early
+        CU(cudaStreamWaitEvent(s, (d.validate || !derive) ? p.up_all : p.up_idx, 0));
+        p.csc_off = (const int32_t*)off_d;
+        p.csc_idx = (const int32_t*)idx_d;
+        p.csc_w = (const uint32_t*)w_d;
+        p.csr_off = (const int32_t*)roff_d;
+        p.csr_idx = (const int32_t*)ridx_d;
+        p.csr_w = (const uint32_t*)rw_d;
     } else {
         p.csc_off = d.csc_offsets; p.csc_idx = d.csc_indices; p.csc_w = d.csc_weights;
         p.csr_off = d.csr_offsets; p.csr_idx = d.csr_indices; p.csr_w = d.csr_weights;
@@ -1533,12 +1564,14 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         int32_t *o, *ix;
         uint32_t* wx = nullptr;
         transpose_rows(p, g->n, p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, s,
-                       &o, &ix, &wx);
+                       &o, &ix, &wx, d.memory == IPREGEL_MEMORY_HOST ? p.up_w : nullptr);
         p.csr_off = o;
         p.csr_idx = ix;
         p.csr_w = wx;
         p.csr_edges = p.csc_edges;
     }
+    if (d.memory == IPREGEL_MEMORY_HOST)
+        CU(cudaStreamWaitEvent(s, p.up_all, 0));   // every upload resident before any run
     p.pull_cnt = p.graph_mem.alloc<PullCounters>(1, s, true);
     p.dscratch = p.graph_mem.alloc<unsigned long long>(64, s, true);
     p.front_cnt = p.graph_mem.alloc<FrontierCounters>(1, s, true);
@@ -1575,11 +1608,14 @@ void destroy_graph(ipregel_graph* g) {
             S.mem.release();
         }
         p.graph_mem.release();
+        for (cudaEvent_t e : {p.up_idx, p.up_w, p.up_all})
+            if (e) cudaEventDestroy(e);
         if (p.host_cnt) cudaFreeHost(p.host_cnt);
         p.host_cnt = nullptr;
     }
     if (g->pr_graph.exec) cudaGraphExecDestroy(g->pr_graph.exec);
     if (g->capture_stream) cudaStreamDestroy(g->capture_stream);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
     for (auto e : g->events) cudaEventDestroy(e);
     g->graph_mem.release();
     cudaStreamSynchronize(g->stream);

@@ -175,17 +175,18 @@ __global__ void k_validate_indices(const int32_t* __restrict__ idx, int64_t edge
 // CSC rows (u -> v) and, for CC, the owned CSR rows reversed (u <- v taken as u -> v).
 // Sort-based transpose (coalesced writes; an atomic-cursor scatter writes 4-byte words at
 // random, which costs ~7x the bytes in DRAM read-modify-write): every edge becomes a
-// (source, row | weight << 32) pair, a stable LSD radix sort by source groups the pairs into
-// the transposed rows with their destinations ascending (the input is in row order), and the
-// unpack writes indices and weights contiguously.
-__global__ void k_transpose_pack(const int32_t* __restrict__ off, const uint32_t* __restrict__ w,
-                                 int64_t rows, int64_t vbase, unsigned long long* __restrict__ vals) {
+// (source, row | edge << 32) pair, a stable LSD radix sort by source groups the pairs into the
+// transposed rows with their destinations ascending (the input is in row order), and the unpack
+// writes the indices contiguously and fetches each weight by its edge index -- so the weights
+// are needed only at the very end (the host upload of them overlaps the sort).
+__global__ void k_transpose_pack(const int32_t* __restrict__ off, int64_t rows, int64_t vbase,
+                                 unsigned long long* __restrict__ vals) {
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
     const unsigned long long v = (unsigned long long)(uint32_t)(vbase + r);
     for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32)
-        vals[e] = v | ((unsigned long long)(w ? w[e] : 1u) << 32);
+        vals[e] = v | ((unsigned long long)(uint32_t)e << 32);
 }
 
 // Run boundaries of the sorted sources: start[k] = first position of source k, end[k] = one past
@@ -206,12 +207,13 @@ __global__ void k_run_counts(const int32_t* __restrict__ start, int64_t n,
 }
 
 __global__ void k_transpose_unpack(const unsigned long long* __restrict__ vals, int64_t edges,
-                                   int32_t* __restrict__ out_idx, uint32_t* __restrict__ out_w) {
+                                   const uint32_t* __restrict__ w, int32_t* __restrict__ out_idx,
+                                   uint32_t* __restrict__ out_w) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
          i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long x = vals[i];
         out_idx[i] = (int32_t)(uint32_t)x;
-        if (out_w) out_w[i] = (uint32_t)(x >> 32);
+        if (out_w) out_w[i] = w ? __ldg(w + (uint32_t)(x >> 32)) : 1u;
     }
 }
 
