@@ -32,6 +32,9 @@
  *   - A CUDA or NCCL failure poisons the handle: later calls on it return
  *     IPREGEL_ERR_STATE.  Only ipregel_graph_destroy remains valid.
  *   - One host thread at a time per handle.
+ *   - Library-owned device memory comes from the device's default stream-ordered pool
+ *     (cudaMallocAsync); freed memory is kept for later graphs up to IPREGEL_POOL_RETAIN_BYTES
+ *     (environment, default 96 GiB), so creating and destroying graphs stays cheap.
  */
 #ifndef IPREGEL_H
 #define IPREGEL_H
