@@ -591,16 +591,30 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_r
     if constexpr (Op::kAggregates) op.flush_aggregate(cnt);
 }
 
-// Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.
+// Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A
+// thread takes kPrFinishRows rows (block-strided, coalesced) with their sums loaded up front.
+constexpr int kPrFinishRows = 4;
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
     __shared__ unsigned long long s_cnt[4];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
+    if (counters && threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     LaneCounters c{0u, 0u, 0u, 0ull};
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row < rows) op.finish((int32_t)row, op.contrib_next[op.vbase + row], c);
-    flush_counters(c, s_cnt, counters);
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kPrFinishRows + threadIdx.x;
+    double sum[kPrFinishRows];
+#pragma unroll
+    for (int j = 0; j < kPrFinishRows; ++j) {
+        const int64_t row = base + (int64_t)j * blockDim.x;
+        sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kPrFinishRows; ++j) {
+        const int64_t row = base + (int64_t)j * blockDim.x;
+        if (row < rows) op.finish((int32_t)row, sum[j], c);
+    }
+    if (counters) {   // to-convergence runs only (grid-uniform)
+        __syncthreads();
+        flush_counters(c, s_cnt, counters);
+    }
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is

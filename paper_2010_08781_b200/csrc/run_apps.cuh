@@ -135,8 +135,8 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                     sop.vbase = p.vb;
                     launch_pull(sop, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
                                 g->gather_policy, g->degree_ordered);
-                    k_pr_finish<<<grid_for(p.rows, 256), 256, 0, s>>>(op, p.rows,
-                                                                      track ? p.pull_cnt : nullptr);
+                    k_pr_finish<<<grid_for(ceil_div(p.rows, kPrFinishRows), 256), 256, 0, s>>>(
+                        op, p.rows, track ? p.pull_cnt : nullptr);
                     LAUNCH_CHECK();
                 } else {
                     launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr,
