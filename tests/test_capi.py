@@ -101,3 +101,21 @@ def test_library_fails_loudly_without_gpu():
     st = ipr.load().ipregel_device_check(0)
     assert st in (ipr.ERR_CUDA, ipr.ERR_UNSUPPORTED)
     assert ipr.last_error()
+
+
+def test_product_path_never_imports_the_oracle():
+    """The oracle is test infrastructure: the package (and its program catalog) must not import
+    it, and no product source mentions it as a module."""
+    import subprocess
+    import sys
+    code = ("import sys; import paper_2010_08781_b200, paper_2010_08781_b200.programs; "
+            "print('oracle' in sys.modules)")
+    out = subprocess.check_output([sys.executable, "-c", code],
+                                  cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.decode().strip() == "False"
+    pkg = os.path.join(os.path.dirname(__file__), "..", "paper_2010_08781_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(root, f)).read()
+                assert "import oracle" not in text and "oracle/" not in text, f
