@@ -87,6 +87,7 @@ struct ProgArgs {
     uint32_t* p2p_in_recv; //   and their recipient bitmap (NULL: the program never sends)
     double aggregate;      // the aggregator after the previous superstep
     int32_t agg_op;        // -1 none
+    int32_t pull_all;      // k_prog_apply after a pull: every vertex computes
     int64_t vbase, rows, n;
     uint32_t superstep;
     int32_t sym;
@@ -307,7 +308,7 @@ __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int6
     A.flags[row] = (uint8_t)((b ? 1u : 0u) | (act ? 2u : 0u));   // plain store, no atomics
     if (b) {
         c.changed += 1;
-        c.messages += (uint32_t)x.out_degree + (A.sym ? (uint32_t)x.in_degree : 0u);
+        c.messages += (uint32_t)x.out_degree + (P::kSym ? (uint32_t)x.in_degree : 0u);
     }
     c.aux += act ? 1ull : 0ull;
 }
@@ -393,10 +394,8 @@ struct ProgPull : ProgArgs<typename P::V> {
     // row need not be gathered (and whole ranges of such rows are skipped)
     static constexpr bool kAbsorbing = P::kAbsorbing;
     static constexpr bool kAbsorbingPartial = false;
-    static constexpr bool kAggregates = P::kAggregates;
-    __device__ void flush_aggregate(const LaneCounters& c) const {
-        flush_prog_aggregate(c, this->agg_op, this->shared ? this->shared->agg : nullptr);
-    }
+    static constexpr bool kAggregates = false;   // compute runs in k_prog_apply
+    __device__ void flush_aggregate(const LaneCounters&) const {}
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }
@@ -406,16 +405,12 @@ struct ProgPull : ProgArgs<typename P::V> {
     }
     __device__ bool absorbing(T) const { return false; }
     __device__ static T message(T g, uint32_t w) { return P::edge(g, w); }
-    __device__ void finish(int32_t row, T m, LaneCounters& c) const {
-        if (kPass == 1) {
-            this->mbox[row] = m;
-            return;
-        }
-        if (kPass == 2) {
-            m = C::combine(this->mbox[row], m);
-            this->mbox[row] = C::identity();
-        }
-        prog_vertex<P>(*this, row, m, c);
+    // The range kernels only fold each row's messages into its mailbox; the user's compute
+    // runs row-parallel in k_prog_apply (pull_all) -- the same split as the built-in PageRank,
+    // which keeps the gather loop free of the program's registers.
+    __device__ void finish(int32_t row, T m, LaneCounters&) const {
+        if (kPass == 2) m = C::combine(this->mbox[row], m);
+        this->mbox[row] = m;
     }
 };
 
@@ -473,6 +468,35 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     }
     __syncwarp();
     if (row < A.rows && (row & 31) == 0) A.recv[row >> 5] = 0u;
+    flush_counters(c, s_cnt, counters);
+    if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
+}
+
+// After a pull superstep: every vertex computes on the mailbox the range kernels folded (pull
+// selection, reading R28).  kProgPullRows rows per thread, block-strided, mailboxes loaded up
+// front.  The mailboxes are not reset here: the next pull overwrites them, and a switch to push
+// refills them with the identity first.
+constexpr int kProgPullRows = 4;
+template <class P>
+__global__ void __launch_bounds__(256) k_prog_pull_apply(ProgArgs<typename P::V> A,
+                                                         PullCounters* counters) {
+    using V = typename P::V;
+    __shared__ unsigned long long s_cnt[4];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    LaneCounters c{};
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kProgPullRows + threadIdx.x;
+    V m[kProgPullRows];
+#pragma unroll
+    for (int j = 0; j < kProgPullRows; ++j) {
+        const int64_t row = base + (int64_t)j * blockDim.x;
+        if (row < A.rows) m[j] = A.mbox[row];
+    }
+#pragma unroll
+    for (int j = 0; j < kProgPullRows; ++j) {
+        const int64_t row = base + (int64_t)j * blockDim.x;
+        if (row < A.rows) prog_vertex<P>(A, row, m[j], c);
+    }
+    __syncthreads();
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }

@@ -6,7 +6,7 @@
 // user vertex programs: NVRTC compilation and the generic superstep loop
 // =============================================================================================
 enum { PK_INIT, PK_PULL0, PK_PULL1, PK_PULL2, PK_FIX0, PK_FIX1, PK_FIX2, PK_EXPAND, PK_APPLY,
-       PK_COUNT };
+       PK_PULL_APPLY, PK_COUNT };
 static const char* const kProgKernelNames[PK_COUNT] = {
     "ipr::k_prog_init<UserProgram>",
     "ipr::k_pull_ranges<ipr::ProgPull<UserProgram, 0> >",
@@ -17,6 +17,7 @@ static const char* const kProgKernelNames[PK_COUNT] = {
     "ipr::k_pull_fixup<ipr::ProgPull<UserProgram, 2> >",
     "ipr::k_prog_expand<UserProgram>",
     "ipr::k_prog_apply<UserProgram>",
+    "ipr::k_prog_pull_apply<UserProgram>",
 };
 
 struct ipregel_program {
@@ -113,6 +114,7 @@ std::string program_tu(const ipregel_program_desc& d) {
     s += "\n#line 1 \"ipregel_program_adapter\"\n";
     s += "struct UserProgram {\n  typedef ipr_value_t V;\n";
     s += "  static constexpr int kCombiner = " + std::to_string(d.combiner) + ";\n";
+    s += std::string("  static constexpr bool kSym = ") + (d.symmetric ? "true" : "false") + ";\n";
     s += std::string("  static constexpr bool kSends = ") +
          (strstr(d.source, "ipr_send") ? "true" : "false") + ";\n";
     s += std::string("  static constexpr bool kAggregates = ") +
@@ -365,6 +367,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         a.p2p_in_recv = pr->sends ? S.pv_p2p_recv[(step & 1u) ^ 1u] : nullptr;
         a.aggregate = agg_prev;
         a.agg_op = pr->agg_op;
+        a.pull_all = 0;
         a.vbase = p.vb;
         a.rows = p.rows;
         a.n = n;
@@ -408,6 +411,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
     g->steps[0].messages = messages;
     g->steps[0].model_bytes = (uint64_t)n * sizeof(V);
     int cur = 0;
+    int prev_mode = 0;
     ipregel_status status = IPREGEL_OK;
 
     for (uint32_t step = 1; messages > 0 || active > 0; ++step) {
@@ -423,6 +427,14 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
         reset_extras();
         if (mode == 2) {
+            if (prev_mode == 1) {   // a pull left folded mailboxes behind: back to the identity
+                for (auto& p : g->parts) {
+                    if (!p.rows) continue;
+                    k_fill_u64<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                        static_cast<uint64_t*>(p.st[app].pv_mbox), p.rows, ident, (int)sizeof(V));
+                    LAUNCH_CHECK();
+                }
+            }
             // frontier = the broadcasters of superstep s-1 (flag bytes -> bitmap -> ids)
             for (auto& p : g->parts) {
                 if (p.rows) {
@@ -471,6 +483,14 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
                                            p.pull_cnt);
                 }
             }
+            // every vertex computes on its folded mailbox (pull selection, reading R28)
+            for (auto& p : g->parts) {
+                ProgArgs<V> a = args_for(p, step, cur);
+                PullCounters* cnt = p.pull_cnt;
+                void* args[] = {&a, &cnt};
+                launch_jit(pr->k[PK_PULL_APPLY], grid_for(ceil_div(p.rows, kProgPullRows), 256),
+                           256, args, s);
+            }
             T.kend();
         }
         exchange(1 - cur);
@@ -491,6 +511,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         R.changed = changed;
         R.messages = messages;
         cur = 1 - cur;
+        prev_mode = mode;
     }
     g->cur = cur;
     finalize_times(g);
