@@ -410,7 +410,29 @@ __device__ __forceinline__ typename Op::T warp_fold(typename Op::T x) {
     return x;
 }
 
-// One warp, one range q (see the file header).  `my_sum` is the warp's 128-slot sum array.
+// Two lane-private partials reduced at once (results on every lane): the first xor step
+// pairs a over the low half-warp and b over the high one, so both take 5 + 2 shuffles
+// instead of 2 x 5.  The one-end chunks and the general ones close the first and last
+// segments of a chunk with this same tree (bit-identical partitioned views).
+template <class Op>
+__device__ __forceinline__ void warp_fold2(typename Op::T a, typename Op::T b,
+                                           typename Op::T& fa, typename Op::T& fb) {
+    using T = typename Op::T;
+    const int lane = threadIdx.x & 31;
+    const bool hi = lane & 16;
+    const T o = shfl_xor(hi ? a : b, 16);
+    T x = hi ? Op::combine(o, b) : Op::combine(a, o);
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        const T y = shfl_xor(x, d);
+        x = (lane & d) ? Op::combine(y, x) : Op::combine(x, y);
+    }
+    fa = shfl_idx(x, 0);
+    fb = shfl_idx(x, 16);
+}
+
+// One warp, one range q (see the file header).  `my_sum` is the warp's sum array: 128 slots
+// by chunk position + 2 for the first / last segment of 8-byte chunks.
 template <class Op>
 __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int64_t q,
                                            typename Op::T* my_sum, LaneCounters& cnt) {
@@ -498,8 +520,10 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
                 if (32 * k + lane < p) t1 = Op::combine(t1, v[k]);
                 else t2 = Op::combine(t2, v[k]);
             }
-            const T total = Op::combine(Op::combine(carry, warp_fold<Op>(la)), warp_fold<Op>(t1));
-            carry = warp_fold<Op>(t2);
+            T f1, f2;
+            warp_fold2<Op>(t1, t2, f1, f2);
+            const T total = Op::combine(Op::combine(carry, warp_fold<Op>(la)), f1);
+            carry = f2;
             la = Op::identity();
             if (lane == 0) {
                 if (r == defer) static_cast<T*>(A.head_out)[q] = total;
@@ -523,6 +547,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         uint32_t f[4] = {0u, 0u, 0u, 0u};
         int32_t n_emit = 0;
         int32_t E0 = 0;   // window 0's row end for this lane (reused by the emission)
+        int32_t pl = -e0;  // last row end in the chunk (the partition start if none)
         for (int32_t rw = r;; rw += 32) {
             const int32_t row = rw + lane;
             const int32_t E = row < x1 ? A.off[row + 1] : INT_MAX;
@@ -534,12 +559,37 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
 #pragma unroll
             for (int k = 0; k < 4; ++k) f[k] |= __reduce_or_sync(kFull, word == k ? bit : 0u);
             const int n = __popc(__ballot_sync(kFull, p <= kChunk));
+            if (sizeof(T) == 8 && n > 0) pl = shfl_idx(p, n - 1);
             n_emit += n;
             if (n < 32) break;
         }
         if (part_head) {
             const int p = -e0;   // in [1, 127]
             f[p >> 5] |= 1u << (p & 31);
+        }
+        if constexpr (sizeof(T) == 8) {
+            // the first segment (the open row r, unless the partition starts in this chunk) and
+            // the last one (the row running past the chunk) are closed with the same masked
+            // folds as the one-end chunks above; only rows wholly inside the chunk use the
+            // scan.  Each row's combine tree then depends on its own ends only, not on how
+            // many other rows end in the chunk -- which differs between a partition's view and
+            // the whole graph's at partition boundaries -- so any partitioning reduces every
+            // row bit-identically (E4)
+            const int32_t p1 = part_head ? 0 : Ec - e0;
+            T t1 = Op::identity(), t2 = Op::identity();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t pos = 32 * k + lane;
+                if (pos < p1) t1 = Op::combine(t1, v[k]);
+                else if (pos >= pl) t2 = Op::combine(t2, v[k]);
+            }
+            T f1, f2;
+            warp_fold2<Op>(t1, t2, f1, f2);
+            if (lane == 0) {
+                my_sum[4 * 32] = Op::combine(carry, f1);
+                my_sum[4 * 32 + 1] = f2;
+            }
+            carry = Op::identity();
         }
 
         // segmented scan over positions 0..127: 4 independent warp scans (segment starts from
@@ -579,7 +629,8 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
                 T val = Op::identity();
                 if (B < E) {
                     const int pos = E - e0 - 1;
-                    val = pos >= 0 ? my_sum[pos] : Op::identity();
+                    val = pos >= 0 ? my_sum[(sizeof(T) == 8 && k + lane == 0 && !part_head)
+                                                ? 4 * 32 : pos] : Op::identity();
                     if (E - e0 == kChunk) ended_at_end = true;
                 }
                 if (row == defer) static_cast<T*>(A.head_out)[q] = val;
@@ -592,7 +643,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         En = r + 1 < A.rows ? A.off[r + 2] : INT_MAX;
         absorbed = r < x1 && op.absorbed(r);
         if (__any_sync(kFull, ended_at_end)) next_carry = Op::identity();
-        carry = next_carry;
+        carry = sizeof(T) == 8 ? my_sum[4 * 32 + 1] : next_carry;
         if constexpr (Op::kAbsorbingPartial) {
             if (!absorbed && r < x1) absorbed = op.absorbing(carry);   // carry is warp-uniform
         }
@@ -611,7 +662,7 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
 template <class Op>
 __global__ void __launch_bounds__(kPullThreads, IPREGEL_PULL_MINBLOCKS) k_pull_ranges(Op op, RangeArgs A) {
     using T = typename Op::T;
-    __shared__ T s_sum[kWarpsPerCta][4 * 32];   // chunk sums by position (conflict-free)
+    __shared__ T s_sum[kWarpsPerCta][4 * 32 + 2];   // chunk sums by position (conflict-free)
     __shared__ unsigned long long s_cnt[4];
     const int wid = threadIdx.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;

@@ -661,3 +661,31 @@ def test_pagerank_graph_replay_matches_first_run():
     st = G.run("pagerank", mode="pull", iterations=10, max_supersteps=5, allow_guard=True)
     assert st == ipr.ERR_MAX_SUPERSTEPS and G.stats()["supersteps"] == 5
     G.close()
+
+
+@pytest.mark.parametrize("exchange", ["fused", "collective"])
+def test_pagerank_pull_bit_identical_random_bounds(exchange):
+    """PageRank pull sums of many terms (rows of 0..400 in-edges, so chunks hold zero, one or
+    many row ends) are bit-identical between one partition and four partitions at random
+    bounds: every row's combine tree depends on its own edge positions on the global 128-edge
+    grid only (E4), whatever rows the partition boundaries cut off a chunk."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    kind = rng.integers(0, 3, n)
+    deg = np.where(kind == 0, rng.integers(0, 6, n),
+                   np.where(kind == 1, rng.integers(6, 100, n), rng.integers(100, 400, n)))
+    dst = np.repeat(np.arange(n), deg)
+    src = rng.integers(0, n, len(dst))
+    keep = src != dst
+    g = csr_csc(n, src[keep], dst[keep])
+    G1 = make_graph(g, weighted=False)
+    G1.run("pagerank", mode="pull")
+    v1 = G1.values(host=True)
+    G1.close()
+    for _ in range(12):
+        b = np.sort(rng.choice(np.arange(1, n), 3, replace=False))
+        bounds = np.concatenate([[0], b, [n]])
+        Gp = make_graph(g, partitions=4, weighted=False, bounds=bounds)
+        Gp.run("pagerank", mode="pull", exchange=exchange)
+        np.testing.assert_array_equal(Gp.values(host=True), v1, err_msg=str(bounds.tolist()))
+        Gp.close()
