@@ -395,6 +395,11 @@ struct ProgPull : ProgArgs<typename P::V> {
     static constexpr bool kAbsorbing = P::kAbsorbing;
     static constexpr bool kAbsorbingPartial = false;
     static constexpr bool kAggregates = false;   // compute runs in k_prog_apply
+    // 8-byte values: 3 CTAs per SM, as PageRankSum (PageRank program 79.7 -> 78.4 ms at cfg4)
+#ifndef IPREGEL_PROG_MINBLOCKS8
+#define IPREGEL_PROG_MINBLOCKS8 3
+#endif
+    static constexpr int kMinBlocks = sizeof(T) == 8 ? IPREGEL_PROG_MINBLOCKS8 : IPREGEL_PULL_MINBLOCKS;
     __device__ void flush_aggregate(const LaneCounters&) const {}
     __device__ static T identity() { return C::identity(); }
     __device__ static T combine(T a, T b) { return C::combine(a, b); }

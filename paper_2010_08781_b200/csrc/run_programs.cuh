@@ -146,8 +146,12 @@ void compile_program(ipregel_program* pr, const ipregel_program_desc& d) {
     // IEEE arithmetic as written (no FMA contraction), the oracle's convention (R7)
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
                           "-default-device", "--ptxas-options=-v",
-                          "-DIPREGEL_JIT=1"};
-    r = N.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+                          "-DIPREGEL_JIT=1", nullptr};
+    // tuning knob: one extra NVRTC option (e.g. -DIPREGEL_PROG_MINBLOCKS8=3)
+    const char* extra = getenv("IPREGEL_NVRTC_OPT");
+    int nopts = (int)(sizeof(opts) / sizeof(opts[0])) - 1;
+    if (extra && *extra) opts[nopts++] = extra;
+    r = N.compile(prog, nopts, opts);
     size_t ls = 0;
     N.log_size(prog, &ls);
     std::string log(ls, '\0');
