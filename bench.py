@@ -422,16 +422,18 @@ def e2e_measure(g, args, msgs_per_step, stream):
     one()  # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for _ in range(steps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
         one()
-    stop.record(stream)
+        ev[i + 1].record(stream)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps
-    ms = start.elapsed_time(stop) / steps
+    each = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    ms = ev[0].elapsed_time(ev[steps]) / steps
     return {"value": msgs_per_step / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "wall_ms_per_step": wall * 1e3,
+            "ms_each_step": [round(x, 2) for x in each],
             "steps": steps,
             "path": "ipregel_graph_create(IPREGEL_MEMORY_HOST, pinned CSC + weights + vertex ids; "
                     "CSR derived on the device) + ipregel_run x apps + ipregel_get_values(host) + "

@@ -39,6 +39,22 @@ void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
     *n_out = d->num_vertices;
 }
 
+__global__ void k_noop() {}
+
+// Measured on B200 (tools/lab/stream_wait_lab3.cu): once a stream's latest operation is a host ->
+// device copy, a cross-stream wait issued on it next is released only after the OTHER stream's
+// queued copies finish too (it sits behind them on the copy engine) -- here that would hold the
+// derived CSR's sort and the weight windows until the whole upload ends.  An empty kernel first
+// puts the wait back on the compute queue.
+void compute_fence(cudaStream_t s) {
+    k_noop<<<1, 32, 0, s>>>();
+    LAUNCH_CHECK();
+}
+
+// windows of the CSC weights' upload when the CSR is derived (the last window's permutation is
+// all that remains after the upload)
+constexpr int kWeightWindows = 8;
+
 void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
     cudaStream_t s = g->stream;
     p.vb = d.vertex_begin;
@@ -47,10 +63,12 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
     p.csc_edges = d.csc_edges;
     p.csr_edges = d.csr_edges;
     const bool derive = !d.csr_offsets && !d.csr_indices;
+    p.host_cnt = static_cast<unsigned long long*>(pinned_acquire(16 * sizeof(unsigned long long)));
     if (d.memory == IPREGEL_MEMORY_HOST) {
-        // uploads run on a copy stream in the order the device work needs them: the CSC
-        // offsets and indices first (the derived CSR's sort starts as soon as they land), then
-        // the weights (needed only by the sort's last pass) and the rest
+        // uploads run on a copy stream in the order the device work needs them: the adjacency
+        // structure first (validation, the derived CSR's sort and the tile plans start as soon
+        // as it lands), then the weights -- in windows when the CSR is derived, each window's
+        // share of the weight permutation running while the next one uploads (finish_uploads)
         if (!g->copy_stream) CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
         cudaStream_t cs = g->copy_stream;
         auto alloc = [&](const void* src, size_t bytes) -> void* {
@@ -69,17 +87,35 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         auto up = [&](void* dst, const void* src, size_t bytes) {
             if (src) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs));
         };
+        g_ctrace.mark("uploads begin", cs);
         up(off_d, d.csc_offsets, (p.rows + 1) * 4);
         up(idx_d, d.csc_indices, d.csc_edges * 4);
-        CU(cudaEventRecord(p.up_idx, cs));
-        up(w_d, d.csc_weights, d.csc_edges * 4);
-        CU(cudaEventRecord(p.up_w, cs));
         up(roff_d, d.csr_offsets, (p.rows + 1) * 4);
         up(ridx_d, d.csr_indices, d.csr_edges * 4);
+        CU(cudaEventRecord(p.up_idx, cs));
+        g_ctrace.mark("uploaded structure", cs);
+        int windows = (derive && w_d && d.csc_edges >= (int64_t(1) << 24)) ? kWeightWindows : 1;
+        if (const char* e = getenv("IPREGEL_WEIGHT_WINDOWS"))   // test hook
+            if (derive && w_d) windows = std::max(1, std::min(atoi(e), 64));
+        p.wc_bounds.assign(1, 0);
+        for (int c = 0; c < windows; ++c) {
+            const int64_t lo = d.csc_edges * c / windows, hi = d.csc_edges * (c + 1) / windows;
+            if (w_d) up((uint32_t*)w_d + lo, (const uint32_t*)d.csc_weights + lo, (hi - lo) * 4);
+            cudaEvent_t e;
+            CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CU(cudaEventRecord(e, cs));
+            p.up_wc.push_back(e);
+            p.wc_bounds.push_back(hi);
+        }
+        CU(cudaEventRecord(p.up_w, cs));
+        g_ctrace.mark("uploaded csc w", cs);
         up(rw_d, d.csr_weights, d.csr_edges * 4);
         CU(cudaEventRecord(p.up_all, cs));
-        // validation reads every array; otherwise only a derived CSR starts early
-        CU(cudaStreamWaitEvent(s, (d.validate || !derive) ? p.up_all : p.up_idx, 0));
+        g_ctrace.mark("uploaded all", cs);
+        // validation and everything up to the weights need the structure only
+        compute_fence(s);   // s uploaded the vertex ids
+        CU(cudaStreamWaitEvent(s, p.up_idx, 0));
+        g_ctrace.mark("structure landed", s);
         p.csc_off = (const int32_t*)off_d;
         p.csc_idx = (const int32_t*)idx_d;
         p.csc_w = (const uint32_t*)w_d;
@@ -97,9 +133,10 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         if (p.csr_off)
             k_validate_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csr_off, p.rows, p.csr_edges, flags);
         LAUNCH_CHECK();
-        unsigned h = 0;
-        CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s));
+        unsigned* hf = reinterpret_cast<unsigned*>(p.host_cnt);
+        kernel_copy(hf, flags, 4, s);   // not a cudaMemcpy: see compute_fence
         CU(cudaStreamSynchronize(s));
+        unsigned h = *hf;
         if (h == 0) {
             if (p.csc_edges)
                 k_validate_indices<<<std::min<unsigned>(grid_for(p.csc_edges, 256), 4096), 256, 0, s>>>(
@@ -108,14 +145,16 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
                 k_validate_indices<<<std::min<unsigned>(grid_for(p.csr_edges, 256), 4096), 256, 0, s>>>(
                     p.csr_idx, p.csr_edges, g->n, flags);
             LAUNCH_CHECK();
-            CU(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s));
+            kernel_copy(hf, flags, 4, s);
             CU(cudaStreamSynchronize(s));
+            h = *hf;
         }
         if (h)
             fail(IPREGEL_ERR_INVALID_GRAPH, "graph validation failed (flags 0x%x: %s%s%s)", h,
                  (h & 1) ? "offsets[0]/offsets[rows] " : "", (h & 2) ? "non-monotone offsets " : "",
                  (h & 4) ? "index out of range" : "");
     }
+    g_ctrace.mark("validated", s);
     if (!d.csr_offsets && !d.csr_indices) {
         // out-adjacency (and its weights) derived from the CSC on the device: the transpose of
         // the whole graph's in-edges (single partition, checked by validate_desc;
@@ -123,43 +162,79 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         int32_t *o, *ix;
         uint32_t* wx = nullptr;
         transpose_rows(p, g->n, p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, s,
-                       &o, &ix, &wx, d.memory == IPREGEL_MEMORY_HOST ? p.up_w : nullptr);
+                       &o, &ix, &wx, d.memory == IPREGEL_MEMORY_HOST);
         p.csr_off = o;
         p.csr_idx = ix;
         p.csr_w = wx;
         p.csr_edges = p.csc_edges;
+        if (p.pend.perm) {
+            // permute each weight window as it lands, on a side stream (the run stream goes
+            // on with the tile plans); transpose_rows returned with perm complete
+            if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+            for (size_t c = 0; c + 1 < p.wc_bounds.size(); ++c) {
+                CU(cudaStreamWaitEvent(g->aux_stream, p.up_wc[c], 0));
+                k_permute_window<<<148 * 8, 256, 0, g->aux_stream>>>(
+                    p.pend.perm, p.pend.edges, p.wc_bounds[c], p.wc_bounds[c + 1], p.pend.w,
+                    p.pend.wx);
+                LAUNCH_CHECK();
+            }
+            CU(cudaEventCreateWithFlags(&p.perm_done, cudaEventDisableTiming));
+            CU(cudaEventRecord(p.perm_done, g->aux_stream));
+            g_ctrace.mark("weights permuted", g->aux_stream);
+        }
     }
-    if (d.memory == IPREGEL_MEMORY_HOST)
-        CU(cudaStreamWaitEvent(s, p.up_all, 0));   // every upload resident before any run
     p.pull_cnt = p.graph_mem.alloc<PullCounters>(1, s, true);
     p.dscratch = p.graph_mem.alloc<unsigned long long>(64, s, true);
     p.front_cnt = p.graph_mem.alloc<FrontierCounters>(1, s, true);
-    CU(cudaMallocHost(&p.host_cnt, 16 * sizeof(unsigned long long)));
     // PageRank broadcasters (out-degree > 0)
     unsigned long long* cnt = p.graph_mem.alloc<unsigned long long>(1, s, true);
     if (p.rows) {
         k_count_nondangling<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, cnt);
         LAUNCH_CHECK();
     }
-    unsigned long long h = 0;
-    CU(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+    kernel_copy(p.host_cnt, cnt, 8, s);   // not a cudaMemcpy: see compute_fence
     CU(cudaStreamSynchronize(s));
-    p.nondangling = (int64_t)h;
+    p.nondangling = (int64_t)p.host_cnt[0];
+    g_ctrace.mark("partition ready", s);
+}
+
+// The tail of a create from host memory, after the tile plans: the derived CSR's weights
+// permuted (aux stream, window by window as the windows landed), then every upload resident
+// before create returns (the caller may free its host arrays afterwards).
+void finish_uploads(ipregel_graph* g, Partition& p) {
+    cudaStream_t s = g->stream;
+    if (p.pend.perm) {
+        CU(cudaStreamWaitEvent(s, p.perm_done, 0));
+        p.pend.tmp.release();   // stream-ordered, after the permutation
+        p.pend.perm = nullptr;
+    }
+    if (p.up_all) CU(cudaStreamWaitEvent(s, p.up_all, 0));
 }
 
 void build_plans(ipregel_graph* g) {
     for (auto& p : g->parts) {
         build_plan(p.plan_csc, p.csc_off, p.csc_idx, p.csc_w, p.rows, p.csc_edges, p.vb,
-                   p.csc_ebase, p.graph_mem, g->stream);
+                   p.csc_ebase, p.graph_mem, g->stream, g->pinned);
         build_plan(p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.rows, p.csr_edges, p.vb,
-                   p.csr_ebase, p.graph_mem, g->stream);
+                   p.csr_ebase, p.graph_mem, g->stream, g->pinned);
     }
     CU(cudaStreamSynchronize(g->stream));
 }
 
 void destroy_graph(ipregel_graph* g) {
     if (!g) return;
+    auto t0 = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {   // IPREGEL_TRACE_CREATE: host time of each phase
+        if (!g_ctrace.on) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[ipregel destroy] %-22s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
     cudaStreamSynchronize(g->stream);
+    if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);   // a failed create's uploads
+    if (g->aux_stream) cudaStreamSynchronize(g->aux_stream);
+    tick("sync");
     for (auto& p : g->parts) {
         for (auto& S : p.st) {
             for (void* q : S.ipc_opened) cudaIpcCloseMemHandle(q);
@@ -169,15 +244,25 @@ void destroy_graph(ipregel_graph* g) {
         p.graph_mem.release();
         for (cudaEvent_t e : {p.up_idx, p.up_w, p.up_all})
             if (e) cudaEventDestroy(e);
-        if (p.host_cnt) cudaFreeHost(p.host_cnt);
+        for (cudaEvent_t e : p.up_wc) cudaEventDestroy(e);
+        if (p.perm_done) cudaEventDestroy(p.perm_done);
+        p.perm_done = nullptr;
+        p.up_wc.clear();
+        p.pend.tmp.release();
+        pinned_release(p.host_cnt);
         p.host_cnt = nullptr;
     }
+    tick("partition memory");
     if (g->pr_graph.exec) cudaGraphExecDestroy(g->pr_graph.exec);
     if (g->capture_stream) cudaStreamDestroy(g->capture_stream);
     if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+    if (g->aux_stream) cudaStreamDestroy(g->aux_stream);
     for (auto e : g->events) cudaEventDestroy(e);
+    tick("graph exec, streams");
     g->graph_mem.release();
+    g->pinned.release();
     cudaStreamSynchronize(g->stream);
+    tick("frees synchronised");
     delete g;
 }
 

@@ -1,6 +1,8 @@
 // paper_2010_08781_b200/csrc/engine.cuh -- errors, device memory, the graph and partition state, launch helpers, exchanges, frontier machinery, the fused exchange and per-superstep timing.
 // Host part of the single translation unit ipregel.cu (included once, in order).
 #pragma once
+#include <chrono>
+#include <mutex>
 
 // =============================================================================================
 // errors
@@ -143,6 +145,59 @@ struct DeviceBuffers {
     }
 };
 
+// Pinned host blocks, cached for the process: cudaMallocHost / cudaFreeHost cost milliseconds
+// (page pinning, a device synchronisation) and showed up as tens of ms of jitter per graph
+// create / destroy, so blocks go back to this cache instead of being freed.
+std::mutex g_pin_mu;
+std::vector<std::pair<void*, size_t>> g_pin_free;
+std::vector<std::pair<void*, size_t>> g_pin_sizes;   // every block ever allocated
+void* pinned_acquire(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 4096);
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        size_t best = g_pin_free.size();
+        for (size_t i = 0; i < g_pin_free.size(); ++i)
+            if (g_pin_free[i].second >= bytes &&
+                (best == g_pin_free.size() || g_pin_free[i].second < g_pin_free[best].second))
+                best = i;
+        if (best < g_pin_free.size()) {
+            void* p = g_pin_free[best].first;
+            g_pin_free.erase(g_pin_free.begin() + best);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CU(cudaMallocHost(&p, bytes));
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_sizes.push_back({p, bytes});
+    return p;
+}
+void pinned_release(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (auto& b : g_pin_sizes)
+        if (b.first == p) {
+            g_pin_free.push_back(b);
+            return;
+        }
+}
+
+// Per-graph staging slots over the cache.
+struct PinnedStage {
+    std::vector<std::pair<void*, size_t>> slots;
+    void* get(size_t bytes, int slot) {
+        if ((int)slots.size() <= slot) slots.resize(slot + 1, {nullptr, 0});
+        if (slots[slot].first && slots[slot].second >= bytes) return slots[slot].first;
+        pinned_release(slots[slot].first);
+        slots[slot] = {pinned_acquire(bytes), std::max<size_t>(bytes, 4096)};
+        return slots[slot].first;
+    }
+    void release() {
+        for (auto& b : slots) pinned_release(b.first);
+        slots.clear();
+    }
+};
+
 // Vertex state of one app on one partition: Theta(N), never a function of E
 // (single-slot mailboxes).
 struct AppState {
@@ -204,6 +259,18 @@ struct Partition {
     int64_t nondangling = 0;
     DeviceBuffers graph_mem;      // host copies, tile plans, push view
     cudaEvent_t up_idx = nullptr, up_w = nullptr, up_all = nullptr;   // host-upload progress
+    // derived CSR weights permuted window by window as the CSC weights' windows land (create
+    // from host memory): wx[i] = w[perm[i]] for perm[i] in [wc_bounds[c], wc_bounds[c + 1])
+    struct {
+        DeviceBuffers tmp;
+        int32_t* perm = nullptr;     // [edges] CSC position of each transposed entry
+        const uint32_t* w = nullptr;
+        uint32_t* wx = nullptr;
+        int64_t edges = 0;
+    } pend;
+    std::vector<cudaEvent_t> up_wc;   // one per weight window (copy stream)
+    cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
+    std::vector<int64_t> wc_bounds;
     AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
@@ -226,6 +293,7 @@ struct ipregel_graph {
     cudaStream_t stream = nullptr;
     ipregel_comm* comm = nullptr;
     std::vector<Partition> parts;
+    PinnedStage pinned;                      // create's staging (kernel copies)
     std::vector<int64_t> rank_vb, rank_rows;  // multi-GPU: every rank's owned range
     bool poisoned = false;
     int last_app = -1;             // ipregel_app, or kAppProgram
@@ -237,6 +305,7 @@ struct ipregel_graph {
     const int32_t* inv_ids = nullptr;   // original -> internal id (user programs' ipr_send)
     cudaStream_t capture_stream = nullptr;   // private stream for CUDA-graph capture
     cudaStream_t copy_stream = nullptr;      // host -> device uploads (MEMORY_HOST create)
+    cudaStream_t aux_stream = nullptr;       // create: weight permutation while uploading
     // PageRank (fixed k, pull) captured once as a CUDA graph and replayed: one launch per run
     struct {
         bool valid = false;
@@ -276,9 +345,26 @@ void check_device(int device) {
              device, prop.major, prop.minor);
 }
 
+// Copies through a kernel (UVA: either side may be pinned host memory).  Create uses them for
+// its small readbacks and uploads so the copy engines stay out of the host-upload window: a
+// cudaMemcpy on the run stream would queue behind the upload (see compute_fence, create.cuh).
+__global__ void k_copy_words(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+void kernel_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    if (bytes % 4) fail(IPREGEL_ERR_INVALID_ARGUMENT, "kernel_copy of %zu bytes", bytes);
+    const int64_t n = (int64_t)(bytes / 4);
+    k_copy_words<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, s>>>(
+        static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), n);
+    LAUNCH_CHECK();
+}
+
 void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint32_t* w,
                 int64_t rows, int64_t edges, int64_t vertex_base, int64_t edge_base,
-                DeviceBuffers& mem, cudaStream_t s) {
+                DeviceBuffers& mem, cudaStream_t s, PinnedStage& pin) {
     P.rows = (int32_t)rows;
     P.edges = edges;
     // ranges on the global merge grid (diagonal = global row + global edge index), chunks on the
@@ -303,8 +389,8 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
     int32_t* infl = tmp.alloc<int32_t>(Q, s);
     k_plan_inflight<<<grid_for(Q, 256), 256, 0, s>>>(off, P.cx, P.cy, P.rows, Q, infl);
     LAUNCH_CHECK();
-    std::vector<int32_t> h(Q);
-    CU(cudaMemcpyAsync(h.data(), infl, Q * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    int32_t* h = static_cast<int32_t*>(pin.get(Q * sizeof(int32_t), 0));
+    kernel_copy(h, infl, Q * sizeof(int32_t), s);
     CU(cudaStreamSynchronize(s));
     tmp.release();
     std::vector<int4> groups;
@@ -318,8 +404,9 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
     P.num_groups = (int32_t)groups.size();
     if (P.num_groups) {
         P.groups = mem.alloc<int4>(P.num_groups, s);
-        CU(cudaMemcpyAsync(P.groups, groups.data(), groups.size() * sizeof(int4),
-                           cudaMemcpyHostToDevice, s));
+        int4* hg = static_cast<int4*>(pin.get(groups.size() * sizeof(int4), 1));
+        memcpy(hg, groups.data(), groups.size() * sizeof(int4));
+        kernel_copy(P.groups, hg, groups.size() * sizeof(int4), s);
         CU(cudaStreamSynchronize(s));
     }
 }
@@ -545,6 +632,39 @@ void exscan_i32(int32_t* a, int64_t n, DeviceBuffers& tmp, cudaStream_t s) {
     LAUNCH_CHECK();
 }
 
+// Optional create-phase timeline (IPREGEL_TRACE_CREATE=1): CUDA events on the streams doing the
+// work, printed to stderr relative to the first mark when ipregel_graph_create returns.
+struct CreateTrace {
+    bool on = getenv("IPREGEL_TRACE_CREATE") != nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    std::vector<double> host_ms;   // when the host recorded the mark
+    std::chrono::steady_clock::time_point t0;
+    void mark(const char* name, cudaStream_t s) {
+        if (!on) return;
+        if (ev.empty()) t0 = std::chrono::steady_clock::now();
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        CU(cudaEventRecord(e, s));
+        ev.push_back({name, e});
+        host_ms.push_back(
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    void dump() {
+        if (!on || ev.empty()) return;
+        CU(cudaDeviceSynchronize());
+        for (size_t i = 0; i < ev.size(); ++i) {
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ev[0].second, ev[i].second));
+            fprintf(stderr, "[ipregel create] %-22s %9.2f ms (host %9.2f)\n", ev[i].first, ms,
+                    host_ms[i]);
+        }
+        for (auto& x : ev) cudaEventDestroy(x.second);
+        ev.clear();
+        host_ms.clear();
+    }
+};
+inline CreateTrace g_ctrace;
+
 // Transpose of a partition's rows (row r lists neighbours u) into a source-major adjacency over all
 // N sources (u lists vb + r), allocated in the partition's graph memory: a stable radix sort by
 // source (setup.cuh), so each transposed row lists its neighbours in ascending order.  w_ready:
@@ -552,7 +672,7 @@ void exscan_i32(int32_t* a, int64_t n, DeviceBuffers& tmp, cudaStream_t s) {
 void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* idx,
                     const uint32_t* w, int64_t edges, bool want_w, cudaStream_t s,
                     int32_t** out_off, int32_t** out_idx, uint32_t** out_w,
-                    cudaEvent_t w_ready = nullptr) {
+                    bool defer_w = false) {
     int32_t* o = p.graph_mem.alloc<int32_t>(n + 1, s, true);
     int32_t* ix = p.graph_mem.alloc<int32_t>(edges, s);
     uint32_t* wx = want_w ? p.graph_mem.alloc<uint32_t>(edges, s) : nullptr;
@@ -565,9 +685,11 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
         int32_t* k1 = tmp.alloc<int32_t>(edges, s);
         unsigned long long* v0 = tmp.alloc<unsigned long long>(edges, s);
         unsigned long long* v1 = tmp.alloc<unsigned long long>(edges, s);
+        g_ctrace.mark("transpose begin", s);
         CU(cudaMemcpyAsync(k0, idx, edges * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         k_transpose_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(off, p.rows, p.vb, v0);
         LAUNCH_CHECK();
+        g_ctrace.mark("transpose packed", s);
         cub::DoubleBuffer<int32_t> keys(k0, k1);
         cub::DoubleBuffer<unsigned long long> vals(v0, v1);
         int bits = 1;
@@ -576,9 +698,19 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
         CU(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, vals, edges, 0, bits, s));
         void* temp = tmp.alloc<uint8_t>((int64_t)temp_bytes, s);
         CU(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, vals, edges, 0, bits, s));
-        if (w_ready) CU(cudaStreamWaitEvent(s, w_ready, 0));   // weights uploaded meanwhile
+        g_ctrace.mark("transpose sorted", s);
+        int32_t* perm = nullptr;
+        if (defer_w && wx) {
+            // the weights are still uploading: keep each entry's CSC position, and let
+            // finish_uploads permute the weights window by window as they land
+            perm = p.pend.tmp.alloc<int32_t>(edges, s);
+            p.pend.perm = perm;
+            p.pend.w = w;
+            p.pend.wx = wx;
+            p.pend.edges = edges;
+        }
         k_transpose_unpack<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
-            vals.Current(), edges, w, ix, wx);
+            vals.Current(), edges, w, ix, wx, perm);
         LAUNCH_CHECK();
         // offsets from the sorted sources: run lengths, then an exclusive scan
         int32_t* st = tmp.alloc<int32_t>(n, s, true);
@@ -586,7 +718,9 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
             keys.Current(), edges, st, o);
         k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, o);
         LAUNCH_CHECK();
+        g_ctrace.mark("transpose unpacked", s);
         exscan_i32(o, n + 1, tmp, s);
+        g_ctrace.mark("transpose offsets", s);
     }
     CU(cudaStreamSynchronize(s));
     tmp.release();

@@ -250,6 +250,7 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
         }
         g->degree_ordered = descs[0].degree_ordered != 0;
         g->gather_policy = g_gather_policy >= 0 ? g_gather_policy : (g->degree_ordered ? 3 : 1);
+        g_ctrace.mark("create begin", g->stream);
         if (descs[0].vertex_ids) {
             if (descs[0].memory == IPREGEL_MEMORY_HOST) {
                 int32_t* d = g->graph_mem.alloc<int32_t>(n, g->stream);
@@ -273,6 +274,11 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
         }
         for (int i = 0; i < np; ++i) init_partition(g, g->parts[i], descs[i]);
         build_plans(g);
+        g_ctrace.mark("plans built", g->stream);
+        for (auto& p : g->parts) finish_uploads(g, p);
+        CU(cudaStreamSynchronize(g->stream));
+        g_ctrace.mark("create end", g->stream);
+        g_ctrace.dump();
     } catch (...) {
         destroy_graph(g);
         throw;

@@ -208,12 +208,25 @@ __global__ void k_run_counts(const int32_t* __restrict__ start, int64_t n,
 
 __global__ void k_transpose_unpack(const unsigned long long* __restrict__ vals, int64_t edges,
                                    const uint32_t* __restrict__ w, int32_t* __restrict__ out_idx,
-                                   uint32_t* __restrict__ out_w) {
+                                   uint32_t* __restrict__ out_w, int32_t* __restrict__ out_perm) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
          i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long x = vals[i];
         out_idx[i] = (int32_t)(uint32_t)x;
-        if (out_w) out_w[i] = w ? __ldg(w + (uint32_t)(x >> 32)) : 1u;
+        if (out_perm) out_perm[i] = (int32_t)(uint32_t)(x >> 32);   // weights permuted later
+        else if (out_w) out_w[i] = w ? __ldg(w + (uint32_t)(x >> 32)) : 1u;
+    }
+}
+
+// One window [lo, hi) of the deferred weight permutation: wx[i] = w[perm[i]] where perm[i] falls
+// in the window (the window's upload has landed; the others are written by their own passes).
+__global__ void k_permute_window(const int32_t* __restrict__ perm, int64_t edges, int64_t lo,
+                                 int64_t hi, const uint32_t* __restrict__ w,
+                                 uint32_t* __restrict__ wx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = perm[i];
+        if (e >= lo && e < hi) wx[i] = __ldg(w + e);
     }
 }
 

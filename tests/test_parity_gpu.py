@@ -585,10 +585,14 @@ def test_cc_rowlist_pull_matches_oracle(parts, mode):
 
 # ------------------------------------------------------------------ CSR derived from the CSC
 
-@pytest.mark.parametrize("host", [False, True])
-def test_csr_derived_on_device_matches_given_csr(host):
+@pytest.mark.parametrize("host,windows", [(False, None), (True, None), (True, "7")])
+def test_csr_derived_on_device_matches_given_csr(host, windows, monkeypatch):
+    """windows: the host upload of the CSC weights in 7 windows, each permuted into the derived
+    CSR's weights as it lands (create.cuh finish_uploads; cfg4 uses 8)."""
     import paper_2010_08781_b200 as ipr
     from tests.graphs import to_device
+    if windows:
+        monkeypatch.setenv("IPREGEL_WEIGHT_WINDOWS", windows)
     rng = np.random.default_rng(31)
     n = 2500
     src, dst, w = checkers.random_graph(rng, n, 15000, weighted=True)
