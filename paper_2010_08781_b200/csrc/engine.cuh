@@ -1,6 +1,7 @@
 // paper_2010_08781_b200/csrc/engine.cuh -- errors, device memory, the graph and partition state, launch helpers, exchanges, frontier machinery, the fused exchange and per-superstep timing.
 // Host part of the single translation unit ipregel.cu (included once, in order).
 #pragma once
+#include <algorithm>
 #include <chrono>
 #include <mutex>
 
@@ -401,7 +402,12 @@ void build_plan(TilePlan& P, const int32_t* off, const int32_t* idx, const uint3
         else
             groups.push_back(make_int4(h[b], b, b, 0));
     }
+    // short spans first (one thread each in k_pull_fixup), hub rows after (one warp each)
+    std::stable_partition(groups.begin(), groups.end(),
+                          [](const int4& G) { return G.z - G.y + 1 <= kFixupShortSpan; });
     P.num_groups = (int32_t)groups.size();
+    P.num_short = 0;
+    for (const int4& G : groups) P.num_short += (G.z - G.y + 1 <= kFixupShortSpan) ? 1 : 0;
     if (P.num_groups) {
         P.groups = mem.alloc<int4>(P.num_groups, s);
         int4* hg = static_cast<int4*>(pin.get(groups.size() * sizeof(int4), 1));
@@ -426,8 +432,8 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
     k_pull_ranges<Op><<<(unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads, 0, s>>>(op, A);
     LAUNCH_CHECK();
     if (P.num_groups) {
-        k_pull_fixup<Op><<<grid_for((int64_t)P.num_groups * 32, 256), 256, 0, s>>>(
-            op, P.groups, P.num_groups, static_cast<const T*>(P.carry),
+        k_pull_fixup<Op><<<fixup_grid(P.num_groups, P.num_short), 256, 0, s>>>(
+            op, P.groups, P.num_groups, P.num_short, static_cast<const T*>(P.carry),
             static_cast<const T*>(P.head), cnt);
         LAUNCH_CHECK();
     }

@@ -72,6 +72,7 @@ struct TilePlan {
     int32_t* cx = nullptr;    // [num_tiles + 1] rows finished before each range boundary
     int32_t* cy = nullptr;    // [num_tiles + 1] edges consumed before each range boundary
     int32_t num_groups = 0;
+    int32_t num_short = 0;    // groups[0, num_short) span <= kFixupShortSpan boundaries
     int4* groups = nullptr;   // rows cut by range boundaries: (row, first boundary a, last b, 0)
     void* carry = nullptr;    // [num_tiles] partial of the row leaving the range (8-byte slots)
     void* head = nullptr;     // [num_tiles] partial of the row entering and ending in the range
@@ -710,32 +711,51 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
-// carry[a-1] (+) carry[a] (+) ... (+) carry[b-1] (+) head[b], folded in a fixed order
-// (lane-strided partials, then a fixed xor tree).  One warp per spanning row.
+// carry[a-1] (+) carry[a] (+) ... (+) carry[b-1] (+) head[b], folded in a fixed order that
+// depends on the span only (ranges sit on the global grid, so on every partitioning alike):
+//   groups [0, num_short) span <= kFixupShortSpan boundaries: one thread each, a left fold;
+//   the rest (hub rows): one warp each, lane-strided partials then a fixed xor tree.
+// The first ceil(num_short / blockDim) blocks take the short groups (grid: fixup_grid()).
+constexpr int32_t kFixupShortSpan = 16;
+inline unsigned fixup_grid(int32_t num_groups, int32_t num_short) {
+    return (unsigned)((num_short + 255) / 256 + ((int64_t)(num_groups - num_short) * 32 + 255) / 256);
+}
 template <class Op>
 __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num_groups,
-                             const typename Op::T* __restrict__ carry,
+                             int32_t num_short, const typename Op::T* __restrict__ carry,
                              const typename Op::T* __restrict__ head,
                              PullCounters* __restrict__ counters) {
     using T = typename Op::T;
     __shared__ unsigned long long s_cnt[4];
     const int lane = threadIdx.x & 31;
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
-    if (g < num_groups) {
-        const int4 G = groups[g];
-        T acc = Op::identity();
-        for (int t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const T o = shfl_xor(acc, d);
-            acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
+    const int32_t short_blocks = (num_short + (int32_t)blockDim.x - 1) / (int32_t)blockDim.x;
+    if ((int32_t)blockIdx.x < short_blocks) {
+        const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (g < num_short) {
+            const int4 G = groups[g];
+            T acc = carry[G.y - 1];
+            for (int t = G.y; t <= G.z - 1; ++t) acc = Op::combine(acc, carry[t]);
+            op.finish(G.x, Op::combine(acc, head[G.z]), c);
         }
-        if (lane == 0) {
-            acc = Op::combine(acc, head[G.z]);
-            op.finish(G.x, acc, c);
+    } else {
+        const int64_t g =
+            num_short + (((int64_t)(blockIdx.x - short_blocks) * blockDim.x + threadIdx.x) >> 5);
+        if (g < num_groups) {
+            const int4 G = groups[g];
+            T acc = Op::identity();
+            for (int t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const T o = shfl_xor(acc, d);
+                acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
+            }
+            if (lane == 0) {
+                acc = Op::combine(acc, head[G.z]);
+                op.finish(G.x, acc, c);
+            }
         }
     }
     // one global atomic per CTA (not per group: the counters are shared by every group)

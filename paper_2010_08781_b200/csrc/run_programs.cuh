@@ -250,11 +250,11 @@ void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, 
                args, g->stream);
     if (P.num_groups) {
         const int4* groups = P.groups;
-        int32_t ng = P.num_groups;
+        int32_t ng = P.num_groups, ns = P.num_short;
         const V* carry = static_cast<const V*>(P.carry);
         const V* head = static_cast<const V*>(P.head);
-        void* fargs[] = {&a, &groups, &ng, &carry, &head, &cnt};
-        launch_jit(pr->k[PK_FIX0 + pass], grid_for((int64_t)ng * 32, 256), 256, fargs, g->stream);
+        void* fargs[] = {&a, &groups, &ng, &ns, &carry, &head, &cnt};
+        launch_jit(pr->k[PK_FIX0 + pass], fixup_grid(ng, ns), 256, fargs, g->stream);
     }
 }
 
