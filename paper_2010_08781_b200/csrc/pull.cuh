@@ -28,6 +28,10 @@
 
 namespace ipr {
 
+// L2 prefetch distance of the index / weight stream in chunks (0 = off)
+#ifndef IPREGEL_IDX_PREFETCH
+#define IPREGEL_IDX_PREFETCH 0
+#endif
 #ifndef IPREGEL_PULL_MINBLOCKS
 #define IPREGEL_PULL_MINBLOCKS 4
 #endif
@@ -161,6 +165,7 @@ struct NoAggregate {
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
 struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
+    static constexpr int kMinBlocks = 3;   // as PageRankSum
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
     PeerSlots<double> peers;                  // fused exchange: other replicas (n = 0: none)
@@ -441,6 +446,10 @@ __device__ __forceinline__ void warp_fold2(typename Op::T a, typename Op::T b,
     fb = shfl_idx(x, 16);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // One warp, one range q (see the file header).  `my_sum` is the warp's sum array: 128 slots
 // by chunk position + 2 for the first / last segment of 8-byte chunks.
 template <class Op>
@@ -497,6 +506,18 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
         Lc = Ln;
         Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, e0 + 2 * kChunk, y0, y1, lane, pol_s,
                                        absorbed && r < x1 && Ec > e0 + 3 * kChunk);
+#if IPREGEL_IDX_PREFETCH > 0
+        {
+            // the index (and weight) stream further ahead into L2: under the gathers' load the
+            // DRAM latency of the loads two chunks ahead is not covered (ncu: the top stall)
+            const int32_t pc = e0 + IPREGEL_IDX_PREFETCH * kChunk;
+            const int32_t pe = pc + 4 * lane;
+            if (pe < y1 && !(absorbed && r < x1 && Ec > pc + kChunk)) {
+                prefetch_l2(A.idx + pe);
+                if (Op::kWeighted && A.wts) prefetch_l2(A.wts + pe);
+            }
+        }
+#endif
         T v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
