@@ -226,6 +226,47 @@ template <> struct ProgComb<int64_t, 2> {
     }
 };
 
+// The combiner's absorbing element z (combine(z, x) == combine(x, z) == z for every message x)
+// of the integer MIN / MAX combiners: once a row's partial mailbox fold reaches z, its remaining
+// messages cannot change it, so the pull skips their gathers (exact).  SUM has none; the
+// floating-point MIN / MAX are left out (a NaN message would not be absorbed in every order).
+template <class V, int kComb> struct ProgAbsorb {
+    static constexpr bool kHas = false;
+    __device__ static bool is(V) { return false; }
+};
+template <> struct ProgAbsorb<uint32_t, 1> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(uint32_t x) { return x == 0u; }
+};
+template <> struct ProgAbsorb<uint32_t, 2> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(uint32_t x) { return x == 0xFFFFFFFFu; }
+};
+template <> struct ProgAbsorb<int32_t, 1> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(int32_t x) { return x == (int32_t)0x80000000u; }
+};
+template <> struct ProgAbsorb<int32_t, 2> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(int32_t x) { return x == (int32_t)0x7FFFFFFF; }
+};
+template <> struct ProgAbsorb<uint64_t, 1> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(uint64_t x) { return x == 0ull; }
+};
+template <> struct ProgAbsorb<uint64_t, 2> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(uint64_t x) { return x == ~0ull; }
+};
+template <> struct ProgAbsorb<int64_t, 1> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(int64_t x) { return x == (int64_t)0x8000000000000000ull; }
+};
+template <> struct ProgAbsorb<int64_t, 2> {
+    static constexpr bool kHas = true;
+    __device__ static bool is(int64_t x) { return x == (int64_t)0x7FFFFFFFFFFFFFFFll; }
+};
+
 template <class V>
 __device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
     ProgCtx x;
@@ -294,7 +335,7 @@ __device__ __forceinline__ void flush_prog_aggregate(const LaneCounters& c, int 
 }
 
 // Record what one vertex did: outbox slot (identity unless it broadcast), bitmap, counters.
-template <class P>
+template <class P, bool kInit = false>
 __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int64_t row,
                                           const ProgCtx& x, unsigned f, typename P::V msg,
                                           LaneCounters& c) {
@@ -305,7 +346,10 @@ __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int6
     A.out_next[A.vbase + row] = ob;
     A.peers.store(A.vbase + row, ob);
     const bool act = (f & kProgStayActive) != 0;
-    A.flags[row] = (uint8_t)((b ? 1u : 0u) | (act ? 2u : 0u));   // plain store, no atomics
+    // bit 2: broadcast one superstep earlier, i.e. the outbox buffer written NEXT holds a
+    // non-identity value for this row (k_prog_apply then has to clear it)
+    const uint8_t hist = kInit ? 4u : (uint8_t)((A.flags[row] & 1u) << 2);
+    A.flags[row] = (uint8_t)((b ? 1u : 0u) | (act ? 2u : 0u) | hist);   // plain store
     if (b) {
         c.changed += 1;
         c.messages += (uint32_t)x.out_degree + (P::kSym ? (uint32_t)x.in_degree : 0u);
@@ -375,7 +419,7 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
                 c.agg_n = 1u;
             }
         }
-        prog_emit<P>(A, row, x, f, msg, c);
+        prog_emit<P, true>(A, row, x, f, msg, c);   // buffer 1 holds a previous run's values
     }
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
@@ -390,10 +434,14 @@ struct ProgPull : ProgArgs<typename P::V> {
     using T = typename P::V;
     using C = ProgComb<T, P::kCombiner>;
     static constexpr bool kWeighted = true;
+    using Z = ProgAbsorb<T, P::kCombiner>;
     // optional ipr_absorbing(value): a vertex holding such a value ignores its messages, so its
-    // row need not be gathered (and whole ranges of such rows are skipped)
-    static constexpr bool kAbsorbing = P::kAbsorbing;
-    static constexpr bool kAbsorbingPartial = false;
+    // row need not be gathered (and whole ranges of such rows are skipped).  Second half of a
+    // symmetric pull: a row whose first-half mailbox already holds the combiner's absorbing
+    // element needs no second-half gathers either; and any partial fold reaching it ends the
+    // row's gathers (kAbsorbingPartial).
+    static constexpr bool kAbsorbing = P::kAbsorbing || (kPass == 2 && Z::kHas);
+    static constexpr bool kAbsorbingPartial = Z::kHas;
     static constexpr bool kAggregates = false;   // compute runs in k_prog_apply
     // 8-byte values: 3 CTAs per SM, as PageRankSum (PageRank program 79.7 -> 78.4 ms at cfg4)
 #ifndef IPREGEL_PROG_MINBLOCKS8
@@ -405,10 +453,12 @@ struct ProgPull : ProgArgs<typename P::V> {
     __device__ static T combine(T a, T b) { return C::combine(a, b); }
     __device__ const T* gptr() const { return this->out_cur; }
     __device__ bool absorbed(int32_t row) const {
+        if constexpr (kPass == 2 && Z::kHas)
+            if (Z::is(this->mbox[row])) return true;
         if constexpr (P::kAbsorbing) return P::absorbing(this->value[row]);
         return false;
     }
-    __device__ bool absorbing(T) const { return false; }
+    __device__ bool absorbing(T x) const { return Z::is(x); }
     __device__ static T message(T g, uint32_t w) { return P::edge(g, w); }
     // The range kernels only fold each row's messages into its mailbox; the user's compute
     // runs row-parallel in k_prog_apply (pull_all) -- the same split as the built-in PageRank,
@@ -461,14 +511,20 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
         got = (A.recv[row >> 5] >> (row & 31)) & 1u;
         if constexpr (P::kSends)
             if (A.p2p_in_recv) got = got || ((A.p2p_in_recv[row >> 5] >> (row & 31)) & 1u);
-        if (got || (A.flags[row] & 2u)) {
+        const uint8_t fl = A.flags[row];
+        if (got || (fl & 2u)) {
             const V m = A.mbox[row];
             A.mbox[row] = C::identity();
             prog_vertex<P>(A, row, m, c);
-        } else {
-            A.out_next[A.vbase + row] = C::identity();
-            A.peers.store(A.vbase + row, C::identity());
-            A.flags[row] = 0;
+        } else if (fl) {
+            // halted and no messages: no broadcast.  The buffer written now holds a value only
+            // if the row broadcast two supersteps ago (bit 2); rows with no flags are untouched
+            // (the common case: one byte read per vertex instead of an outbox store)
+            if (fl & 4u) {
+                A.out_next[A.vbase + row] = C::identity();
+                A.peers.store(A.vbase + row, C::identity());
+            }
+            A.flags[row] = (uint8_t)((fl & 1u) << 2);
         }
     }
     __syncwarp();
