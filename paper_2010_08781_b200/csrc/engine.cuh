@@ -231,7 +231,8 @@ struct AppState {
     void* pv_value = nullptr;                  // owned values [rows]
     void* pv_out[2] = {nullptr, nullptr};      // outbox replicas [N] (identity = no broadcast)
     void* pv_mbox = nullptr;                   // owned mailboxes [rows]
-    uint8_t* pv_flags = nullptr;               // owned: bit 0 broadcast, bit 1 active
+    uint8_t* pv_flags = nullptr;               // owned: bit 0 broadcast, bit 1 active, bit 2
+                                               // broadcast one superstep earlier (padded to 32)
     uint32_t* pv_recv = nullptr;               // owned recipient bitmap (push)
     double* pv_params = nullptr;               // program parameters [8]
     void* pv_p2p[2] = {nullptr, nullptr};      // point-to-point mailboxes [rows] (by parity)
@@ -571,7 +572,7 @@ void ensure_state(ipregel_graph* g, int app) {
             S.pv_out[0] = S.mem.alloc<uint64_t>(n, s, true, ipc);
             S.pv_out[1] = S.mem.alloc<uint64_t>(n, s, true, ipc);
             S.pv_mbox = S.mem.alloc<uint64_t>(p.rows, s, true);
-            S.pv_flags = S.mem.alloc<uint8_t>(p.rows, s, true);
+            S.pv_flags = S.mem.alloc<uint8_t>(ceil_div(p.rows, 32) * 32, s, true);   // vector reads
             S.pv_recv = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.pv_params = S.mem.alloc<double>(kProgParams, s, true);
             for (int w = 0; w < 2; ++w) {

@@ -496,6 +496,9 @@ k_prog_expand(PushAdj adj, const int32_t* __restrict__ e_id, const long long* __
 
 // After the expansion: compute on recipients and active vertices (naive selection, PAPER.md:
 // 171-175, which here equals the bypass list plus the non-halted), reset their mailboxes.
+// kProgApplyRows rows per thread: one 16-byte load of their flags and half a recipient word
+// decide, in the common case of a sparse frontier, that none of them has anything to do.
+constexpr int kProgApplyRows = 16;
 template <class P>
 __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
                                                     PullCounters* counters) {
@@ -505,30 +508,38 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{};
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool got = false;
-    if (row < A.rows) {
-        got = (A.recv[row >> 5] >> (row & 31)) & 1u;
+    const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kProgApplyRows;
+    if (base < A.rows) {
+        const uint4 f4 = *reinterpret_cast<const uint4*>(A.flags + base);   // padded array
+        uint32_t got16 = (A.recv[base >> 5] >> (base & 31)) & 0xFFFFu;
         if constexpr (P::kSends)
-            if (A.p2p_in_recv) got = got || ((A.p2p_in_recv[row >> 5] >> (row & 31)) & 1u);
-        const uint8_t fl = A.flags[row];
-        if (got || (fl & 2u)) {
-            const V m = A.mbox[row];
-            A.mbox[row] = C::identity();
-            prog_vertex<P>(A, row, m, c);
-        } else if (fl) {
-            // halted and no messages: no broadcast.  The buffer written now holds a value only
-            // if the row broadcast two supersteps ago (bit 2); rows with no flags are untouched
-            // (the common case: one byte read per vertex instead of an outbox store)
-            if (fl & 4u) {
-                A.out_next[A.vbase + row] = C::identity();
-                A.peers.store(A.vbase + row, C::identity());
+            if (A.p2p_in_recv) got16 |= (A.p2p_in_recv[base >> 5] >> (base & 31)) & 0xFFFFu;
+        if ((f4.x | f4.y | f4.z | f4.w | got16) != 0u) {
+            const uint32_t fw[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll 1
+            for (int j = 0; j < kProgApplyRows; ++j) {
+                const int64_t row = base + j;
+                if (row >= A.rows) break;
+                const uint8_t fl = (uint8_t)(fw[j >> 2] >> (8 * (j & 3)));
+                if (((got16 >> j) & 1u) || (fl & 2u)) {
+                    const V m = A.mbox[row];
+                    A.mbox[row] = C::identity();
+                    prog_vertex<P>(A, row, m, c);
+                } else if (fl) {
+                    // halted and no messages: no broadcast.  The buffer written now holds a
+                    // value only if the row broadcast two supersteps ago (bit 2); rows without
+                    // flags are not touched at all
+                    if (fl & 4u) {
+                        A.out_next[A.vbase + row] = C::identity();
+                        A.peers.store(A.vbase + row, C::identity());
+                    }
+                    A.flags[row] = (uint8_t)((fl & 1u) << 2);
+                }
             }
-            A.flags[row] = (uint8_t)((fl & 1u) << 2);
         }
     }
-    __syncwarp();
-    if (row < A.rows && (row & 31) == 0) A.recv[row >> 5] = 0u;
+    __syncwarp();   // both halves of a recipient word were read above
+    if (base < A.rows && (base & 31) == 0) A.recv[base >> 5] = 0u;
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }

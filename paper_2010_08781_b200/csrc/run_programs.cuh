@@ -305,7 +305,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             CU(cudaMemcpyAsync(S.pv_shared, &h, sizeof(h), cudaMemcpyHostToDevice, s));
             if (pr->sends && p.rows) {
                 for (int w = 0; w < 2; ++w) {
-                    k_fill_u64<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                    k_fill_u64<<<grid_for(ceil_div(p.rows * (int64_t)sizeof(V), 16), 256), 256, 0, s>>>(
                         static_cast<uint64_t*>(S.pv_p2p[w]), p.rows, ident, (int)sizeof(V));
                     LAUNCH_CHECK();
                     CU(cudaMemsetAsync(S.pv_p2p_recv[w], 0, words_of(p.rows) * 4, s));
@@ -434,7 +434,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             if (prev_mode == 1) {   // a pull left folded mailboxes behind: back to the identity
                 for (auto& p : g->parts) {
                     if (!p.rows) continue;
-                    k_fill_u64<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                    k_fill_u64<<<grid_for(ceil_div(p.rows * (int64_t)sizeof(V), 16), 256), 256, 0, s>>>(
                         static_cast<uint64_t*>(p.st[app].pv_mbox), p.rows, ident, (int)sizeof(V));
                     LAUNCH_CHECK();
                 }
@@ -442,7 +442,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             // frontier = the broadcasters of superstep s-1 (flag bytes -> bitmap -> ids)
             for (auto& p : g->parts) {
                 if (p.rows) {
-                    k_bits_from_flags<<<grid_for(p.rows, 256), 256, 0, s>>>(p.st[app].pv_flags,
+                    k_bits_from_flags<<<grid_for(ceil_div(p.rows, 32), 256), 256, 0, s>>>(p.st[app].pv_flags,
                                                                            p.rows, p.st[app].bits);
                     LAUNCH_CHECK();
                 }
@@ -469,7 +469,8 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
                 ProgArgs<V> a = args_for(p, step, cur);
                 PullCounters* cnt = p.pull_cnt;
                 void* args[] = {&a, &cnt};
-                launch_jit(pr->k[PK_APPLY], grid_for(p.rows, 256), 256, args, s);
+                launch_jit(pr->k[PK_APPLY], grid_for(ceil_div(p.rows, kProgApplyRows), 256), 256,
+                           args, s);
             }
             T.kend();
         } else {

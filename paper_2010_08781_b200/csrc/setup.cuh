@@ -24,10 +24,18 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
 // for the frontier compaction of a push superstep (ballot per warp).
 __global__ void k_bits_from_flags(const uint8_t* __restrict__ flags, int64_t rows,
                                   uint32_t* __restrict__ bits) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool pred = i < rows && (flags[i] & 1u);
-    const uint32_t b = __ballot_sync(kFull, pred);
-    if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
+    // one thread per 32 rows: two 16-byte loads of flag bytes (the flag array is padded to a
+    // multiple of 32 bytes with zeros) -> one bitmap word
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= (rows + 31) / 32) return;
+    const uint4* f = reinterpret_cast<const uint4*>(flags + 32 * w);
+    const uint4 a = f[0], b = f[1];
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t m = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        m |= ((v[i] & 1u) | ((v[i] >> 7) & 2u) | ((v[i] >> 14) & 4u) | ((v[i] >> 21) & 8u)) << (4 * i);
+    bits[w] = m;
 }
 
 // Max of (INF - value) over a device list of values (SSSP: the smallest distance among a push
@@ -66,10 +74,20 @@ __global__ void k_min_u32(const uint32_t* __restrict__ a, int64_t n, unsigned* _
 
 // Fill 8-byte slots with a pattern (vsz 4: the low 32 bits into a u32 array of the same count).
 __global__ void k_fill_u64(uint64_t* __restrict__ a, int64_t n, uint64_t pattern, int vsz) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (vsz == 8) a[i] = pattern;
-    else reinterpret_cast<uint32_t*>(a)[i] = (uint32_t)pattern;
+    // 16 bytes per thread
+    const int64_t bytes = n * vsz;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16;
+    if (i >= bytes) return;
+    uint8_t* p = reinterpret_cast<uint8_t*>(a) + i;
+    if (i + 16 <= bytes) {
+        const uint64_t q = vsz == 8 ? pattern : ((pattern & 0xFFFFFFFFull) | (pattern << 32));
+        *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(q, q);
+    } else {
+        for (int64_t k = i; k < bytes; k += vsz) {
+            if (vsz == 8) *reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(a) + k) = pattern;
+            else *reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(a) + k) = (uint32_t)pattern;
+        }
+    }
 }
 
 // inv[ids[v]] = v
