@@ -707,7 +707,10 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
 
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A
 // thread takes kPrFinishRows rows (block-strided, coalesced) with their sums loaded up front.
-constexpr int kPrFinishRows = 4;
+#ifndef IPREGEL_PR_FINISH_ROWS
+#define IPREGEL_PR_FINISH_ROWS 4
+#endif
+constexpr int kPrFinishRows = IPREGEL_PR_FINISH_ROWS;
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
     __shared__ unsigned long long s_cnt[4];
