@@ -324,3 +324,53 @@ __device__ unsigned ipr_edge(unsigned m, unsigned) { return m; }
         st = G.run_program(p, mode="pull", max_supersteps=10, allow_guard=True)
         assert st == ipr.ERR_MAX_SUPERSTEPS
         G.close()
+
+
+PULSE = r"""
+// s=0,1: everyone broadcasts 1 (pull supersteps).  s=2: vertex 0 broadcasts, even ids stay
+// active, odd ids halt -> few messages, so AUTO pushes at s=3, where the even ids broadcast id+1
+// and the odd ids (halted, mostly without messages) must leave NO stale value in the outbox
+// buffer they last wrote at s=1: s=4 pulls it, summing only the even senders.
+__device__ unsigned ipr_init(const ipr_ctx&, unsigned* value, unsigned* message) {
+    *value = 0;
+    *message = 1;
+    return IPR_BROADCAST;
+}
+__device__ unsigned ipr_compute(const ipr_ctx& c, unsigned* value, unsigned mailbox, unsigned* message) {
+    if (c.superstep == 1) { *message = 1; return IPR_BROADCAST; }
+    if (c.superstep == 2) {
+        if (c.id == 0) { *message = 7; return IPR_BROADCAST | IPR_STAY_ACTIVE; }
+        return (c.id % 2 == 0) ? IPR_STAY_ACTIVE : 0;
+    }
+    if (c.superstep == 3) {
+        if (c.id % 2 == 0) { *message = (unsigned)c.id + 1; return IPR_BROADCAST; }
+        return 0;
+    }
+    *value = mailbox;
+    return 0;
+}
+__device__ unsigned ipr_edge(unsigned m, unsigned) { return m; }
+"""
+
+
+@pytest.mark.parametrize("parts,exchange", [(1, "auto"), (3, "fused"), (3, "collective")])
+def test_push_superstep_clears_stale_outbox(parts, exchange):
+    """Push supersteps skip idle rows (program.cuh k_prog_apply, flag bit 2 = broadcast two
+    supersteps ago): a halted row without messages must still clear the outbox slot it wrote two
+    supersteps earlier, or the next pull superstep would gather its stale message."""
+    import paper_2010_08781_b200 as ipr
+    p = ipr.Program(PULSE, "u32", "sum")
+    rng = np.random.default_rng(17)
+    n = 3000
+    src, dst, _ = checkers.random_graph(rng, n, 30000, weighted=False)
+    src = np.concatenate([src, np.zeros(3, np.int64)])
+    dst = np.concatenate([dst, np.array([5, 6, 9])])
+    G = make_graph(csr_csc(n, src, dst), partitions=parts, weighted=False)
+    G.run_program(p, mode="auto", push_fraction=0.05, exchange=exchange)
+    s = G.stats()
+    modes = "".join("ilpr"[m] for m in s["mode"])
+    assert modes[3] == "p" and modes[4] == "l", modes   # push at s=3, pull at s=4
+    even = (src % 2) == 0
+    want = np.bincount(dst[even], weights=(src[even] + 1), minlength=n).astype(np.uint32)
+    np.testing.assert_array_equal(G.values(host=True), want)
+    G.close()
