@@ -32,6 +32,9 @@ namespace ipr {
 #ifndef IPREGEL_IDX_PREFETCH
 #define IPREGEL_IDX_PREFETCH 0
 #endif
+#ifndef IPREGEL_PR_MINBLOCKS
+#define IPREGEL_PR_MINBLOCKS 3   // PageRankSum / PageRankPull CTAs per SM
+#endif
 #ifndef IPREGEL_PULL_MINBLOCKS
 #define IPREGEL_PULL_MINBLOCKS 4
 #endif
@@ -80,6 +83,7 @@ struct TilePlan {
     int4* groups = nullptr;   // rows cut by range boundaries: (row, first boundary a, last b, 0)
     void* carry = nullptr;    // [num_tiles] partial of the row leaving the range (8-byte slots)
     void* head = nullptr;     // [num_tiles] partial of the row entering and ending in the range
+    int32_t* ctr = nullptr;   // dynamic range counter (zeroed before each launch)
 };
 
 // Range boundary b: local diagonal clamp(b * kRangeItems - phase, 0, rows + edges) and its merge
@@ -165,7 +169,7 @@ struct NoAggregate {
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
 struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
-    static constexpr int kMinBlocks = 3;   // as PageRankSum
+    static constexpr int kMinBlocks = IPREGEL_PR_MINBLOCKS;   // as PageRankSum
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
     PeerSlots<double> peers;                  // fused exchange: other replicas (n = 0: none)
@@ -204,7 +208,7 @@ struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
     // 3 CTAs per SM (80 registers, no spills) instead of 4 (64 + stack): PageRank run 77.2 ->
     // 75.4 ms at cfg4 (the u32 min ops are faster at 4)
-    static constexpr int kMinBlocks = 3;
+    static constexpr int kMinBlocks = IPREGEL_PR_MINBLOCKS;
     const double* __restrict__ contrib_cur;
     double* __restrict__ sum_out;             // = contrib_next of the superstep (global ids)
     int64_t vbase;
@@ -383,6 +387,7 @@ struct RangeArgs {
     const void* gbase;
     uint32_t ghot, gtotal;
     int32_t l1hot;
+    int32_t* range_ctr;   // non-null: warps take ranges from this zeroed counter (dynamic)
 };
 
 // counters: warp reduce, one shared atomic per warp, one global atomic per CTA
@@ -700,7 +705,22 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters cnt{0u, 0u, 0u, 0ull, 0.0, 0u};
-    if (q < A.num_ranges) pull_range<Op>(op, A, q, s_sum[wid], cnt);
+    // warps stride over the ranges independently (the grid may be smaller than one warp per
+    // range): no warp waits for the slowest warp of its CTA before taking its next range
+    if (A.range_ctr) {
+        // dynamic: the next range index is fetched while the current one runs
+        const int lane = threadIdx.x & 31;
+        int32_t r = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
+        r = __shfl_sync(kFull, r, 0);
+        while (r < A.num_ranges) {
+            const int32_t nx = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
+            pull_range<Op>(op, A, r, s_sum[wid], cnt);
+            r = __shfl_sync(kFull, nx, 0);
+        }
+    } else {
+        const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+        for (int64_t r = q; r < A.num_ranges; r += nw) pull_range<Op>(op, A, r, s_sum[wid], cnt);
+    }
     flush_counters(cnt, s_cnt, A.counters);
     if constexpr (Op::kAggregates) op.flush_aggregate(cnt);
 }

@@ -246,7 +246,14 @@ void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, 
     RangeArgs A = range_args(P, off, idx, w, cnt, g->stream, a.out_cur, g->n, sizeof(V),
                              g->gather_policy, g->degree_ordered);
     void* args[] = {&a, &A};
-    launch_jit(pr->k[PK_PULL0 + pass], (unsigned)ceil_div(P.num_tiles, kWarpsPerCta), kPullThreads,
+    // resident CTAs per SM = the op's launch bound (the JIT kernels carry the same bounds)
+    static int sms = 0;
+    if (!sms) CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    const int64_t need = ceil_div(P.num_tiles, kWarpsPerCta);
+    const int64_t resident = (int64_t)sms * (sizeof(V) == 8 ? IPREGEL_PROG_MINBLOCKS8 : IPREGEL_PULL_MINBLOCKS);
+    const unsigned grid = (unsigned)(g_pull_waves == 0 || !A.range_ctr
+                                         ? need : std::min<int64_t>(need, resident * g_pull_waves));
+    launch_jit(pr->k[PK_PULL0 + pass], grid, kPullThreads,
                args, g->stream);
     if (P.num_groups) {
         const int4* groups = P.groups;
