@@ -47,7 +47,10 @@ template <class Op> struct PullMinBlocks<Op, void_t_<decltype(Op::kMinBlocks)>> 
 constexpr int kPullThreads = 256;                 // 8 warps per CTA
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
-constexpr int kRangeItems = 4096;                 // merge items (edges + rows) per warp range
+#ifndef IPREGEL_RANGE_ITEMS
+#define IPREGEL_RANGE_ITEMS 8192   // 4096: PageRank +0.5 ms; 2048 / 16384 / 32768 slower (cfg4)
+#endif
+constexpr int kRangeItems = IPREGEL_RANGE_ITEMS;  // merge items (edges + rows) per warp range
 
 struct PullCounters {
     unsigned long long changed;
