@@ -303,6 +303,13 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * `value` ignores every message (e.g. Hash-Min's label 0): pull supersteps then skip gathering
  * its in-edges, and whole merge-path ranges of such vertices (compute still runs, with the
  * identity as mailbox).
+ * Optional hint (MIN combiner, no ipr_send): __device__ bool ipr_settled(ipr_value_t value,
+ * ipr_value_t bound) -- true when a vertex holding `value` cannot change if every message it
+ * receives is >= `bound`.  Defining it asserts that ipr_edge is non-decreasing in both the
+ * message and the weight; the library then takes bound = ipr_edge(smallest message broadcast in
+ * the previous superstep, smallest edge weight) for each pull superstep and skips the gathers
+ * of settled vertices (and, for integer values, of rows whose partial fold is <= bound) --
+ * SSSP's "distance <= min frontier distance + min weight" (one GPU: whole graph or loopback).
  * The run ends when a superstep has no broadcast and no active vertex.
  * Selection (R28): push supersteps run compute on recipients and active vertices
  * only; pull supersteps run it on every vertex, the non-recipients getting the identity, so a

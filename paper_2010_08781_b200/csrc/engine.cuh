@@ -244,6 +244,8 @@ struct AppState {
     ProgShared* pv_shared = nullptr;           // device copy of the run's ProgShared
     unsigned long long* pv_sends = nullptr;    // point-to-point sends of the superstep
     double* pv_agg = nullptr;                  // aggregator fold of the superstep
+    unsigned long long* pv_mkey = nullptr;     // ipr_settled: min broadcast key [2] (by parity)
+    unsigned long long* pv_bound = nullptr;    //   and the pull superstep's bound [1]
     DeviceBuffers mem;
 };
 
@@ -614,6 +616,8 @@ void ensure_state(ipregel_graph* g, int app) {
             S.pv_shared = S.mem.alloc<ProgShared>(1, s, true);
             S.pv_sends = S.mem.alloc<unsigned long long>(1, s, true);
             S.pv_agg = S.mem.alloc<double>(1, s, true);
+            S.pv_mkey = S.mem.alloc<unsigned long long>(2, s, true);
+            S.pv_bound = S.mem.alloc<unsigned long long>(1, s, true);
             S.bits = S.mem.alloc<uint32_t>(words_of(p.rows), s, true);
             S.f_id = S.mem.alloc<int32_t>(p.rows, s);
             S.f_val = S.mem.alloc<uint32_t>(p.rows, s);

@@ -399,6 +399,8 @@ ipregel_status ipregel_program_create(const ipregel_program_desc* desc, ipregel_
     pr->sym = desc->symmetric;
     pr->agg_op = desc->aggregator - 1;   // -1 none, else SUM / MIN / MAX
     pr->sends = strstr(desc->source, "ipr_send") != nullptr;
+    pr->settled = strstr(desc->source, "ipr_settled") != nullptr &&
+                  desc->combiner == IPREGEL_COMBINE_MIN && !pr->sends;
     try {
         compile_program(pr, *desc);
     } catch (...) {

@@ -91,7 +91,62 @@ struct ProgArgs {
     int64_t vbase, rows, n;
     uint32_t superstep;
     int32_t sym;
+    // ipr_settled programs (NULL otherwise): the minimum message broadcast this superstep (order
+    // key, folded here) and the bound every message of this superstep is at least (computed by
+    // k_prog_bound from the previous superstep's minimum; ~0 = no broadcast at all)
+    unsigned long long* mkey_out;
+    const unsigned long long* bound;
+    uint32_t w_min;        // smallest edge weight (1 without weights)
 };
+
+// Order-preserving unsigned keys of the value types (atomicMin over any of them).
+template <class V> struct ProgKey;
+template <> struct ProgKey<uint32_t> {
+    __device__ static unsigned long long key(uint32_t x) { return x; }
+    __device__ static uint32_t value(unsigned long long k) { return (uint32_t)k; }
+};
+template <> struct ProgKey<int32_t> {
+    __device__ static unsigned long long key(int32_t x) { return (uint32_t)x ^ 0x80000000u; }
+    __device__ static int32_t value(unsigned long long k) { return (int32_t)((uint32_t)k ^ 0x80000000u); }
+};
+template <> struct ProgKey<uint64_t> {
+    __device__ static unsigned long long key(uint64_t x) { return x; }
+    __device__ static uint64_t value(unsigned long long k) { return k; }
+};
+template <> struct ProgKey<int64_t> {
+    __device__ static unsigned long long key(int64_t x) { return (unsigned long long)x ^ (1ull << 63); }
+    __device__ static int64_t value(unsigned long long k) { return (int64_t)(k ^ (1ull << 63)); }
+};
+template <> struct ProgKey<float> {
+    __device__ static unsigned long long key(float x) {
+        const uint32_t b = (uint32_t)__float_as_int(x);
+        return (b & 0x80000000u) ? (unsigned long long)(~b) : (unsigned long long)(b | 0x80000000u);
+    }
+    __device__ static float value(unsigned long long k) {
+        const uint32_t b = (uint32_t)k;
+        return __int_as_float((int)((b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b));
+    }
+};
+template <> struct ProgKey<double> {
+    __device__ static unsigned long long key(double x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+        return (b >> 63) ? ~b : (b | (1ull << 63));
+    }
+    __device__ static double value(unsigned long long k) {
+        return __longlong_as_double((long long)((k >> 63) ? (k & ~(1ull << 63)) : ~k));
+    }
+};
+
+// warp min of the broadcast keys, one atomic per warp
+__device__ __forceinline__ void flush_mkey(unsigned long long k, unsigned long long* out) {
+    if (!out) return;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, k, d);
+        k = o < k ? o : k;
+    }
+    if ((threadIdx.x & 31) == 0 && k != ~0ull) atomicMin(out, k);
+}
 
 // ---- combiners (commutative and associative) -----------------------------------
 template <class V, int kComb> struct ProgComb;
@@ -343,6 +398,12 @@ __device__ __forceinline__ void prog_emit(const ProgArgs<typename P::V>& A, int6
     using C = ProgComb<V, P::kCombiner>;
     const bool b = (f & kProgBroadcast) != 0;
     const V ob = b ? msg : C::identity();
+    if constexpr (P::kSettled) {
+        if (b) {
+            const unsigned long long k = ProgKey<V>::key(msg);
+            c.mkey = k < c.mkey ? k : c.mkey;
+        }
+    }
     A.out_next[A.vbase + row] = ob;
     A.peers.store(A.vbase + row, ob);
     const bool act = (f & kProgStayActive) != 0;
@@ -422,6 +483,7 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
         prog_emit<P, true>(A, row, x, f, msg, c);   // buffer 1 holds a previous run's values
     }
     flush_counters(c, s_cnt, counters);
+    if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }
 
@@ -435,13 +497,18 @@ struct ProgPull : ProgArgs<typename P::V> {
     using C = ProgComb<T, P::kCombiner>;
     static constexpr bool kWeighted = true;
     using Z = ProgAbsorb<T, P::kCombiner>;
+    // ipr_settled (MIN programs): every message of this superstep is >= *bound (k_prog_bound), so
+    // a row holding a settled value needs no gathers, and (integer values) a partial fold that is
+    // already <= the bound cannot drop further
+    static constexpr bool kSettledPartial =
+        P::kSettled && P::kCombiner == 1 && (T(3) / T(2) == T(1));   // integer types
     // optional ipr_absorbing(value): a vertex holding such a value ignores its messages, so its
     // row need not be gathered (and whole ranges of such rows are skipped).  Second half of a
     // symmetric pull: a row whose first-half mailbox already holds the combiner's absorbing
     // element needs no second-half gathers either; and any partial fold reaching it ends the
     // row's gathers (kAbsorbingPartial).
-    static constexpr bool kAbsorbing = P::kAbsorbing || (kPass == 2 && Z::kHas);
-    static constexpr bool kAbsorbingPartial = Z::kHas;
+    static constexpr bool kAbsorbing = P::kAbsorbing || (kPass == 2 && Z::kHas) || P::kSettled;
+    static constexpr bool kAbsorbingPartial = Z::kHas || kSettledPartial;
     static constexpr bool kAggregates = false;   // compute runs in k_prog_apply
     // 8-byte values: 3 CTAs per SM, as PageRankSum (PageRank program 79.7 -> 78.4 ms at cfg4)
 #ifndef IPREGEL_PROG_MINBLOCKS8
@@ -455,10 +522,24 @@ struct ProgPull : ProgArgs<typename P::V> {
     __device__ bool absorbed(int32_t row) const {
         if constexpr (kPass == 2 && Z::kHas)
             if (Z::is(this->mbox[row])) return true;
+        if constexpr (P::kSettled) {
+            if (this->bound) {
+                const unsigned long long b = *this->bound;
+                if (b == ~0ull || P::settled(this->value[row], ProgKey<T>::value(b))) return true;
+            }
+        }
         if constexpr (P::kAbsorbing) return P::absorbing(this->value[row]);
         return false;
     }
-    __device__ bool absorbing(T x) const { return Z::is(x); }
+    __device__ bool absorbing(T x) const {
+        if constexpr (kSettledPartial) {
+            if (this->bound) {
+                const unsigned long long b = *this->bound;
+                if (b == ~0ull || !(ProgKey<T>::value(b) < x)) return true;
+            }
+        }
+        return Z::is(x);
+    }
     __device__ static T message(T g, uint32_t w) { return P::edge(g, w); }
     // The range kernels only fold each row's messages into its mailbox; the user's compute
     // runs row-parallel in k_prog_apply (pull_all) -- the same split as the built-in PageRank,
@@ -541,6 +622,7 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     __syncwarp();   // both halves of a recipient word were read above
     if (base < A.rows && (base & 31) == 0) A.recv[base >> 5] = 0u;
     flush_counters(c, s_cnt, counters);
+    if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
 }
 
@@ -570,7 +652,21 @@ __global__ void __launch_bounds__(256) k_prog_pull_apply(ProgArgs<typename P::V>
     }
     __syncthreads();
     flush_counters(c, s_cnt, counters);
+    if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
+}
+
+// The bound of a pull superstep of an ipr_settled program: ipr_edge(smallest message broadcast in
+// the previous superstep, smallest edge weight) -- with ipr_edge monotone (the hint's contract)
+// no message of this superstep is below it.  ~0: nothing was broadcast.
+template <class P>
+__global__ void k_prog_bound(const unsigned long long* __restrict__ mkey_in, uint32_t w_min,
+                             unsigned long long* __restrict__ bound) {
+    using V = typename P::V;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const unsigned long long k = *mkey_in;
+        *bound = k == ~0ull ? ~0ull : ProgKey<V>::key(P::edge(ProgKey<V>::value(k), w_min));
+    }
 }
 
 }  // namespace ipr

@@ -70,6 +70,7 @@ struct LaneCounters {
     unsigned long long dmax;
     double agg;        // user programs: this thread's fold of ipr_aggregate values
     uint32_t agg_n;    //   (agg_n = 0: nothing folded)
+    unsigned long long mkey = ~0ull;   // user programs with ipr_settled: min broadcast (order key)
 };
 
 // Range plan for one adjacency of one partition.

@@ -6,7 +6,7 @@
 // user vertex programs: NVRTC compilation and the generic superstep loop
 // =============================================================================================
 enum { PK_INIT, PK_PULL0, PK_PULL1, PK_PULL2, PK_FIX0, PK_FIX1, PK_FIX2, PK_EXPAND, PK_APPLY,
-       PK_PULL_APPLY, PK_COUNT };
+       PK_PULL_APPLY, PK_BOUND, PK_COUNT };
 static const char* const kProgKernelNames[PK_COUNT] = {
     "ipr::k_prog_init<UserProgram>",
     "ipr::k_pull_ranges<ipr::ProgPull<UserProgram, 0> >",
@@ -18,6 +18,7 @@ static const char* const kProgKernelNames[PK_COUNT] = {
     "ipr::k_prog_expand<UserProgram>",
     "ipr::k_prog_apply<UserProgram>",
     "ipr::k_prog_pull_apply<UserProgram>",
+    "ipr::k_prog_bound<UserProgram>",
 };
 
 struct ipregel_program {
@@ -26,6 +27,7 @@ struct ipregel_program {
     int sym = 0;
     int agg_op = -1;      // aggregator (ipregel_combiner over f64), -1 none
     bool sends = false;   // the source calls ipr_send (point-to-point messages)
+    bool settled = false; // the source defines ipr_settled (MIN combiner, no ipr_send)
     std::vector<char> cubin;
     std::string log;
     std::string lowered[PK_COUNT];
@@ -120,6 +122,14 @@ std::string program_tu(const ipregel_program_desc& d) {
     s += std::string("  static constexpr bool kAggregates = ") +
          (d.aggregator != IPREGEL_AGG_NONE ? "true" : "false") + ";\n";
     const bool absorbing = strstr(d.source, "ipr_absorbing") != nullptr;
+    // ipr_settled: MIN programs without point-to-point sends (their messages bypass the bound)
+    const bool settled = strstr(d.source, "ipr_settled") != nullptr &&
+                         d.combiner == IPREGEL_COMBINE_MIN && !strstr(d.source, "ipr_send");
+    s += std::string("  static constexpr bool kSettled = ") + (settled ? "true" : "false") + ";\n";
+    if (settled)
+        s += "  static __device__ __forceinline__ bool settled(V v, V b) { return ipr_settled(v, b); }\n";
+    else
+        s += "  static __device__ __forceinline__ bool settled(V, V) { return false; }\n";
     s += std::string("  static constexpr bool kAbsorbing = ") + (absorbing ? "true" : "false") + ";\n";
     if (absorbing)
         s += "  static __device__ __forceinline__ bool absorbing(V v) { return ipr_absorbing(v); }\n";
@@ -288,6 +298,13 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
     if (pr->sends && np > kProgMaxParts)
         fail(IPREGEL_ERR_UNSUPPORTED, "ipr_send supports at most %d partitions", kProgMaxParts);
     const uint64_t ident = prog_identity_bits(pr);
+    // ipr_settled: one min-broadcast key pair and bound for the whole graph (partition 0's
+    // buffers, written by every loopback partition); not across ranks (it would need a
+    // collective per superstep)
+    const bool settle = pr->settled && !(multi_rank(g) && g->comm->world > 1);
+    unsigned long long* mkey = settle ? g->parts[0].st[app].pv_mkey : nullptr;
+    unsigned long long* bound = settle ? g->parts[0].st[app].pv_bound : nullptr;
+    const uint32_t wmin = settle ? min_weight(g) : 1u;
     const double agg_id = pr->agg_op == 0 ? 0.0 : (pr->agg_op == 1 ? INFINITY : -INFINITY);
     double agg_prev = agg_id;
     if (pr->sends || pr->agg_op >= 0) {
@@ -384,6 +401,9 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         a.n = n;
         a.superstep = step;
         a.sym = sym ? 1 : 0;
+        a.mkey_out = settle ? mkey + (step & 1u) : nullptr;
+        a.bound = settle ? bound : nullptr;
+        a.w_min = wmin;
         return a;
     };
     auto exchange = [&](int w) {
@@ -401,6 +421,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
         CU(cudaMemsetAsync(S.pv_recv, 0, words_of(p.rows) * 4, s));
     }
+    if (settle) CU(cudaMemsetAsync(mkey, 0xFF, sizeof(unsigned long long), s));
     reset_extras();
     T0.kbegin();
     for (auto& p : g->parts) {
@@ -436,6 +457,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         T.begin();
         const uint64_t frontier_len = changed;
         for (auto& p : g->parts) CU(cudaMemsetAsync(p.pull_cnt, 0, sizeof(PullCounters), s));
+        if (settle) CU(cudaMemsetAsync(mkey + (step & 1u), 0xFF, sizeof(unsigned long long), s));
         reset_extras();
         if (mode == 2) {
             if (prev_mode == 1) {   // a pull left folded mailboxes behind: back to the identity
@@ -482,6 +504,12 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             T.kend();
         } else {
             T.kbegin();
+            if (settle) {   // the bound of this pull from the previous superstep's broadcasts
+                const unsigned long long* kin = mkey + ((step - 1) & 1u);
+                uint32_t w = wmin;
+                void* bargs[] = {&kin, &w, &bound};
+                launch_jit(pr->k[PK_BOUND], 1, 32, bargs, s);
+            }
             for (auto& p : g->parts) {
                 if (p.rows == 0) continue;
                 ProgArgs<V> a = args_for(p, step, cur);

@@ -74,6 +74,9 @@ __device__ unsigned ipr_compute(const ipr_ctx&, unsigned* value, unsigned mailbo
 __device__ unsigned ipr_edge(unsigned message, unsigned weight) {
     return ipr_sat_add(message, weight);                   // value + w, saturating (R9)
 }
+// hint: compute lowers a value only to a smaller mailbox and ipr_edge is monotone, so a vertex
+// at or below the superstep's message bound cannot change (its gathers are skipped)
+__device__ bool ipr_settled(unsigned value, unsigned bound) { return value <= bound; }
 """
 
 # Breadth-first levels from params[0]: Fig. 10 exactly (every edge adds 1, weights ignored).
@@ -158,6 +161,9 @@ __device__ unsigned ipr_compute(const ipr_ctx&, double* value, double mailbox, d
     return 0;
 }
 __device__ double ipr_edge(double message, unsigned weight) { return message + (double)weight; }
+// hint: compute lowers a value only to a smaller mailbox and ipr_edge is monotone, so a vertex
+// at or below the superstep's message bound cannot change (its gathers are skipped)
+__device__ bool ipr_settled(double value, double bound) { return value <= bound; }
 """
 
 # PageRank to convergence with a Pregel aggregator (PAPER.md:322): every vertex folds its rank
@@ -236,6 +242,9 @@ __device__ unsigned ipr_compute(const ipr_ctx&, float* value, float mailbox, flo
     return 0;
 }
 __device__ float ipr_edge(float message, unsigned weight) { return message + (float)weight; }
+// hint: compute lowers a value only to a smaller mailbox and ipr_edge is monotone, so a vertex
+// at or below the superstep's message bound cannot change (its gathers are skipped)
+__device__ bool ipr_settled(float value, float bound) { return value <= bound; }
 """
 
 SSSP_I32 = r"""
@@ -259,6 +268,9 @@ __device__ unsigned ipr_compute(const ipr_ctx&, int* value, int mailbox, int* me
 __device__ int ipr_edge(int message, unsigned weight) {
     return message == 0x7FFFFFFF ? message : message + (int)weight;
 }
+// hint: compute lowers a value only to a smaller mailbox and ipr_edge is monotone, so a vertex
+// at or below the superstep's message bound cannot change (its gathers are skipped)
+__device__ bool ipr_settled(int value, int bound) { return value <= bound; }
 """
 
 HASHMIN_U64 = r"""
