@@ -32,6 +32,10 @@ namespace ipr {
 #ifndef IPREGEL_IDX_PREFETCH
 #define IPREGEL_IDX_PREFETCH 0
 #endif
+// u32 min ops take the one-row-end path too (two redux.sync.min instead of the scan)
+#ifndef IPREGEL_U32_ONE_END
+#define IPREGEL_U32_ONE_END 1
+#endif
 #ifndef IPREGEL_CHUNK_UNROLL
 #define IPREGEL_CHUNK_UNROLL 1   // chunk-loop unroll (2: CC +0.3 ms, SSSP +0.2 ms, PageRank equal; 4: all slower)
 #endif
@@ -136,6 +140,7 @@ struct SumF64 {
 };
 struct MinU32 {
     using T = uint32_t;
+    static constexpr bool kReduxMin = true;   // warp folds by redux.sync.min (min is exact)
     __device__ static T identity() { return kInf; }
     __device__ static T combine(T a, T b) { return a > b ? b : a; }   // Fig. 5 ip_combine
 };
@@ -426,9 +431,16 @@ __device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned
     }
 }
 
-// Fixed xor-tree reduction of a lane-private partial (result on every lane).
+template <class Op, class = void> struct ReduxMin { static constexpr bool value = false; };
+template <class Op> struct ReduxMin<Op, void_t_<decltype(Op::kReduxMin)>> {
+    static constexpr bool value = Op::kReduxMin;
+};
+
+// Fixed xor-tree reduction of a lane-private partial (result on every lane); u32 min ops use
+// the warp-reduce instruction (min is order-independent, so exact either way).
 template <class Op>
 __device__ __forceinline__ typename Op::T warp_fold(typename Op::T x) {
+    if constexpr (ReduxMin<Op>::value) return __reduce_min_sync(kFull, x);
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -551,7 +563,8 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
             }
             continue;
         }
-        if (sizeof(T) == 8 && !part_head && Ec > e0 && En > e0 + kChunk) {
+        if ((sizeof(T) == 8 || (IPREGEL_U32_ONE_END && ReduxMin<Op>::value)) && !part_head &&
+            Ec > e0 && En > e0 + kChunk) {
             // exactly one row (r) ends inside the chunk and the next one runs past it -- the
             // common case for rows of a few hundred edges: two masked warp folds instead of the
             // segmented scan (positions < p close row r, the rest open row r + 1).  8-byte values
@@ -565,7 +578,12 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
                 else t2 = Op::combine(t2, v[k]);
             }
             T f1, f2;
-            warp_fold2<Op>(t1, t2, f1, f2);
+            if constexpr (ReduxMin<Op>::value) {   // two warp-reduce instructions
+                f1 = __reduce_min_sync(kFull, t1);
+                f2 = __reduce_min_sync(kFull, t2);
+            } else {
+                warp_fold2<Op>(t1, t2, f1, f2);
+            }
             const T total = Op::combine(Op::combine(carry, warp_fold<Op>(la)), f1);
             carry = f2;
             la = Op::identity();
