@@ -509,6 +509,8 @@ struct ProgPull : ProgArgs<typename P::V> {
     // row's gathers (kAbsorbingPartial).
     static constexpr bool kAbsorbing = P::kAbsorbing || (kPass == 2 && Z::kHas) || P::kSettled;
     static constexpr bool kAbsorbingPartial = Z::kHas || kSettledPartial;
+    // u32 / i32 MIN: warp folds by redux.sync.min (exact in any order), one-row-end chunk path
+    static constexpr bool kReduxMin = sizeof(T) == 4 && P::kCombiner == 1 && (T(3) / T(2) == T(1));
     static constexpr bool kAggregates = false;   // compute runs in k_prog_apply
     // 8-byte values: 3 CTAs per SM, as PageRankSum (PageRank program 79.7 -> 78.4 ms at cfg4)
 #ifndef IPREGEL_PROG_MINBLOCKS8
