@@ -53,7 +53,7 @@ void compute_fence(cudaStream_t s) {
 
 // windows of the CSC weights' upload when the CSR is derived (the last window's permutation is
 // all that remains after the upload)
-constexpr int kWeightWindows = 8;
+constexpr int kWeightWindows = 16;   // 8: +1.3 ms, 32: +18 ms (create at cfg4)
 
 void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
     cudaStream_t s = g->stream;
