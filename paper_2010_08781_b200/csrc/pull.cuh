@@ -7,17 +7,20 @@
 //
 // Work decomposition (B200-first; the paper's OpenMP static vertex split, is
 // prior art): the merge of the two sorted lists {row ends} and {in-edges} is cut into fixed
-// RANGES of kRangeItems items (merge path), one warp each, so every warp gets the same number of
-// edges + rows whatever the degree distribution (hub rows of in-degree ~1.5M at scale 26, long
-// runs of rows without in-edges) -- no degree binning pass, no shared-memory staging, no block
-// barrier.  A warp walks the edges of its range in CHUNKS of 128 (4 per lane):
+// RANGES of kRangeItems items (merge path), so every range holds the same number of edges + rows
+// whatever the degree distribution (hub rows of in-degree ~1.5M at scale 26, long runs of rows
+// without in-edges) -- no degree binning pass, no shared-memory staging, no block barrier.  One
+// resident wave of CTAs runs; each warp takes range after range from an atomic counter.  A warp
+// walks the edges of its range in CHUNKS of 128 (4 per lane):
 //   1. column indices arrive with coalesced L2-evict-first loads two chunks ahead and the
 //      outbox values are gathered one chunk ahead (software pipeline, 8 gathers in flight per
 //      lane); each gather instruction reads the sources of 32 consecutive edges;
 //   2. a chunk inside one row (most edges: long rows) only adds into lane-private accumulators;
-//   3. a chunk where rows end builds a 128-bit head-flag mask from the CSC offsets
-//      (__reduce_or_sync), folds it with four 5-step segmented shuffle scans (segment starts read
-//      off the uniform flag words), and each row ending there reads its sum from a per-warp slot
+//   3. a chunk where exactly one row ends closes it with two masked warp folds; a chunk where
+//      more rows end builds a 128-bit head-flag mask from the CSC offsets (__reduce_or_sync),
+//      folds it with four 5-step segmented shuffle scans (segment starts read off the uniform
+//      flag words; 8-byte values close the first and last segments with the same masked folds
+//      as the one-end chunks), and each row ending there reads its sum from a per-warp slot
 //      array and runs the recipient compute (fused epilogue);
 //   4. a row cut by a range boundary is joined by k_pull_fixup in a fixed order.
 // Range boundaries sit at multiples of kRangeItems in GLOBAL merge coordinates and chunks at
