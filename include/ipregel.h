@@ -309,7 +309,8 @@ ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
  * message and the weight; the library then takes bound = ipr_edge(smallest message broadcast in
  * the previous superstep, smallest edge weight) for each pull superstep and skips the gathers
  * of settled vertices (and, for integer values, of rows whose partial fold is <= bound) --
- * SSSP's "distance <= min frontier distance + min weight" (one GPU: whole graph or loopback).
+ * SSSP's "distance <= min frontier distance + min weight" (across ranks the minimum is
+ * all-reduced each superstep).
  * The run ends when a superstep has no broadcast and no active vertex.
  * Selection (R28): push supersteps run compute on recipients and active vertices
  * only; pull supersteps run it on every vertex, the non-recipients getting the identity, so a

@@ -299,12 +299,17 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         fail(IPREGEL_ERR_UNSUPPORTED, "ipr_send supports at most %d partitions", kProgMaxParts);
     const uint64_t ident = prog_identity_bits(pr);
     // ipr_settled: one min-broadcast key pair and bound for the whole graph (partition 0's
-    // buffers, written by every loopback partition); not across ranks (it would need a
-    // collective per superstep)
-    const bool settle = pr->settled && !(multi_rank(g) && g->comm->world > 1);
+    // buffers, written by every loopback partition; across ranks the superstep's key is
+    // all-reduced with ncclMin)
+    const bool settle = pr->settled;
     unsigned long long* mkey = settle ? g->parts[0].st[app].pv_mkey : nullptr;
     unsigned long long* bound = settle ? g->parts[0].st[app].pv_bound : nullptr;
     const uint32_t wmin = settle ? min_weight(g) : 1u;
+    auto settle_allreduce = [&](uint32_t step) {
+        if (settle && multi_rank(g))
+            NC(ncclAllReduce(mkey + (step & 1u), mkey + (step & 1u), 1, ncclUint64, ncclMin,
+                             g->comm->nccl, s));
+    };
     const double agg_id = pr->agg_op == 0 ? 0.0 : (pr->agg_op == 1 ? INFINITY : -INFINITY);
     double agg_prev = agg_id;
     if (pr->sends || pr->agg_op >= 0) {
@@ -432,6 +437,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
     }
     T0.kend();
     exchange(0);
+    settle_allreduce(0);
     unsigned long long c[4];
     reduce_counters(g, false, c, 4);
     uint64_t sends = 0;
@@ -534,6 +540,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
             T.kend();
         }
         exchange(1 - cur);
+        settle_allreduce(step);
         reduce_counters(g, false, c, 4);
         fold_extras(&sends, &agg_prev);
         T.end();

@@ -473,6 +473,14 @@ def test_nccl_path_single_rank_matches_oracle(exchange):
         G.run("pagerank", mode=mode, exchange=exchange)
         assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
         np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
+    # a user program on the rank path (the ipr_settled minimum is all-reduced with NCCL)
+    from paper_2010_08781_b200 import programs
+    p = programs.compile("sssp")
+    o = oracle.sssp(n, src, dst, w, source=5)
+    for mode in ("pull", "auto"):
+        G.run_program(p, params=[5], mode=mode, exchange=exchange)
+        np.testing.assert_array_equal(G.values(host=True), o["values"])
+        np.testing.assert_array_equal(G.stats()["changed"], o["changed"])
     G.close()
     comm.close()
 
