@@ -105,7 +105,8 @@ def test_library_fails_loudly_without_gpu():
 
 def test_product_path_never_imports_the_oracle():
     """The oracle is test infrastructure: the package (and its program catalog) must not import
-    it, and no product source mentions it as a module."""
+    it, and no product, input-generator or tool source mentions it as a module (only tests/,
+    smoke() and bench.py's cpu_baseline / --impl reference legs use it)."""
     import subprocess
     import sys
     code = ("import sys; import paper_2010_08781_b200, paper_2010_08781_b200.programs; "
@@ -113,9 +114,10 @@ def test_product_path_never_imports_the_oracle():
     out = subprocess.check_output([sys.executable, "-c", code],
                                   cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.decode().strip() == "False"
-    pkg = os.path.join(os.path.dirname(__file__), "..", "paper_2010_08781_b200")
-    for root, _, files in os.walk(pkg):
-        for f in files:
-            if f.endswith((".py", ".cu", ".cuh", ".h")):
-                text = open(os.path.join(root, f)).read()
-                assert "import oracle" not in text and "oracle/" not in text, f
+    repo = os.path.join(os.path.dirname(__file__), "..")
+    for sub in ("paper_2010_08781_b200", "tools", "inputs", "include"):
+        for root, _, files in os.walk(os.path.join(repo, sub)):
+            for f in files:
+                if f.endswith((".py", ".cu", ".cuh", ".h", ".c")):
+                    text = open(os.path.join(root, f)).read()
+                    assert "import oracle" not in text and "oracle/" not in text, f

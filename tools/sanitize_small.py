@@ -7,7 +7,6 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-import oracle  # noqa: E402
 from tests import checkers  # noqa: E402
 from tests.graphs import csr_csc, make_graph  # noqa: E402
 
@@ -38,5 +37,4 @@ for parts in (1, 3):
                                   exchange=ex)
                     v = G.values(host=True)
     G.close()
-o = oracle.sssp(n, src, dst, w)
-print("ok", int((o["values"] != oracle.INF).sum()))
+print("ok")   # a run-everything smoke; parity against the oracle lives in tests/ only
