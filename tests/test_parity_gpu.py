@@ -701,3 +701,30 @@ def test_pagerank_pull_bit_identical_random_bounds(exchange):
         Gp.run("pagerank", mode="pull", exchange=exchange)
         np.testing.assert_array_equal(Gp.values(host=True), v1, err_msg=str(bounds.tolist()))
         Gp.close()
+
+
+@pytest.mark.parametrize("n,m", [(1, 0), (5, 0), (7, 3), (300, 40000)])
+def test_host_create_derived_csr_small_and_empty(n, m, monkeypatch):
+    """The host-memory create pipeline (structure upload, derived CSR, weight windows permuted on
+    a side stream, kernel-copy readbacks) on empty, tiny and duplicate-heavy graphs."""
+    import paper_2010_08781_b200 as ipr
+    monkeypatch.setenv("IPREGEL_WEIGHT_WINDOWS", "3")
+    rng = np.random.default_rng(n + m)
+    src = rng.integers(0, n, m)
+    dst = rng.integers(0, n, m)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    w = rng.integers(0, 50, len(src)).astype(np.uint32)
+    g = csr_csc(n, src, dst, w)
+    h = {k: np.ascontiguousarray(g[k]).view(np.int32) for k in ("csc_off", "csc_idx", "csc_w")}
+    G = ipr.Graph(ipr.Partition(n, g["e"], 0, n, h["csc_off"], h["csc_idx"], None, None,
+                                h["csc_w"], None), validate=True)
+    for mode in ("pull", "push", "auto"):
+        G.run("cc", mode=mode)
+        np.testing.assert_array_equal(G.values(host=True), oracle.hashmin_cc(n, src, dst)["values"])
+        G.run("sssp", mode=mode, source=0)
+        np.testing.assert_array_equal(G.values(host=True),
+                                      oracle.sssp(n, src, dst, w, source=0)["values"])
+    G.run("pagerank", mode="pull")
+    assert np.abs(G.values(host=True) - oracle.pagerank(n, src, dst)["values"]).max() <= PR_ABS
+    G.close()
