@@ -266,6 +266,17 @@ ipregel_status ipregel_run(ipregel_graph* graph, ipregel_app app, ipregel_combin
 ipregel_status ipregel_get_values(ipregel_graph* graph, void* out, size_t out_bytes,
                                   int out_is_device);
 
+/* Asynchronous ipregel_get_values into HOST memory: the last run's N values are staged on the
+ * device (a private copy, so later runs -- of any app -- do not affect them) and copied to `out`
+ * on the library's copy stream while the caller goes on (e.g. with the next run); `out` is
+ * complete once ipregel_graph_sync returns (destroy also waits).  `out` should be pinned
+ * (cudaHostAlloc / registered); pageable memory makes the copy synchronous.  Same size rules and
+ * errors as ipregel_get_values; one GPU or loopback partitions (ranks: UNSUPPORTED). */
+ipregel_status ipregel_get_values_async(ipregel_graph* graph, void* out, size_t out_bytes);
+
+/* Waits for every asynchronous copy of the graph (ipregel_get_values_async). */
+ipregel_status ipregel_graph_sync(ipregel_graph* graph);
+
 /* Fills the caller-owned arrays of *inout (up to capacity entries) for the last run. */
 ipregel_status ipregel_get_stats(ipregel_graph* graph, ipregel_stats* inout);
 

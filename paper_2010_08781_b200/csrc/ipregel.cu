@@ -488,6 +488,71 @@ ipregel_status ipregel_run_program(ipregel_graph* g, ipregel_program* program,
     ABI_END
 }
 
+ipregel_status ipregel_get_values_async(ipregel_graph* g, void* out, size_t out_bytes) {
+    ABI_BEGIN
+    if (!g || !out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph or out is NULL");
+    if (g->poisoned) fail(IPREGEL_ERR_STATE, "graph handle was poisoned");
+    if (g->last_app < 0) fail(IPREGEL_ERR_STATE, "no completed run");
+    if (multi_rank(g)) fail(IPREGEL_ERR_UNSUPPORTED, "ipregel_get_values_async across ranks");
+    const bool owned = g->last_app == IPREGEL_APP_PAGERANK || g->last_app == kAppProgram;
+    const size_t esz = (size_t)g->last_vsz;
+    if (out_bytes != (size_t)g->n * esz)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "out_bytes %zu != N * %zu", out_bytes, esz);
+    cudaStream_t s = g->stream;
+    try {
+        if (!g->copy_stream) CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+        // a private staging vector in original order, built by kernels on the run stream (no
+        // copy-engine work there: see compute_fence), then a device -> host copy on the copy
+        // stream, after which the staging buffer goes back to the pool
+        uint8_t* stage = nullptr;
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&stage), (size_t)g->n * esz, s));
+        uint8_t* full = stage;
+        if (g->vertex_ids) {
+            if (!g->gather_tmp) g->gather_tmp = g->graph_mem.alloc<double>(g->n, s);
+            full = reinterpret_cast<uint8_t*>(g->gather_tmp);
+        }
+        for (auto& p : g->parts) {
+            const void* src = owned ? (g->last_app == IPREGEL_APP_PAGERANK
+                                           ? (const void*)p.st[0].rank
+                                           : p.st[kAppProgram].pv_value)
+                                    : (const void*)(reinterpret_cast<const uint8_t*>(
+                                           p.st[g->last_app].val[g->cur]) + p.vb * esz);
+            if (p.rows) kernel_copy(full + p.vb * esz, src, p.rows * esz, s);
+        }
+        if (g->vertex_ids) {
+            if (esz == 8)
+                k_to_original<double><<<grid_for(g->n, 256), 256, 0, s>>>(
+                    (const double*)full, g->vertex_ids, g->n, (double*)stage);
+            else
+                k_to_original<uint32_t><<<grid_for(g->n, 256), 256, 0, s>>>(
+                    (const uint32_t*)full, g->vertex_ids, g->n, (uint32_t*)stage);
+            LAUNCH_CHECK();
+        }
+        cudaEvent_t ready;
+        CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CU(cudaEventRecord(ready, s));
+        compute_fence(g->copy_stream);   // its latest op may be a copy (see compute_fence)
+        CU(cudaStreamWaitEvent(g->copy_stream, ready, 0));
+        CU(cudaEventDestroy(ready));     // released once the wait has been recorded
+        CU(cudaMemcpyAsync(out, stage, (size_t)g->n * esz, cudaMemcpyDeviceToHost, g->copy_stream));
+        CU(cudaFreeAsync(stage, g->copy_stream));
+    } catch (const Failure& f) {
+        if (f.status == IPREGEL_ERR_CUDA || f.status == IPREGEL_ERR_NCCL) g->poisoned = true;
+        throw;
+    }
+    return IPREGEL_OK;
+    ABI_END
+}
+
+ipregel_status ipregel_graph_sync(ipregel_graph* g) {
+    ABI_BEGIN
+    if (!g) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph is NULL");
+    if (g->copy_stream) CU(cudaStreamSynchronize(g->copy_stream));
+    CU(cudaStreamSynchronize(g->stream));
+    return IPREGEL_OK;
+    ABI_END
+}
+
 ipregel_status ipregel_get_values(ipregel_graph* g, void* out, size_t out_bytes,
                                   int out_is_device) {
     ABI_BEGIN

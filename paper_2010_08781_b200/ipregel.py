@@ -96,7 +96,8 @@ EXPORTS = [
     "ipregel_run_params_default", "ipregel_nccl_unique_id", "ipregel_comm_create",
     "ipregel_comm_destroy", "ipregel_partition", "ipregel_graph_create",
     "ipregel_graph_create_partitioned", "ipregel_graph_destroy", "ipregel_memory_footprint",
-    "ipregel_run", "ipregel_get_values", "ipregel_get_stats",
+    "ipregel_run", "ipregel_get_values", "ipregel_get_values_async", "ipregel_graph_sync",
+    "ipregel_get_stats",
     "ipregel_program_create", "ipregel_program_log", "ipregel_program_cubin_bytes",
     "ipregel_program_destroy", "ipregel_run_program",
 ]
@@ -133,6 +134,8 @@ def load() -> ctypes.CDLL:
                                          ctypes.POINTER(ctypes.c_uint64)]),
         "ipregel_run": (I, [P, I, I, ctypes.c_uint32, ctypes.POINTER(RunParams)]),
         "ipregel_get_values": (I, [P, P, ctypes.c_size_t, I]),
+        "ipregel_get_values_async": (I, [P, P, ctypes.c_size_t]),
+        "ipregel_graph_sync": (I, [P]),
         "ipregel_get_stats": (I, [P, ctypes.POINTER(Stats)]),
         "ipregel_program_create": (I, [ctypes.POINTER(ProgramDesc), ctypes.POINTER(P)]),
         "ipregel_program_log": (ctypes.c_char_p, [P]),
@@ -391,6 +394,17 @@ class Graph:
         self.last_app = APP_PROGRAM
         self._last_vt = program.value_type
         return st
+
+    def values_async(self, out):
+        """Start copying the last run's values into `out` (a pinned CPU torch tensor of N
+        elements); complete after sync()."""
+        _check(load().ipregel_get_values_async(self.handle, out.data_ptr(),
+                                               out.numel() * out.element_size()),
+               "ipregel_get_values_async")
+        return out
+
+    def sync(self):
+        _check(load().ipregel_graph_sync(self.handle), "ipregel_graph_sync")
 
     def values(self, out=None, host: bool = False):
         """Full N-vector of the last run: torch CUDA tensor (default) or numpy (host=True)."""

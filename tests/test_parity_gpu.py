@@ -728,3 +728,37 @@ def test_host_create_derived_csr_small_and_empty(n, m, monkeypatch):
     G.run("pagerank", mode="pull")
     assert np.abs(G.values(host=True) - oracle.pagerank(n, src, dst)["values"]).max() <= PR_ABS
     G.close()
+
+
+@pytest.mark.parametrize("ids", [False, True])
+def test_get_values_async_matches_sync(ids):
+    """ipregel_get_values_async: each app's values staged privately and copied on the copy
+    stream while the next app runs; after sync they equal the synchronous readback."""
+    import torch
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    rng = np.random.default_rng(41)
+    n = 5000
+    src, dst, w = checkers.random_graph(rng, n, 40000, weighted=True)
+    perm = rng.permutation(n) if ids else np.arange(n)
+    g = csr_csc(n, perm[src], perm[dst], w)
+    d = to_device(g)
+    vid = None
+    if ids:
+        inv = np.empty(n, np.int32)
+        inv[perm] = np.arange(n, dtype=np.int32)
+        vid = torch.from_numpy(inv).cuda()
+    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"],
+                                     d["csr_idx"], d["csc_w"], d["csr_w"], vertex_ids=vid))
+    want, got = {}, {}
+    for app in ("pagerank", "cc", "sssp"):
+        G.run(app)
+        want[app] = G.values(host=True).copy()
+        got[app] = torch.empty(n, dtype=torch.float64 if app == "pagerank" else torch.int32,
+                               pin_memory=True)
+        G.values_async(got[app])
+    G.run("pagerank", iterations=3)   # a later run of an app already read must not matter
+    G.sync()
+    for app in want:
+        np.testing.assert_array_equal(got[app].numpy().view(want[app].dtype), want[app])
+    G.close()
