@@ -353,8 +353,13 @@ def main():
 
     # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = e2e_measure(g, args, msgs, stream)
+    G.close()   # its device state goes back to the pool for the e2e graphs
+    G = None
+    if not args.no_e2e:
+        if use_comm:
+            e2e = e2e_measure_ranks(part, n, e, args, msgs, stream, comm, world)
+        else:
+            e2e = e2e_measure(g, args, msgs, stream)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -377,11 +382,81 @@ def main():
         line["cpu_baseline"].pop("apps", None)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    G.close()
     if comm:
         comm.close()
     if use_comm:
         dist.destroy_process_group()
+
+
+def e2e_measure_ranks(part, n, e, args, msgs_per_step, stream, comm, world):
+    """e2e on the rank path (torchrun, N >= 1 with a communicator): every rank creates its
+    partition from pinned host copies of its CSC + CSR slices (+ weights, vertex layout), runs
+    the apps and reads every result back (ipregel_get_values: collective, every rank receives
+    all N values).  Device time of the slowest rank; bytes summed over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_08781_b200 as ipr
+
+    def pin(t):
+        if t is None:
+            return None, 0
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h, h.numel() * h.element_size()
+
+    hs, h2d = {}, 0
+    for k in ("csc_offsets", "csc_indices", "csc_weights", "csr_offsets", "csr_indices",
+              "csr_weights", "vertex_ids"):
+        hs[k], b = pin(getattr(part, k))
+        h2d += b
+    hpart = ipr.Partition(n, e, part.vertex_begin, part.vertex_end,
+                          *[None if hs[k] is None else hs[k].numpy() for k in
+                            ("csc_offsets", "csc_indices", "csr_offsets", "csr_indices",
+                             "csc_weights", "csr_weights", "vertex_ids")], True)
+    outs = {app: torch.empty(n, dtype=torch.float64 if app == "pagerank" else torch.int32,
+                             pin_memory=True) for app in args.apps}
+    d2h = sum(o.numel() * o.element_size() for o in outs.values())
+    steps = max(1, min(args.steps, 3))
+
+    def one():
+        G = ipr.Graph(hpart, comm=comm, stream=stream)
+        lib = ipr.load()
+        for app in args.apps:
+            G.run(app, mode="pull" if app == "pagerank" else "auto")
+            o = outs[app]
+            assert lib.ipregel_get_values(G.handle, o.data_ptr(), o.numel() * o.element_size(),
+                                          0) == 0, ipr.last_error()
+        G.close()
+
+    one()  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        one()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall = (time.perf_counter() - t0) / steps
+    each = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    t = torch.tensor([ev[0].elapsed_time(ev[steps]) / steps, float(h2d), float(d2h)],
+                     device="cuda", dtype=torch.float64)
+    tmax = t[:1].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tsum = t[1:].clone()
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    ms = float(tmax.item())
+    return {"value": msgs_per_step / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": int(tsum[0].item()), "d2h_bytes_per_step": int(tsum[1].item()),
+            "ms_per_step": ms, "wall_ms_per_step": wall * 1e3,
+            "ms_each_step": [round(x, 2) for x in each], "steps": steps, "ranks": world,
+            "path": "per rank: ipregel_graph_create(IPREGEL_MEMORY_HOST, pinned CSC + CSR slices + "
+                    "weights + vertex ids, communicator) + ipregel_run x apps + "
+                    "ipregel_get_values(host, collective) + destroy; max over ranks, bytes "
+                    "summed over ranks"}
 
 
 def e2e_measure(g, args, msgs_per_step, stream):
@@ -424,7 +499,8 @@ def e2e_measure(g, args, msgs_per_step, stream):
         assert lib.ipregel_graph_sync(G.handle) == 0, ipr.last_error()
         G.close()
 
-    one()  # warm-up
+    for _ in range(2):   # warm-up (the pool and pinned pages settle over the first steps)
+        one()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]

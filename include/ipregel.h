@@ -34,7 +34,7 @@
  *   - One host thread at a time per handle.
  *   - Library-owned device memory comes from the device's default stream-ordered pool
  *     (cudaMallocAsync); freed memory is kept for later graphs up to IPREGEL_POOL_RETAIN_BYTES
- *     (environment, default 96 GiB), so creating and destroying graphs stays cheap.
+ *     (environment, default 144 GiB), so creating and destroying graphs stays cheap.
  */
 #ifndef IPREGEL_H
 #define IPREGEL_H

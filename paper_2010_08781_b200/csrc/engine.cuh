@@ -103,7 +103,7 @@ struct ipregel_comm {
 namespace {
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync), which keeps up to
-// IPREGEL_POOL_RETAIN_BYTES (default 96 GiB) of freed memory for the next graph instead of
+// IPREGEL_POOL_RETAIN_BYTES (default 144 GiB) of freed memory for the next graph instead of
 // returning it to the driver: creating and destroying a graph handle per job stays cheap (a
 // plain cudaMalloc/cudaFree of the 7.5 GB adjacency copies costs ~100 ms each).  Buffers another
 // process maps with CUDA IPC (fused-exchange replicas of a rank) use cudaMalloc.
@@ -117,7 +117,7 @@ void configure_pool(int device) {
         return;
     }
     const char* e = getenv("IPREGEL_POOL_RETAIN_BYTES");
-    uint64_t keep = e ? strtoull(e, nullptr, 10) : (96ull << 30);
+    uint64_t keep = e ? strtoull(e, nullptr, 10) : (144ull << 30);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
 }
 
@@ -596,7 +596,9 @@ void ensure_state(ipregel_graph* g, int app) {
         if (S.ready) continue;
         cudaStream_t s = g->stream;
         const int64_t n = g->n;
-        const bool ipc = multi_rank(g);   // replicas a peer maps for the fused exchange
+        // replicas a peer maps for the fused exchange (cudaMalloc: IPC-exportable); a world of one
+        // rank has no peer, so its replicas stay in the stream-ordered pool
+        const bool ipc = multi_rank(g) && g->comm->world > 1;
         if (app == IPREGEL_APP_PAGERANK) {
             S.rank = S.mem.alloc<double>(p.rows, s);
             S.contrib[0] = S.mem.alloc<double>(n, s, true, ipc);
@@ -926,6 +928,11 @@ void setup_ipc_peers(ipregel_graph* g, int app) {
     if (S.peers_state != 0) return;
     cudaStream_t s = g->stream;
     const int world = g->comm->world, rank = g->comm->rank;
+    if (world == 1) {   // no peer: the fused exchange stores nowhere but the own replica
+        S.npeer = 0;
+        S.peers_state = 1;
+        return;
+    }
     constexpr size_t H = sizeof(cudaIpcMemHandle_t);
     unsigned long long bad = world - 1 > kMaxPeers ? 1ull : 0ull;
     std::vector<uint8_t> mine(2 * H, 0), all(2 * H * world, 0);
