@@ -417,7 +417,7 @@ def e2e_measure_ranks(part, n, e, args, msgs_per_step, stream, comm, world):
     outs = {app: torch.empty(n, dtype=torch.float64 if app == "pagerank" else torch.int32,
                              pin_memory=True) for app in args.apps}
     d2h = sum(o.numel() * o.element_size() for o in outs.values())
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
 
     def one():
         G = ipr.Graph(hpart, comm=comm, stream=stream)
@@ -481,7 +481,7 @@ def e2e_measure(g, args, msgs_per_step, stream):
     outs = {app: torch.empty(g["n"], dtype=torch.float64 if app == "pagerank" else torch.int32,
                              pin_memory=True) for app in args.apps}
     d2h = 0
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
 
     def one():
         # each app's values are copied to pinned host memory asynchronously (the copy overlaps
