@@ -346,11 +346,17 @@ namespace {
 bool multi_rank(const ipregel_graph* g) { return g->comm != nullptr; }
 
 void check_device(int device) {
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10 || prop.minor != 0)
+    // the compute capability only (cudaGetDeviceProperties measured 5-190 ms per call inside
+    // graph creation), checked once per device
+    static int ok[64] = {};
+    if (device >= 0 && device < 64 && ok[device]) return;
+    int major = 0, minor = 0;
+    CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CU(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
         fail(IPREGEL_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
-             device, prop.major, prop.minor);
+             device, major, minor);
+    if (device >= 0 && device < 64) ok[device] = 1;
 }
 
 // Copies through a kernel (UVA: either side may be pinned host memory).  Create uses them for

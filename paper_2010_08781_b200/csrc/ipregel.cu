@@ -171,6 +171,7 @@ void ipregel_comm_destroy(ipregel_comm* comm) {
 static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipregel_comm* comm,
                                     void* stream, ipregel_graph** out) {
     ABI_BEGIN
+    const auto t_entry = std::chrono::steady_clock::now();
     if (!out) fail(IPREGEL_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (!descs || np < 1) fail(IPREGEL_ERR_INVALID_ARGUMENT, "no partition descriptors");
@@ -250,6 +251,10 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
         }
         g->degree_ordered = descs[0].degree_ordered != 0;
         g->gather_policy = g_gather_policy >= 0 ? g_gather_policy : (g->degree_ordered ? 3 : 1);
+        if (g_ctrace.on)
+            fprintf(stderr, "[ipregel create] host entry -> begin    %9.2f ms\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                              t_entry).count());
         g_ctrace.mark("create begin", g->stream);
         if (descs[0].vertex_ids) {
             if (descs[0].memory == IPREGEL_MEMORY_HOST) {

@@ -22,7 +22,7 @@ del g
 torch.cuda.empty_cache()
 out_pr = torch.empty(n, dtype=torch.float64, pin_memory=True)
 out_u = torch.empty(n, dtype=torch.int32, pin_memory=True)
-for derive in (True, False, True, True, True):
+for derive in (True, False) + (True,) * 8:
     if derive:
         part = ipr.Partition(n, e, 0, n, host["csc_off"], host["csc_idx"], None, None,
                              host["csc_w"], None, host["vertex_ids"], True)
