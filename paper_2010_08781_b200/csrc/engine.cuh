@@ -786,7 +786,10 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     if (p.push_view_ready) return;
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
-    if (g->parts.size() == 1 && !multi_rank(g)) {
+    // one partition holding every vertex (no comm, or a world of one rank): the graph's own
+    // CSR is the source-major view
+    if (g->parts.size() == 1 && p.vb == 0 && p.rows == n &&
+        (!multi_rank(g) || g->comm->world == 1)) {
         p.push_sssp = PushAdj{p.csr_off, p.csr_idx, p.csr_w, nullptr, nullptr, nullptr, 0, n};
         p.push_cc = PushAdj{p.csr_off, p.csr_idx, p.csr_w, p.csc_off, p.csc_idx, p.csc_w, 0, n};
         p.push_view_ready = true;
