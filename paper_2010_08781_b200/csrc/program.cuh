@@ -579,8 +579,9 @@ k_prog_expand(PushAdj adj, const int32_t* __restrict__ e_id, const long long* __
 
 // After the expansion: compute on recipients and active vertices (naive selection, PAPER.md:
 // 171-175, which here equals the bypass list plus the non-halted), reset their mailboxes.
-// kProgApplyRows rows per thread: one 16-byte load of their flags and half a recipient word
-// decide, in the common case of a sparse frontier, that none of them has anything to do.
+// A warp owns 32 x kProgApplyRows consecutive rows; it first checks their flag bytes and
+// recipient bits and skips them all when none has anything to do (the common case of a sparse
+// frontier), else processes them with lane l on rows base + 32 j + l (coalesced stores).
 constexpr int kProgApplyRows = 16;
 template <class P>
 __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
@@ -591,27 +592,39 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{};
-    const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kProgApplyRows;
-    if (base < A.rows) {
-        const uint4 f4 = *reinterpret_cast<const uint4*>(A.flags + base);   // padded array
-        uint32_t got16 = (A.recv[base >> 5] >> (base & 31)) & 0xFFFFu;
-        if constexpr (P::kSends)
-            if (A.p2p_in_recv) got16 |= (A.p2p_in_recv[base >> 5] >> (base & 31)) & 0xFFFFu;
-        if ((f4.x | f4.y | f4.z | f4.w | got16) != 0u) {
-            const uint32_t fw[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll 1
-            for (int j = 0; j < kProgApplyRows; ++j) {
-                const int64_t row = base + j;
-                if (row >= A.rows) break;
-                const uint8_t fl = (uint8_t)(fw[j >> 2] >> (8 * (j & 3)));
-                if (((got16 >> j) & 1u) || (fl & 2u)) {
+    const int lane = threadIdx.x & 31;
+    const int64_t base =
+        (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 * kProgApplyRows);
+    // the check reads lane l's 16 consecutive rows at once: one 16-byte load of their flag bytes
+    // (the array is padded to 32 bytes) and half a recipient word
+    bool any = false;
+    {
+        const int64_t r0 = base + (int64_t)kProgApplyRows * lane;
+        if (r0 < A.rows) {
+            const uint4 f4 = *reinterpret_cast<const uint4*>(A.flags + r0);
+            uint32_t got16 = (A.recv[r0 >> 5] >> (r0 & 31)) & 0xFFFFu;
+            if constexpr (P::kSends)
+                if (A.p2p_in_recv) got16 |= (A.p2p_in_recv[r0 >> 5] >> (r0 & 31)) & 0xFFFFu;
+            any = (f4.x | f4.y | f4.z | f4.w | got16) != 0u;
+        }
+    }
+    if (__any_sync(kFull, any)) {   // then every row of the warp, coalesced
+        for (int j = 0; j < kProgApplyRows; ++j) {
+            const int64_t row = base + 32 * j + lane;
+            uint32_t word = 0u;
+            if (row < A.rows) {
+                word = A.recv[row >> 5];
+                bool got = (word >> lane) & 1u;
+                if constexpr (P::kSends)
+                    if (A.p2p_in_recv) got = got || ((A.p2p_in_recv[row >> 5] >> lane) & 1u);
+                const uint8_t fl = A.flags[row];
+                if (got || (fl & 2u)) {
                     const V m = A.mbox[row];
                     A.mbox[row] = C::identity();
                     prog_vertex<P>(A, row, m, c);
                 } else if (fl) {
                     // halted and no messages: no broadcast.  The buffer written now holds a
-                    // value only if the row broadcast two supersteps ago (bit 2); rows without
-                    // flags are not touched at all
+                    // value only if the row broadcast two supersteps ago (bit 2)
                     if (fl & 4u) {
                         A.out_next[A.vbase + row] = C::identity();
                         A.peers.store(A.vbase + row, C::identity());
@@ -619,10 +632,10 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
                     A.flags[row] = (uint8_t)((fl & 1u) << 2);
                 }
             }
+            __syncwarp();   // every lane read the recipient word
+            if (lane == 0 && word) A.recv[row >> 5] = 0u;
         }
     }
-    __syncwarp();   // both halves of a recipient word were read above
-    if (base < A.rows && (base & 31) == 0) A.recv[base >> 5] = 0u;
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
     if constexpr (P::kAggregates) flush_prog_aggregate(c, A.agg_op, A.shared ? A.shared->agg : nullptr);
