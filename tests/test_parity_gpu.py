@@ -730,8 +730,8 @@ def test_host_create_derived_csr_small_and_empty(n, m, monkeypatch):
     G.close()
 
 
-@pytest.mark.parametrize("ids", [False, True])
-def test_get_values_async_matches_sync(ids):
+@pytest.mark.parametrize("ids,parts", [(False, 1), (True, 1), (False, 3)])
+def test_get_values_async_matches_sync(ids, parts):
     """ipregel_get_values_async: each app's values staged privately and copied on the copy
     stream while the next app runs; after sync they equal the synchronous readback."""
     import torch
@@ -748,8 +748,11 @@ def test_get_values_async_matches_sync(ids):
         inv = np.empty(n, np.int32)
         inv[perm] = np.arange(n, dtype=np.int32)
         vid = torch.from_numpy(inv).cuda()
-    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"],
-                                     d["csr_idx"], d["csc_w"], d["csr_w"], vertex_ids=vid))
+    if parts == 1:
+        G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], d["csr_off"],
+                                         d["csr_idx"], d["csc_w"], d["csr_w"], vertex_ids=vid))
+    else:
+        G = make_graph(g, partitions=parts)
     want, got = {}, {}
     for app in ("pagerank", "cc", "sssp"):
         G.run(app)
