@@ -466,8 +466,10 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{};
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row < A.rows) {
+    // grid-stride (a few waves of CTAs): one counter flush per CTA, not per 256 rows -- with
+    // every vertex broadcasting, 262K CTAs' same-address atomics cost more than the init itself
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
         const ProgCtx x = prog_ctx(A, row);
         V val = C::identity();
         V msg = C::identity();
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
         A.mbox[row] = C::identity();
         if constexpr (P::kAggregates) {
             if (x.agg_n) {
-                c.agg = x.agg_acc;
+                c.agg = c.agg_n ? agg_combine(A.agg_op, c.agg, x.agg_acc) : x.agg_acc;
                 c.agg_n = 1u;
             }
         }
@@ -653,17 +655,20 @@ __global__ void __launch_bounds__(256) k_prog_pull_apply(ProgArgs<typename P::V>
     __shared__ unsigned long long s_cnt[4];
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     LaneCounters c{};
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kProgPullRows + threadIdx.x;
-    V m[kProgPullRows];
+    // grid-stride over blocks of kProgPullRows x 256 rows (one counter flush per CTA)
+    for (int64_t blk = blockIdx.x; blk * blockDim.x * kProgPullRows < A.rows; blk += gridDim.x) {
+        const int64_t base = blk * blockDim.x * kProgPullRows + threadIdx.x;
+        V m[kProgPullRows];
 #pragma unroll
-    for (int j = 0; j < kProgPullRows; ++j) {
-        const int64_t row = base + (int64_t)j * blockDim.x;
-        if (row < A.rows) m[j] = A.mbox[row];
-    }
+        for (int j = 0; j < kProgPullRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            if (row < A.rows) m[j] = A.mbox[row];
+        }
 #pragma unroll
-    for (int j = 0; j < kProgPullRows; ++j) {
-        const int64_t row = base + (int64_t)j * blockDim.x;
-        if (row < A.rows) prog_vertex<P>(A, row, m[j], c);
+        for (int j = 0; j < kProgPullRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            if (row < A.rows) prog_vertex<P>(A, row, m[j], c);
+        }
     }
     __syncthreads();
     flush_counters(c, s_cnt, counters);

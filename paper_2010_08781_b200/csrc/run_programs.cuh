@@ -433,7 +433,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         ProgArgs<V> a = args_for(p, 0, 1);   // out_next = buffer 0
         PullCounters* cnt = p.pull_cnt;
         void* args[] = {&a, &cnt};
-        launch_jit(pr->k[PK_INIT], grid_for(p.rows, 256), 256, args, s);
+        launch_jit(pr->k[PK_INIT], std::min<unsigned>(grid_for(p.rows, 256), 148 * 16), 256, args, s);
     }
     T0.kend();
     exchange(0);
@@ -534,7 +534,8 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
                 ProgArgs<V> a = args_for(p, step, cur);
                 PullCounters* cnt = p.pull_cnt;
                 void* args[] = {&a, &cnt};
-                launch_jit(pr->k[PK_PULL_APPLY], grid_for(ceil_div(p.rows, kProgPullRows), 256),
+                launch_jit(pr->k[PK_PULL_APPLY],
+                           std::min<unsigned>(grid_for(ceil_div(p.rows, kProgPullRows), 256), 148 * 16),
                            256, args, s);
             }
             T.kend();
