@@ -238,6 +238,10 @@ struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
 struct CCPullIn : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
+#ifndef IPREGEL_CCIN_MINBLOCKS
+#define IPREGEL_CCIN_MINBLOCKS 6
+#endif
+    static constexpr int kMinBlocks = IPREGEL_CCIN_MINBLOCKS;   // 6 CTAs/SM (40 registers + 8 B stack): Hash-Min -0.4 ms vs 4 at cfg4
     static constexpr bool kAbsorbing = true;
     static constexpr bool kAbsorbingPartial = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
@@ -259,6 +263,10 @@ struct CCPullIn : MinU32, NoAggregate {
 // "if value < old: broadcast" -> changed / messages counters (degree in the symmetrised graph).
 struct CCPullOut : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
+#ifndef IPREGEL_CCOUT_MINBLOCKS
+#define IPREGEL_CCOUT_MINBLOCKS 5
+#endif
+    static constexpr int kMinBlocks = IPREGEL_CCOUT_MINBLOCKS;   // 5 CTAs/SM (48 registers): with the two below, Hash-Min 17.0 -> 16.5 ms
     static constexpr bool kAbsorbing = true;
     static constexpr bool kAbsorbingPartial = true;
     __device__ static bool absorbing(T x) { return x == 0u; }
@@ -298,6 +306,10 @@ struct CCPullOut : MinU32, NoAggregate {
 // INF - dist in the max-reduced dmax counter).
 struct SSSPPull : MinU32, NoAggregate {
     static constexpr bool kWeighted = true;
+#ifndef IPREGEL_SSSP_MINBLOCKS
+#define IPREGEL_SSSP_MINBLOCKS 5
+#endif
+    static constexpr int kMinBlocks = IPREGEL_SSSP_MINBLOCKS;   // 5 CTAs/SM (48 registers + 32 B stack): SSSP 13.4 -> 12.8 ms (6: 72 B stack, 15.5 ms)
     static constexpr bool kAbsorbing = true;
     static constexpr bool kAbsorbingPartial = true;
     const uint32_t* __restrict__ cur;
