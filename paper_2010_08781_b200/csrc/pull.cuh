@@ -55,7 +55,10 @@ template <class Op, class = void> struct PullMinBlocks { static constexpr int va
 template <class Op> struct PullMinBlocks<Op, void_t_<decltype(Op::kMinBlocks)>> {
     static constexpr int value = Op::kMinBlocks;
 };
-constexpr int kPullThreads = 256;                 // 8 warps per CTA
+#ifndef IPREGEL_PULL_THREADS
+#define IPREGEL_PULL_THREADS 256
+#endif
+constexpr int kPullThreads = IPREGEL_PULL_THREADS;  // 8 warps per CTA
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
 #ifndef IPREGEL_RANGE_ITEMS
