@@ -8,9 +8,8 @@ import torch
 
 
 def local_cpus():
-    bus = torch.cuda.get_device_properties(0).pci_bus_id if hasattr(
-        torch.cuda.get_device_properties(0), "pci_bus_id") else None
-    if bus is None:
+    bus = getattr(torch.cuda.get_device_properties(0), "pci_bus_id", None)
+    if not isinstance(bus, str):   # some torch versions expose the bus number only
         import subprocess
         bus = subprocess.check_output(["nvidia-smi", "--query-gpu=pci.bus_id", "--format=csv,noheader",
                                        "-i", "0"]).decode().strip()
