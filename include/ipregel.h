@@ -183,6 +183,15 @@ typedef struct {
  * reachable: UNSUPPORTED.  The choice is made collectively on the first run of each app. */
 #define IPREGEL_RUN_EXCHANGE_COLLECTIVE 0x1u
 #define IPREGEL_RUN_EXCHANGE_FUSED 0x2u
+/* PageRank (ipregel_run only): after every superstep s, also fold on the device the two sums of
+ * the rank mass invariant (Pregel's PageRank):
+ *   pagerank_mass[s]    = sum over all vertices of r_s(v)
+ *   pagerank_mass_nd[s] = sum over vertices with out-degree > 0 of r_s(v)
+ * so that pagerank_mass[s] = 0.15 + 0.85 * pagerank_mass_nd[s-1] (dangling mass is dropped,
+ * DESIGN.md R4) can be checked on the GPU's own values.  f64 atomics: the summation order is not
+ * deterministic (the values themselves are unaffected).  A diagnostic: off by default (it adds
+ * two atomics per warp to every superstep).  Other apps: INVALID_ARGUMENT. */
+#define IPREGEL_RUN_PAGERANK_MASS 0x4u
 
 /* Per-superstep record of the last run (index = superstep, 0 = initialisation). */
 typedef struct {
@@ -200,6 +209,8 @@ typedef struct {
     uint64_t* model_bytes;    /* algorithmic DRAM bytes of the superstep (DESIGN.md roofline)   */
     double* pagerank_delta;   /* PageRank: max_v |r_s(v) - r_{s-1}(v)| when run to convergence,
                                  else 0                                                         */
+    double* pagerank_mass;    /* PageRank with IPREGEL_RUN_PAGERANK_MASS: sum_v r_s(v), else 0  */
+    double* pagerank_mass_nd; /*   and sum of r_s(v) over vertices with out-degree > 0          */
 } ipregel_stats;
 
 /* ---- errors / device ---------------------------------------------------------------------- */

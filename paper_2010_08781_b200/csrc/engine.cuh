@@ -291,6 +291,7 @@ struct StepRecord {
     uint8_t mode = 0;
     uint64_t changed = 0, messages = 0, edges_scanned = 0, model_bytes = 0;
     double delta = 0.0;   // PageRank: max_v |r_s(v) - r_{s-1}(v)| (to-convergence runs)
+    double mass[2] = {0.0, 0.0};   // PageRank mass check: sum r_s, sum over outdeg > 0
 };
 
 }  // namespace
@@ -328,6 +329,8 @@ struct ipregel_graph {
     int cur = 0;
     std::vector<StepRecord> steps;
     std::vector<cudaEvent_t> events;
+    double* pr_mass = nullptr;     // PageRank mass check: [2 * pr_mass_cap] device sums
+    uint32_t pr_mass_cap = 0;
     double* gather_tmp = nullptr;  // get_values scratch (full vector, internal order)
     double* gather_tmp2 = nullptr; // get_values scratch (original order)
     const int32_t* vertex_ids = nullptr;  // internal -> original id, or NULL

@@ -340,10 +340,13 @@ ipregel_status ipregel_run(ipregel_graph* g, ipregel_app app, ipregel_combiner c
     if (max_supersteps == 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "max_supersteps must be >= 1");
     if (P.mode < IPREGEL_MODE_AUTO || P.mode > IPREGEL_MODE_PUSH)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown mode %d", P.mode);
-    if (P.flags & ~(uint32_t)(IPREGEL_RUN_EXCHANGE_COLLECTIVE | IPREGEL_RUN_EXCHANGE_FUSED))
+    if (P.flags & ~(uint32_t)(IPREGEL_RUN_EXCHANGE_COLLECTIVE | IPREGEL_RUN_EXCHANGE_FUSED |
+                              IPREGEL_RUN_PAGERANK_MASS))
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", P.flags);
     if ((P.flags & IPREGEL_RUN_EXCHANGE_COLLECTIVE) && (P.flags & IPREGEL_RUN_EXCHANGE_FUSED))
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "EXCHANGE_COLLECTIVE and EXCHANGE_FUSED are exclusive");
+    if ((P.flags & IPREGEL_RUN_PAGERANK_MASS) && app != IPREGEL_APP_PAGERANK)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "IPREGEL_RUN_PAGERANK_MASS is for PageRank only");
     if (app == IPREGEL_APP_SSSP && (int64_t)P.sssp_source >= g->n)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "sssp_source %u >= N", P.sssp_source);
     if (!(P.push_fraction >= 0.0f)) fail(IPREGEL_ERR_INVALID_ARGUMENT, "push_fraction < 0");
@@ -636,6 +639,8 @@ ipregel_status ipregel_get_stats(ipregel_graph* g, ipregel_stats* st) {
         if (st->edges_scanned) st->edges_scanned[i] = R.edges_scanned;
         if (st->model_bytes) st->model_bytes[i] = R.model_bytes;
         if (st->pagerank_delta) st->pagerank_delta[i] = R.delta;
+        if (st->pagerank_mass) st->pagerank_mass[i] = R.mass[0];
+        if (st->pagerank_mass_nd) st->pagerank_mass_nd[i] = R.mass[1];
     }
     return IPREGEL_OK;
     ABI_END

@@ -85,6 +85,27 @@ struct LaneCounters {
     double agg;        // user programs: this thread's fold of ipr_aggregate values
     uint32_t agg_n;    //   (agg_n = 0: nothing folded)
     unsigned long long mkey = ~0ull;   // user programs with ipr_settled: min broadcast (order key)
+    double m0 = 0.0, m1 = 0.0;         // PageRank mass check: sum of r, sum of r over outdeg > 0
+};
+
+// PageRank mass check (IPREGEL_RUN_PAGERANK_MASS): the lanes' sums of r and of r over vertices
+// with out-degree > 0, warp-reduced, one f64 atomic pair per warp into this superstep's slot.
+// Every lane of the warp must call it.
+__device__ __forceinline__ void flush_mass(const LaneCounters& c, double* mass) {
+    double a = c.m0, b = c.m1;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        a += __shfl_xor_sync(kFull, a, d);
+        b += __shfl_xor_sync(kFull, b, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (a != 0.0 || b != 0.0)) {
+        atomicAdd(mass, a);
+        atomicAdd(mass + 1, b);
+    }
+}
+template <class Op, class = void> struct HasMass { static constexpr bool value = false; };
+template <class Op> struct HasMass<Op, void_t_<decltype(Op::kMass)>> {
+    static constexpr bool value = Op::kMass;
 };
 
 // Range plan for one adjacency of one partition.
@@ -188,6 +209,7 @@ struct NoAggregate {
 // r = ratio + 0.85 * sum, then broadcast r / outdeg for the next superstep if s < k.
 struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     static constexpr bool kWeighted = false;
+    static constexpr bool kMass = true;
     static constexpr int kMinBlocks = IPREGEL_PR_MINBLOCKS;   // as PageRankSum
     const double* __restrict__ contrib_cur;   // replica, global ids
     double* __restrict__ contrib_next;        // replica, global ids
@@ -199,6 +221,7 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     int broadcast;                            // s < k
     int write_rank;
     int track;                                // to convergence: rank holds r_{s-1}; fold |dr|
+    double* mass;                             // mass check: this superstep's [sum r, sum_nd r]
     const void* gather_base() const { return contrib_cur; }
     __device__ const T* gptr() const { return contrib_cur; }
     __device__ bool absorbed(int32_t) const { return false; }
@@ -211,11 +234,17 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
             c.dmax = d > c.dmax ? d : c.dmax;
         }
         if (write_rank) rank[row] = r;
-        if (broadcast) {
+        if (broadcast || mass) {
             const int32_t deg = out_off[row + 1] - out_off[row];
-            const double c = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
-            contrib_next[vbase + row] = c;
-            peers.store(vbase + row, c);
+            if (mass) {   // the invariant sum r_s = 0.15 + 0.85 sum_{outdeg>0} r_{s-1} (tests)
+                c.m0 += r;
+                if (deg > 0) c.m1 += r;
+            }
+            if (broadcast) {
+                const double x = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
+                contrib_next[vbase + row] = x;
+                peers.store(vbase + row, x);
+            }
         }
     }
 };
@@ -767,6 +796,7 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
     }
     flush_counters(cnt, s_cnt, A.counters);
     if constexpr (Op::kAggregates) op.flush_aggregate(cnt);
+    if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
 }
 
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A
@@ -796,6 +826,7 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
         __syncthreads();
         flush_counters(c, s_cnt, counters);
     }
+    if (op.mass) flush_mass(c, op.mass);
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
@@ -849,6 +880,7 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
     // one global atomic per CTA (not per group: the counters are shared by every group)
     flush_counters(c, s_cnt, counters);
     if constexpr (Op::kAggregates) op.flush_aggregate(c);
+    if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(c, op.mass);
 }
 
 }  // namespace ipr

@@ -428,13 +428,21 @@ __global__ void k_pr_push_apply(double* __restrict__ acc, const int32_t* __restr
                                 int64_t rows, int64_t vbase, double ratio, int broadcast,
                                 int write_rank, double* __restrict__ rank,
                                 double* __restrict__ contrib_next,
-                                unsigned long long* __restrict__ dmax) {
+                                unsigned long long* __restrict__ dmax, double* __restrict__ mass) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double r = 0.0;
     unsigned long long d = 0;
     if (i < rows) {
         r = __dadd_rn(ratio, __dmul_rn(0.85, acc[i]));
         if (dmax) d = (unsigned long long)__double_as_longlong(fabs(__dsub_rn(r, rank[i])));
+    }
+    if (mass) {   // grid-uniform; whole warps
+        LaneCounters c;
+        if (i < rows) {
+            c.m0 = r;
+            c.m1 = out_off[i + 1] > out_off[i] ? r : 0.0;
+        }
+        flush_mass(c, mass);
     }
     if (dmax) {
 #pragma unroll

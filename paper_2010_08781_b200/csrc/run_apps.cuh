@@ -7,6 +7,21 @@ namespace {
 // =============================================================================================
 // PageRank (Fig. 8)
 // =============================================================================================
+// Mass check: the per-superstep device sums into the step records (summed over ranks).
+void read_mass(ipregel_graph* g) {
+    cudaStream_t s = g->stream;
+    const size_t m = 2 * g->steps.size();
+    if (multi_rank(g))
+        NC(ncclAllReduce(g->pr_mass, g->pr_mass, m, ncclFloat64, ncclSum, g->comm->nccl, s));
+    std::vector<double> h(m);
+    CU(cudaMemcpyAsync(h.data(), g->pr_mass, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < g->steps.size(); ++i) {
+        g->steps[i].mass[0] = h[2 * i];
+        g->steps[i].mass[1] = h[2 * i + 1];
+    }
+}
+
 ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_run_params& P) {
     cudaStream_t s = g->stream;
     const cudaStream_t user_stream = g->stream;
@@ -22,6 +37,13 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     // per-vertex change is aggregated on the device; the host halts the run once it is <= tol
     const double tol = P.pagerank_tolerance;
     const bool track = tol >= 0.0;
+    // mass check (IPREGEL_RUN_PAGERANK_MASS): per-superstep device sums, slot 2 s and 2 s + 1
+    const bool mass = (P.flags & IPREGEL_RUN_PAGERANK_MASS) != 0;
+    if (mass && g->pr_mass_cap < k + 1) {
+        g->pr_mass = g->graph_mem.alloc<double>(2 * (size_t)(k + 1), s);
+        g->pr_mass_cap = k + 1;
+    }
+    auto mass_slot = [&](uint32_t step) { return mass ? g->pr_mass + 2 * step : nullptr; };
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -48,6 +70,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->cur = G.cur;
         g->last_exchange = G.exchange;
         finalize_times(g);
+        if (mass) read_mass(g);
         return G.status;
     }
     const unsigned long long launches0 = g_launches.load(std::memory_order_relaxed);
@@ -65,13 +88,14 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     g->steps.assign(1, StepRecord{});
     StepTimer T0{g, 0};
     T0.begin();
+    if (mass) CU(cudaMemsetAsync(g->pr_mass, 0, 2 * sizeof(double) * (k + 1), s));
     T0.kbegin();
     for (auto& p : g->parts) {
         AppState& S = p.st[IPREGEL_APP_PAGERANK];
         if (p.rows == 0) continue;
         k_init_pagerank<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, p.vb, inv_n,
                                                               k > 0, last == 0 || track, S.rank,
-                                                              S.contrib[0]);
+                                                              S.contrib[0], mass_slot(0));
         LAUNCH_CHECK();
     }
     T0.kend();
@@ -128,6 +152,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.broadcast = broadcast;
                 op.write_rank = write_rank;
                 op.track = track;
+                op.mass = mass_slot(step);
                 if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
@@ -150,7 +175,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 LAUNCH_CHECK();
                 k_pr_push_apply<<<grid_for(p.rows, 256), 256, 0, s>>>(
                     S.acc, p.csr_off, p.rows, p.vb, ratio, broadcast, write_rank, S.rank,
-                    S.contrib[1 - cur], track ? &p.pull_cnt->dmax : nullptr);
+                    S.contrib[1 - cur], track ? &p.pull_cnt->dmax : nullptr, mass_slot(step));
                 LAUNCH_CHECK();
             }
         }
@@ -201,6 +226,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         CU(cudaGraphLaunch(G.exec, s));
     }
     finalize_times(g);
+    if (mass) read_mass(g);
     return status;
 }
 

@@ -2,6 +2,7 @@
 // small utility kernels.
 #pragma once
 #include "common.cuh"
+#include "pull.cuh"
 
 namespace ipr {
 
@@ -10,14 +11,20 @@ namespace ipr {
 // (a vertex without out-neighbours does not broadcast, reading R4).
 __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t rows, int64_t vbase,
                                 double inv_n, int broadcast, int write_rank,
-                                double* __restrict__ rank, double* __restrict__ contrib) {
+                                double* __restrict__ rank, double* __restrict__ contrib,
+                                double* __restrict__ mass) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    if (write_rank) rank[i] = inv_n;
-    if (broadcast) {
-        const int32_t deg = out_off[i + 1] - out_off[i];
-        contrib[vbase + i] = deg > 0 ? __ddiv_rn(inv_n, (double)deg) : 0.0;
+    LaneCounters c;
+    if (i < rows) {
+        if (write_rank) rank[i] = inv_n;
+        if (broadcast || mass) {
+            const int32_t deg = out_off[i + 1] - out_off[i];
+            if (broadcast) contrib[vbase + i] = deg > 0 ? __ddiv_rn(inv_n, (double)deg) : 0.0;
+            c.m0 = inv_n;
+            c.m1 = deg > 0 ? inv_n : 0.0;
+        }
     }
+    if (mass) flush_mass(c, mass);   // grid-uniform; whole warps (blocks of 256)
 }
 
 // User programs: broadcaster bitmap of the owned rows from the per-vertex flag bytes (bit 0),

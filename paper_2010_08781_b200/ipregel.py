@@ -43,6 +43,7 @@ APPS = {"pagerank": APP_PAGERANK, "cc": APP_HASHMIN_CC, "sssp": APP_SSSP}
 COMBINER_OF = {APP_PAGERANK: COMBINE_SUM, APP_HASHMIN_CC: COMBINE_MIN, APP_SSSP: COMBINE_MIN}
 MODES = {"auto": MODE_AUTO, "pull": MODE_PULL, "push": MODE_PUSH}
 RUN_EXCHANGE_COLLECTIVE, RUN_EXCHANGE_FUSED = 0x1, 0x2
+RUN_PAGERANK_MASS = 0x4
 EXCHANGES = {"auto": 0, "collective": RUN_EXCHANGE_COLLECTIVE, "fused": RUN_EXCHANGE_FUSED}
 EXCHANGE_NAMES = {0: "none", 1: "collective", 2: "fused"}
 
@@ -80,7 +81,8 @@ class Stats(ctypes.Structure):
                 ("time_ms", ctypes.c_void_p), ("kernel_ms", ctypes.c_void_p),
                 ("mode", ctypes.c_void_p), ("changed", ctypes.c_void_p),
                 ("messages", ctypes.c_void_p), ("edges_scanned", ctypes.c_void_p),
-                ("model_bytes", ctypes.c_void_p), ("pagerank_delta", ctypes.c_void_p)]
+                ("model_bytes", ctypes.c_void_p), ("pagerank_delta", ctypes.c_void_p),
+                ("pagerank_mass", ctypes.c_void_p), ("pagerank_mass_nd", ctypes.c_void_p)]
 
 
 class ProgramDesc(ctypes.Structure):
@@ -364,14 +366,15 @@ class Graph:
 
     def run(self, app, max_supersteps: int = 1 << 30, mode="auto", iterations: int = 10,
             source: int = 0, push_fraction: float = 0.04, combiner=None,
-            allow_guard: bool = False, exchange: str = "auto", tolerance: float = -1.0) -> int:
+            allow_guard: bool = False, exchange: str = "auto", tolerance: float = -1.0,
+            mass: bool = False) -> int:
         app = APPS[app] if isinstance(app, str) else int(app)
         p = run_params_default()
         p.mode = MODES[mode] if isinstance(mode, str) else int(mode)
         p.pagerank_iterations = iterations
         p.sssp_source = source
         p.push_fraction = push_fraction
-        p.flags = EXCHANGES[exchange]
+        p.flags = EXCHANGES[exchange] | (RUN_PAGERANK_MASS if mass else 0)
         p.pagerank_tolerance = tolerance
         comb = COMBINER_OF.get(app, COMBINE_SUM) if combiner is None else combiner
         st = load().ipregel_run(self.handle, app, comb, max_supersteps, ctypes.byref(p))
@@ -438,6 +441,8 @@ class Graph:
             "edges_scanned": np.zeros(capacity, np.uint64),
             "model_bytes": np.zeros(capacity, np.uint64),
             "pagerank_delta": np.zeros(capacity, np.float64),
+            "pagerank_mass": np.zeros(capacity, np.float64),
+            "pagerank_mass_nd": np.zeros(capacity, np.float64),
         }
         st = Stats()
         st.capacity = capacity

@@ -201,3 +201,21 @@ def cc_max_label(n, edges):
     for v in range(n):
         top[mn[v]] = max(top.get(mn[v], v), v)
     return [top[mn[v]] for v in range(n)]
+
+
+def assert_pagerank_mass(stats, n, outdeg_positive=None, rel=1e-12):
+    """The rank mass invariant on the GPU's own per-superstep sums (IPREGEL_RUN_PAGERANK_MASS):
+    sum_v r_s(v) = 0.15 + 0.85 * sum_{outdeg(u)>0} r_{s-1}(u) for s >= 1 (dangling mass dropped,
+    DESIGN.md R4; Pregel's PageRank PAPER.md:515-533), and at superstep 0
+    sum r_0 = 1 (r_0 = 1/N) and sum_nd r_0 = (#vertices with outdeg > 0) / N.  A dropped or
+    doubled edge moves the left side by its message but not the right side."""
+    m, nd = np.asarray(stats["pagerank_mass"]), np.asarray(stats["pagerank_mass_nd"])
+    s = int(stats["supersteps"])
+    assert s >= 1 and len(m) >= s
+    assert abs(m[0] - 1.0) <= rel, m[0]
+    if outdeg_positive is not None:
+        assert abs(nd[0] - outdeg_positive / n) <= rel * max(outdeg_positive / n, 1e-300), nd[0]
+    for t in range(1, s):
+        want = 0.15 + 0.85 * nd[t - 1]
+        assert abs(m[t] - want) <= rel * want, (t, m[t], want)
+        assert 0.0 <= nd[t] <= m[t] * (1 + rel)

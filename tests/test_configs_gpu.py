@@ -16,6 +16,7 @@ import pytest
 
 import inputs
 import oracle
+from tests import checkers
 
 pytestmark = pytest.mark.gpu
 GOLDEN4 = os.path.join(os.path.dirname(__file__), "golden", "cfg4_oracle.json")
@@ -53,13 +54,15 @@ def test_config_vs_live_oracle(name, order):
     assert g["e"] == len(src)
     if cfg.app == "pagerank":
         o = oracle.pagerank(cfg.n, src, dst, k=cfg.iterations)
+        nd = int(((g["csr_off"][1:] - g["csr_off"][:-1]) > 0).sum().item())
         for mode in ("pull", "push"):
-            G.run("pagerank", mode=mode, iterations=cfg.iterations)
+            G.run("pagerank", mode=mode, iterations=cfg.iterations, mass=True)
             v = G.values(host=True)
             err = np.abs(v - o["values"])
             assert err.max() <= 1e-9
             assert (err / o["values"]).max() <= 1e-11
             check_counters(G.stats(), o)
+            checkers.assert_pagerank_mass(G.stats(), cfg.n, nd)
     elif cfg.app == "cc":
         o = oracle.hashmin_cc(cfg.n, src, dst)
         for mode in ("auto", "pull", "push"):

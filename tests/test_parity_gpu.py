@@ -40,11 +40,15 @@ def run_gpu(app, n, src, dst, w=None, mode="auto", k=10, source=0, partitions=1,
             max_supersteps=1 << 30, host=False, allow_guard=False):
     g = csr_csc(n, src, dst, w)
     G = make_graph(g, partitions=partitions, host=host, weighted=w is not None)
+    pr = app == "pagerank"
     st = G.run(app, max_supersteps=max_supersteps, mode=mode, iterations=k, source=source,
-               allow_guard=allow_guard)
+               allow_guard=allow_guard, mass=pr)
     vals = G.values(host=True)
     stats = G.stats()
     G.close()
+    if pr and n > 0:   # the mass invariant on the GPU's own per-superstep sums
+        nd = int(np.count_nonzero(np.bincount(np.asarray(src, np.int64), minlength=n)))
+        checkers.assert_pagerank_mass(stats, n, nd)
     return st, vals, stats
 
 
