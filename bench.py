@@ -180,8 +180,49 @@ def run_step(G, apps, iterations=10):
 
 
 # ------------------------------------------------------------------------------ cpu baseline
+def host_info():
+    """CPU model, logical CPUs and RAM of the box (the oracle's hardware)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu_model"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["ram_gb"] = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
+def cfg4_oracle_context():
+    """The oracle's own per-superstep times at the FULL cfg4 size (one core), from
+    tests/golden/cfg4_oracle.json (written by tests/golden/make_cfg4_golden.py, oracle only):
+    reported as context next to the bounded sample, never timed here."""
+    p = os.path.join(ROOT, "tests", "golden", "cfg4_oracle.json")
+    try:
+        with open(p) as f:
+            gold = json.load(f)
+    except Exception:
+        return None
+    out = {}
+    for app, rec in gold["apps"].items():
+        secs = float(sum(rec["oracle_superstep_seconds"]))
+        d = int(sum(rec["messages"][:-1]))
+        out[app] = {"seconds": round(secs, 1), "gteps": d / secs / 1e9,
+                    "supersteps": rec["supersteps"],
+                    "superstep_seconds": [round(x, 2) for x in rec["oracle_superstep_seconds"]]}
+    return {"source": "tests/golden/cfg4_oracle.json (full cfg4, one core, superstep loop only)",
+            "apps": out}
+
+
 def cpu_baseline(apps, scale=SAMPLE_SCALE, repeats=1):
-    """The oracle (single-threaded C Pregel interpreter) on a bounded sample of cfg4."""
+    """The oracle (single-threaded C Pregel interpreter) on a bounded sample of cfg4, pinned to
+    one host core (sched_setaffinity, the last CPU of the process's set) while it runs."""
     import inputs
     import oracle
     cfg = inputs.CONFIGS["cfg4"]
@@ -190,17 +231,24 @@ def cpu_baseline(apps, scale=SAMPLE_SCALE, repeats=1):
     msgs = 0
     secs = 0.0
     per_app = {}
-    for _ in range(repeats):
-        for app in apps:
-            r = oracle.run(APP_CODES[app], n, src, dst, w if app == "sssp" else None,
-                           k=cfg.iterations, source=0)
-            d = int(r["messages"][:-1].sum()) if r["supersteps"] > 1 else 0
-            s = float(r["seconds"].sum())
-            msgs += d
-            secs += s
-            per_app[app] = {"gteps": d / s / 1e9 if s > 0 else None, "seconds": s,
-                            "supersteps": int(r["supersteps"])}
+    old_aff = os.sched_getaffinity(0)
+    core = max(old_aff)
+    os.sched_setaffinity(0, {core})
+    try:
+        for _ in range(repeats):
+            for app in apps:
+                r = oracle.run(APP_CODES[app], n, src, dst, w if app == "sssp" else None,
+                               k=cfg.iterations, source=0)
+                d = int(r["messages"][:-1].sum()) if r["supersteps"] > 1 else 0
+                s = float(r["seconds"].sum())
+                msgs += d
+                secs += s
+                per_app[app] = {"gteps": d / s / 1e9 if s > 0 else None, "seconds": s,
+                                "supersteps": int(r["supersteps"])}
+    finally:
+        os.sched_setaffinity(0, old_aff)
     return {"value": msgs / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "pinned_core": core, "host": host_info(), "full_size_context": cfg4_oracle_context(),
             "sample": (f"R-MAT scale {scale}, edgefactor {cfg.edgefactor}, seed {cfg.seed} "
                        f"(cfg4's generator at 1/{1 << (cfg.scale - scale)} of the vertices, "
                        f"E={len(src)}); {'+'.join(apps)} to termination; superstep loop only "
@@ -230,7 +278,8 @@ def reference_arm(args):
         "config": {"workload": f"{args.config} sample: R-MAT scale {args.sample_scale}, ef 28, seed 5",
                    "apps": apps},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": res["sample"]},
+                         "sample": res["sample"], "pinned_core": res["pinned_core"],
+                         "host": res["host"], "full_size_context": res["full_size_context"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -334,22 +383,44 @@ def main():
         sts = [step["pagerank"] for step in per_step]
         k_ms = np.concatenate([s["kernel_ms"][1:] for s in sts])
         mb = np.concatenate([s["model_bytes"][1:] for s in sts]).astype(np.float64)
-        achieved = float(np.mean(mb) / (np.mean(k_ms) * 1e-3) / 1e9)
+        t_ms = float(np.mean(k_ms))
         if world > 1:
-            t = torch.tensor([float(np.mean(k_ms))], device="cuda", dtype=torch.float64)
+            t = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            achieved = float(np.mean(mb) / (float(t.item()) * 1e-3) / 1e9)  # per-rank bytes
+            t_ms = float(t.item())
+        # 12 B per edge + 24 B per vertex (per-rank bytes at N > 1); the 16 B
+        # per-vertex variant leaves out the rank write a fixed-k run does in its last superstep
+        # only
+        achieved = float(np.mean(mb) / (t_ms * 1e-3) / 1e9)
+        mb16 = 12.0 * e + 16.0 * n if world == 1 else np.mean(mb) - 8.0 * (n / world)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(),
-                "kernel": "k_pull_ranges<PageRankSum> + k_pull_fixup + k_pr_finish",
+                "kernel": "PageRank gather superstep: k_pull_ranges<PageRankSum> over the cold "
+                          "CSC + k_pull_fixup + k_pull_ranges_staged<PageRankHot> (hot sources "
+                          "from shared memory, Fig. 8 update) + k_pull_fixup",
                 "bytes_per_launch": float(np.mean(mb)),
-                "model": "12 B/edge (4 B index + 8 B gathered f64 outbox) + 16 B/vertex",
-                "avg_launch_ms": float(np.mean(k_ms)), "peak_source": peak_src,
-                "frac_of_8TBps": achieved / 8000.0}
+                "model": "SURVEY.md 8(d): 12 B/edge (4 B index + 8 B gathered f64 outbox) + "
+                         "24 B/vertex (CSC offset, out-degree, rank, next outbox)",
+                "avg_launch_ms": t_ms, "peak_source": peak_src,
+                "frac_of_8TBps": achieved / 8000.0,
+                "frac_16N": float(mb16 / (t_ms * 1e-3) / 1e9) / peak}
         apps_out["pagerank"]["superstep_ms_median"] = float(np.median(
             np.concatenate([s["time_ms"][1:] for s in sts])))
         apps_out["pagerank"]["gteps_per_gather_superstep"] = float(
             e / (apps_out["pagerank"]["superstep_ms_median"] * 1e-3) / 1e9)
+
+    # device-memory footprint (the Table 3 analog): the user's graph arrays
+    # (borrowed), the library's graph-side memory (plans, hot/cold split) and the vertex state
+    gb, sb = G.memory_footprint()
+    user_bytes = sum(int(t.numel()) * t.element_size() for t in
+                     (part.csc_offsets, part.csc_indices, part.csc_weights, part.csr_offsets,
+                      part.csr_indices, part.csr_weights) if t is not None)
+    memory = {"user_graph_bytes": user_bytes, "library_graph_bytes": int(gb),
+              "vertex_state_bytes": int(sb),
+              "state_bytes_per_vertex": round(sb / (n / world), 2),
+              "note": "vertex state is Theta(N) (single-slot mailboxes, PAPER.md:205-211, "
+                      ":476-480); library graph bytes are range plans + the PageRank hot/cold "
+                      "split of the CSC"}
 
     # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
     e2e = None
@@ -373,6 +444,7 @@ def main():
                    "device": device_info(local),
                    "apps": apps_out},
         "roofline": roof,
+        "memory": memory,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,

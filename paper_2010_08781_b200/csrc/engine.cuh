@@ -280,6 +280,21 @@ struct Partition {
     cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
     std::vector<int64_t> wc_bounds;
     AppState st[4];
+    // PageRank hot/cold split of the in-adjacency (built on the first pull run):
+    // the edges whose source is < hot_n (the hottest vertices under the degree layout) and the
+    // rest, each a CSC over the same rows with its own range plan on its own global grid.
+    struct {
+        int state = 0;              // 0 not built, 1 built, -1 not used
+        int32_t hot_n = 0;
+        int64_t hot_edges = 0, cold_edges = 0;
+        int64_t hot_ebase = 0, cold_ebase = 0;   // global edge offsets of this partition
+        int32_t* hot_off = nullptr;
+        int32_t* hot_idx = nullptr;
+        int32_t* cold_off = nullptr;
+        int32_t* cold_idx = nullptr;
+        TilePlan plan_hot, plan_cold;
+        DeviceBuffers mem;
+    } split;
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
     unsigned long long* host_cnt = nullptr;   // pinned [16]
@@ -463,12 +478,50 @@ unsigned pull_grid(int64_t num_tiles) {
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
                  const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global,
-                 int policy, bool degree_ordered) {
+                 int policy, bool degree_ordered, int32_t l1hot = INT32_MIN) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
     RangeArgs A = range_args(P, off, idx, w, cnt, s, op.gather_base(), n_global, sizeof(T), policy,
                              degree_ordered);
+    if (l1hot != INT32_MIN && g_l1_hot == -2) A.l1hot = l1hot;
     k_pull_ranges<Op><<<pull_grid<Op>(P.num_tiles), kPullThreads, 0, s>>>(op, A);
+    LAUNCH_CHECK();
+    if (P.num_groups) {
+        k_pull_fixup<Op><<<fixup_grid(P.num_groups, P.num_short), 256, 0, s>>>(
+            op, P.groups, P.num_groups, P.num_short, static_cast<const T*>(P.carry),
+            static_cast<const T*>(P.head), cnt);
+        LAUNCH_CHECK();
+    }
+}
+
+// Staged ops (PageRankHot): one CTA of kHotThreads per SM with hot_n values in shared memory.
+template <class Op>
+void launch_pull_staged(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
+                        PullCounters* cnt, cudaStream_t s, int64_t n_global, int policy) {
+    using T = typename Op::T;
+    if (P.num_tiles == 0) return;
+    static int sms = 0;
+    static size_t attr_bytes = 0;
+    const size_t smem = (size_t)op.hot_n * sizeof(T);
+    if (!sms) {
+        int dev = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (smem > attr_bytes) {
+        CU(cudaFuncSetAttribute(k_pull_ranges_staged<Op>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_bytes = smem;
+    }
+    RangeArgs A = range_args(P, off, idx, nullptr, cnt, s, op.gather_base(), n_global, sizeof(T),
+                             policy, false);
+    if (!A.range_ctr) {   // the staged kernel always takes ranges from the counter
+        CU(cudaMemsetAsync(P.ctr, 0, sizeof(int32_t), s));
+        A.range_ctr = P.ctr;
+    }
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(sms, ceil_div(P.num_tiles, kHotWarps)));
+    k_pull_ranges_staged<Op><<<grid, kHotThreads, smem, s>>>(op, A);
     LAUNCH_CHECK();
     if (P.num_groups) {
         k_pull_fixup<Op><<<fixup_grid(P.num_groups, P.num_short), 256, 0, s>>>(
@@ -809,6 +862,98 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, nullptr, 0, n};
     p.push_cc = PushAdj{o1, i1, w1, o2, i2, w2, 0, n};
     p.push_view_ready = true;
+}
+
+// ---- PageRank hot/cold split ---------------------------------------------
+// Tuning knobs: IPREGEL_HOT_SPLIT (1: on, 0: one range kernel over the whole CSC + k_pr_finish)
+// and IPREGEL_HOT_VERTICES (staged vertices, default 16384 = 128 KiB of f64; at most what one
+// CTA's shared memory holds next to the range kernel's own arrays).
+int g_hot_split = getenv("IPREGEL_HOT_SPLIT") ? atoi(getenv("IPREGEL_HOT_SPLIT")) : 1;
+// cold kernel: sources [hot_n, hot_n + IPREGEL_COLD_L1) are L1 evict-last, the rest bypass L1
+// (-1: the default L1 policy for every gather)
+int32_t g_cold_l1 = getenv("IPREGEL_COLD_L1") ? atoi(getenv("IPREGEL_COLD_L1")) : 8192;
+int32_t g_hot_vertices = getenv("IPREGEL_HOT_VERTICES") ? atoi(getenv("IPREGEL_HOT_VERTICES"))
+                                                        : 16384;
+constexpr int32_t kMaxHotVertices =
+    (int32_t)((227 * 1024 - sizeof(double) * kHotWarps * (4 * 32 + 2) - 64) / sizeof(double));
+
+// Builds every partition's split (collective across ranks: the global edge bases of the two
+// parts are all-gathered).  Returns false when the split is off.
+bool ensure_hot_split(ipregel_graph* g) {
+    if (!g_hot_split || g->parts.empty()) return false;
+    Partition& p0 = g->parts[0];
+    if (p0.split.state != 0) return p0.split.state > 0;
+    cudaStream_t s = g->stream;
+    const int32_t hot_n = (int32_t)std::max<int64_t>(
+        1, std::min<int64_t>({(int64_t)std::max(g_hot_vertices, 1), (int64_t)kMaxHotVertices,
+                              g->n}));
+    std::vector<int64_t> hot_e(g->parts.size(), 0);
+    for (size_t i = 0; i < g->parts.size(); ++i) {
+        Partition& p = g->parts[i];
+        auto& S = p.split;
+        S.hot_n = hot_n;
+        DeviceBuffers tmp;
+        const int64_t E = p.csc_edges;
+        int32_t* pos = tmp.alloc<int32_t>(E + 1, s);
+        k_hot_flags<<<std::min<unsigned>(grid_for(E + 1, 256), 148 * 16), 256, 0, s>>>(
+            p.csc_idx, E, hot_n, pos);
+        LAUNCH_CHECK();
+        exscan_i32(pos, E + 1, tmp, s);
+        S.hot_off = S.mem.alloc<int32_t>(p.rows + 1, s);
+        S.cold_off = S.mem.alloc<int32_t>(p.rows + 1, s);
+        k_hot_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csc_off, p.rows, pos, S.hot_off,
+                                                               S.cold_off);
+        LAUNCH_CHECK();
+        int32_t* h = static_cast<int32_t*>(g->pinned.get(sizeof(int32_t), 1));
+        kernel_copy(h, pos + E, sizeof(int32_t), s);
+        CU(cudaStreamSynchronize(s));
+        S.hot_edges = *h;
+        S.cold_edges = E - S.hot_edges;
+        S.hot_idx = S.mem.alloc<int32_t>(S.hot_edges, s);
+        S.cold_idx = S.mem.alloc<int32_t>(S.cold_edges, s);
+        k_hot_scatter<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+            p.csc_idx, E, hot_n, pos, S.hot_idx, S.cold_idx);
+        LAUNCH_CHECK();
+        CU(cudaStreamSynchronize(s));
+        tmp.release();
+        hot_e[i] = S.hot_edges;
+    }
+    // global edge bases of the two parts: partitions in order, then ranks in order
+    int64_t hb = 0, cb = 0;
+    for (auto& p : g->parts) {
+        p.split.hot_ebase = hb;
+        p.split.cold_ebase = cb;
+        hb += p.split.hot_edges;
+        cb += p.split.cold_edges;
+    }
+    if (multi_rank(g)) {
+        DeviceBuffers tmp;
+        const int W = g->comm->world;
+        int64_t mine[2] = {p0.split.hot_edges, p0.split.cold_edges};
+        int64_t* dmine = tmp.alloc<int64_t>(2, s);
+        int64_t* dall = tmp.alloc<int64_t>(2 * W, s);
+        CU(cudaMemcpyAsync(dmine, mine, sizeof(mine), cudaMemcpyHostToDevice, s));
+        NC(ncclAllGather(dmine, dall, 2, ncclInt64, g->comm->nccl, s));
+        std::vector<int64_t> all(2 * W);
+        CU(cudaMemcpyAsync(all.data(), dall, all.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        tmp.release();
+        p0.split.hot_ebase = p0.split.cold_ebase = 0;
+        for (int r = 0; r < g->comm->rank; ++r) {
+            p0.split.hot_ebase += all[2 * r];
+            p0.split.cold_ebase += all[2 * r + 1];
+        }
+    }
+    for (auto& p : g->parts) {
+        auto& S = p.split;
+        build_plan(S.plan_hot, S.hot_off, S.hot_idx, nullptr, p.rows, S.hot_edges, p.vb,
+                   S.hot_ebase, S.mem, s, g->pinned);
+        build_plan(S.plan_cold, S.cold_off, S.cold_idx, nullptr, p.rows, S.cold_edges, p.vb,
+                   S.cold_ebase, S.mem, s, g->pinned);
+        S.state = 1;
+    }
+    CU(cudaStreamSynchronize(s));
+    return true;
 }
 
 // ---- frontier machinery ------------------------------------------------------------------

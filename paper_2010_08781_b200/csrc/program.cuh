@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
                                                    PullCounters* counters) {
     using V = typename P::V;
     using C = ProgComb<V, P::kCombiner>;
-    __shared__ unsigned long long s_cnt[4];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_cnt[5];
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{};
     // grid-stride (a few waves of CTAs): one counter flush per CTA, not per 256 rows -- with
@@ -590,8 +590,8 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
                                                     PullCounters* counters) {
     using V = typename P::V;
     using C = ProgComb<V, P::kCombiner>;
-    __shared__ unsigned long long s_cnt[4];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_cnt[5];
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{};
     const int lane = threadIdx.x & 31;
@@ -652,8 +652,8 @@ template <class P>
 __global__ void __launch_bounds__(256) k_prog_pull_apply(ProgArgs<typename P::V> A,
                                                          PullCounters* counters) {
     using V = typename P::V;
-    __shared__ unsigned long long s_cnt[4];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_cnt[5];
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     LaneCounters c{};
     // grid-stride over blocks of kProgPullRows x 256 rows (one counter flush per CTA)
     for (int64_t blk = blockIdx.x; blk * blockDim.x * kProgPullRows < A.rows; blk += gridDim.x) {

@@ -72,6 +72,7 @@ struct PullCounters {
     unsigned long long dmax;   // PageRank to convergence: max |r_s - r_{s-1}| as f64 bits (>= 0)
     unsigned long long aux;    // user programs: vertices that did not vote to halt; Hash-Min:
                                // symmetrised degree of the rows at label 0 after the superstep
+    unsigned long long gathered;   // absorbing ops: edges whose messages were actually gathered
 };
 
 // A thread's share of the counters while it runs, 32-bit (fewer live registers in the range
@@ -86,6 +87,7 @@ struct LaneCounters {
     uint32_t agg_n;    //   (agg_n = 0: nothing folded)
     unsigned long long mkey = ~0ull;   // user programs with ipr_settled: min broadcast (order key)
     double m0 = 0.0, m1 = 0.0;         // PageRank mass check: sum of r, sum of r over outdeg > 0
+    uint32_t gathered = 0;             // absorbing ops: edges gathered (lane 0 of each warp)
 };
 
 // PageRank mass check (IPREGEL_RUN_PAGERANK_MASS): the lanes' sums of r and of r over vertices
@@ -267,6 +269,22 @@ struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
     __device__ void finish(int32_t row, T sum, LaneCounters&) const { sum_out[vbase + row] = sum; }
 };
 
+// PageRank over the HOT part of the in-adjacency (hot/cold split): the edges
+// whose source is one of the hot_n hottest vertices (internal ids < hot_n under the degree
+// layout).  Their outbox values are staged once per CTA in shared memory, so these gathers never
+// reach L1/L2; the cold part ran first (PageRankSum over the cold CSC, its sums left in the next
+// outbox slots), and this op's recipient compute is Fig. 8's update of cold + hot (the combine
+// order is fixed: one f64 add of the two partial sums, each folded on its own global grid).
+struct PageRankHot : PageRankPull {
+    static constexpr bool kStaged = true;
+    int32_t hot_n;                            // staged vertices [0, hot_n)
+    const double* stage;                      // set inside the kernel (shared memory)
+    __device__ T gather_staged(int32_t u) const { return stage[u]; }
+    __device__ void finish(int32_t row, T hot, LaneCounters& c) const {
+        PageRankPull::finish(row, __dadd_rn(contrib_next[vbase + row], hot), c);
+    }
+};
+
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
 struct CCPullIn : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
@@ -415,10 +433,16 @@ __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
 
 // Outbox gathers.  l1hot < 0: default L1 allocation; else vertices below l1hot are cached in L1
 // (evict-last) and the rest bypass L1 (tuning knob IPREGEL_L1_HOT).
+template <class Op, class = void> struct IsStaged { static constexpr bool value = false; };
+template <class Op> struct IsStaged<Op, void_t_<decltype(Op::kStaged)>> {
+    static constexpr bool value = Op::kStaged;
+};
+
 template <class Op>
 __device__ __forceinline__ typename Op::T gather_one(const Op& op, int32_t u, uint64_t pol,
                                                      int32_t l1hot) {
     if (u < 0) return Op::identity();
+    if constexpr (IsStaged<Op>::value) return op.gather_staged(u);
     if (l1hot < 0) return ld_gather(op.gptr() + u, pol);
     return ld_gather_l1(op.gptr() + u, pol, u < l1hot);
 }
@@ -455,6 +479,7 @@ __device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned
                                                PullCounters* counters) {
     const int lane = threadIdx.x & 31;
     unsigned long long c0 = cnt.changed, c1 = cnt.messages, c2 = cnt.dmax, c3 = cnt.aux;
+    unsigned long long c4 = cnt.gathered;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         c0 += __shfl_xor_sync(kFull, c0, d);
@@ -462,19 +487,22 @@ __device__ __forceinline__ void flush_counters(const LaneCounters& cnt, unsigned
         const unsigned long long o = __shfl_xor_sync(kFull, c2, d);
         c2 = o > c2 ? o : c2;
         c3 += __shfl_xor_sync(kFull, c3, d);
+        c4 += __shfl_xor_sync(kFull, c4, d);
     }
-    if (lane == 0 && (c0 | c1 | c2 | c3)) {
+    if (lane == 0 && (c0 | c1 | c2 | c3 | c4)) {
         atomicAdd(&s_cnt[0], c0);
         atomicAdd(&s_cnt[1], c1);
         atomicMax(&s_cnt[2], c2);
         atomicAdd(&s_cnt[3], c3);
+        atomicAdd(&s_cnt[4], c4);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1] | s_cnt[2] | s_cnt[3])) {
+    if (threadIdx.x == 0 && counters && (s_cnt[0] | s_cnt[1] | s_cnt[2] | s_cnt[3] | s_cnt[4])) {
         atomicAdd(&counters->changed, s_cnt[0]);
         atomicAdd(&counters->messages, s_cnt[1]);
         atomicMax(&counters->dmax, s_cnt[2]);
         atomicAdd(&counters->aux, s_cnt[3]);
+        atomicAdd(&counters->gathered, s_cnt[4]);
     }
 }
 
@@ -566,12 +594,23 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
     ChunkLoad Ln = load_chunk<Op::kWeighted>(A.idx, A.wts, c0 + kChunk, y0, y1, lane, pol_s);
     T gc[4];
     gather_chunk(op, Lc, gc, pol_g, A.l1hot);
+    // absorbing ops count the edges they gather (superstep model bytes, bench.py)
+    auto count_gathered = [&](int32_t cpos) {
+        if constexpr (Op::kAbsorbing) {
+            const int32_t a = cpos > y0 ? cpos : y0;
+            const int32_t b = cpos + kChunk < y1 ? cpos + kChunk : y1;
+            if (lane == 0 && b > a) cnt.gathered += (uint32_t)(b - a);
+        }
+    };
+    count_gathered(c0);
 
 #pragma unroll kChunkUnroll
     for (int32_t e0 = c0; e0 < y1; e0 += kChunk) {
         T gn[4];
         // the next chunk lies inside an absorbed open row: its messages cannot change it
-        gather_chunk(op, Ln, gn, pol_g, A.l1hot, absorbed && r < x1 && Ec > e0 + 2 * kChunk);
+        const bool skip_next = absorbed && r < x1 && Ec > e0 + 2 * kChunk;
+        gather_chunk(op, Ln, gn, pol_g, A.l1hot, skip_next);
+        if (!skip_next) count_gathered(e0 + kChunk);
         uint32_t wc[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) wc[k] = Lc.w[k];
@@ -772,10 +811,10 @@ template <class Op>
 __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull_ranges(Op op, RangeArgs A) {
     using T = typename Op::T;
     __shared__ T s_sum[kWarpsPerCta][4 * 32 + 2];   // chunk sums by position (conflict-free)
-    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned long long s_cnt[5];
     const int wid = threadIdx.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * kWarpsPerCta + wid;
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters cnt{0u, 0u, 0u, 0ull, 0.0, 0u};
     // warps stride over the ranges independently (the grid may be smaller than one warp per
@@ -799,6 +838,44 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
     if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
 }
 
+// Range kernel of a staged op (PageRankHot): one CTA of kHotThreads per SM copies the staged
+// prefix of the outbox, [0, hot_n), into shared memory (dynamic, hot_n * 8 bytes), then its warps
+// take ranges from the plan's counter exactly like k_pull_ranges.  The rows are the same rows,
+// the edges only the hot ones, so every gather is a shared-memory load.
+#ifndef IPREGEL_HOT_THREADS
+#define IPREGEL_HOT_THREADS 1024
+#endif
+constexpr int kHotThreads = IPREGEL_HOT_THREADS;
+constexpr int kHotWarps = kHotThreads / 32;
+template <class Op>
+__global__ void __launch_bounds__(kHotThreads, 1) k_pull_ranges_staged(Op op, RangeArgs A) {
+    using T = typename Op::T;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    __shared__ T s_sum[kHotWarps][4 * 32 + 2];
+    __shared__ unsigned long long s_cnt[5];
+    T* stage = reinterpret_cast<T*>(s_dyn);
+    {
+        const T* src = op.gptr();
+        for (int32_t i = threadIdx.x; i < op.hot_n; i += blockDim.x) stage[i] = src[i];
+    }
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    Op sop = op;
+    sop.stage = stage;
+    const int wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    LaneCounters cnt{0u, 0u, 0u, 0ull, 0.0, 0u};
+    int32_t r = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
+    r = __shfl_sync(kFull, r, 0);
+    while (r < A.num_ranges) {
+        const int32_t nx = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
+        pull_range<Op>(sop, A, r, s_sum[wid], cnt);
+        r = __shfl_sync(kFull, nx, 0);
+    }
+    flush_counters(cnt, s_cnt, A.counters);
+    if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
+}
+
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A
 // thread takes kPrFinishRows rows (block-strided, coalesced) with their sums loaded up front.
 #ifndef IPREGEL_PR_FINISH_ROWS
@@ -807,8 +884,8 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
 constexpr int kPrFinishRows = IPREGEL_PR_FINISH_ROWS;
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
-    __shared__ unsigned long long s_cnt[4];
-    if (counters && threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_cnt[5];
+    if (counters && threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     LaneCounters c{0u, 0u, 0u, 0ull};
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * kPrFinishRows + threadIdx.x;
     double sum[kPrFinishRows];
@@ -845,9 +922,9 @@ __global__ void k_pull_fixup(Op op, const int4* __restrict__ groups, int32_t num
                              const typename Op::T* __restrict__ head,
                              PullCounters* __restrict__ counters) {
     using T = typename Op::T;
-    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned long long s_cnt[5];
     const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
     const int32_t short_blocks = (num_short + (int32_t)blockDim.x - 1) / (int32_t)blockDim.x;

@@ -44,6 +44,8 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->pr_mass_cap = k + 1;
     }
     auto mass_slot = [&](uint32_t step) { return mass ? g->pr_mass + 2 * step : nullptr; };
+    // pull supersteps over the hot/cold split of the in-adjacency (built on the first pull run)
+    const bool split = P.mode != IPREGEL_MODE_PUSH && g_pr_split && ensure_hot_split(g);
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -153,7 +155,24 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.write_rank = write_rank;
                 op.track = track;
                 op.mass = mass_slot(step);
-                if (g_pr_split) {
+                if (split) {
+                    // cold part first: its sums land in the next outbox slots ...
+                    PageRankSum sop;
+                    sop.contrib_cur = op.contrib_cur;
+                    sop.sum_out = op.contrib_next;
+                    sop.vbase = p.vb;
+                    launch_pull(sop, p.split.plan_cold, p.split.cold_off, p.split.cold_idx,
+                                nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered,
+                                g_cold_l1 < 0 ? -1 : p.split.hot_n + g_cold_l1);
+                    // ... then the hot part from shared memory, whose epilogue runs Fig. 8's
+                    // update on cold + hot (and the fused exchange / mass / convergence folds)
+                    PageRankHot hop;
+                    static_cast<PageRankPull&>(hop) = op;
+                    hop.hot_n = p.split.hot_n;
+                    hop.stage = nullptr;
+                    launch_pull_staged(hop, p.split.plan_hot, p.split.hot_off, p.split.hot_idx,
+                                       track ? p.pull_cnt : nullptr, s, n, g->gather_policy);
+                } else if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
                     sop.sum_out = op.contrib_next;
@@ -191,8 +210,12 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         R.changed = broadcast ? (uint64_t)nondangling : 0;
         R.messages = broadcast ? (uint64_t)g->e : 0;
         R.edges_scanned = (uint64_t)g->e;
-        R.model_bytes = push ? 12ull * g->e + 24ull * n : 12ull * g->e + 16ull * n;
-        if (track) R.model_bytes += 16ull * n;   // rank read + write every superstep
+        // 4 B index + 8 B gathered outbox per edge; 4 B CSC offset + 4 B
+        // out-degree + 8 B rank + 8 B next outbox per vertex (fixed-k pull runs write the rank in
+        // the last superstep only, so 12 E + 16 N of it is what they must move; bench.py reports
+        // both)
+        R.model_bytes = 12ull * g->e + 24ull * n;
+        if (track) R.model_bytes += 8ull * n;    // the previous rank is read every superstep
         cur = 1 - cur;
         if (track) {
             const unsigned long long bits = reduce_max_delta(g);
@@ -520,15 +543,17 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             // AllReduce below is the superstep barrier
             if (!fused)
                 exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
-            unsigned long long c[4];
-            reduce_counters(g, false, c, 4);
+            unsigned long long c[5];
+            reduce_counters(g, false, c, 5);
             zero_edges = c[3];
             if (!cc) m_prev = (uint32_t)(kInf - (uint32_t)reduce_max_delta(g));
             T.end();
             StepRecord& R = g->steps.back();
             R.mode = 1;
-            R.edges_scanned = pull_edges;
-            R.model_bytes = cc ? 8ull * pull_edges + 16ull * n : 12ull * pull_edges + 12ull * n;
+            // the edges whose messages were gathered: absorbed rows / ranges skip theirs, so a
+            // superstep's model bytes count only the gathers it did (SURVEY.md 8(d) per edge)
+            R.edges_scanned = c[4];
+            R.model_bytes = cc ? 8ull * c[4] + 16ull * n : 12ull * c[4] + 12ull * n;
             changed = c[0];
             messages = c[1];
             cur = 1 - cur;

@@ -27,6 +27,40 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
     if (mass) flush_mass(c, mass);   // grid-uniform; whole warps (blocks of 256)
 }
 
+// ---- PageRank hot/cold split of the in-adjacency (built once, on the first pull run) --------
+// pos[e] = 1 if edge e's source is hot (< hot_n), pos[edges] = 0; an exclusive scan then makes
+// pos[e] the number of hot edges before e.
+__global__ void k_hot_flags(const int32_t* __restrict__ idx, int64_t edges, int32_t hot_n,
+                            int32_t* __restrict__ pos) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= edges;
+         e += (int64_t)gridDim.x * blockDim.x)
+        pos[e] = e < edges && idx[e] < hot_n ? 1 : 0;
+}
+// Row offsets of the two parts: hot_off[r] = hot edges before row r, cold_off[r] = the rest.
+__global__ void k_hot_offsets(const int32_t* __restrict__ off, int64_t rows,
+                              const int32_t* __restrict__ pos, int32_t* __restrict__ hot_off,
+                              int32_t* __restrict__ cold_off) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows) return;
+    const int32_t o = off[r];
+    const int32_t h = pos[o];
+    hot_off[r] = h;
+    cold_off[r] = o - h;
+}
+// Stable partition of every row: hot sources first into hot_idx, the others into cold_idx, each
+// keeping the row's order.
+__global__ void k_hot_scatter(const int32_t* __restrict__ idx, int64_t edges, int32_t hot_n,
+                              const int32_t* __restrict__ pos, int32_t* __restrict__ hot_idx,
+                              int32_t* __restrict__ cold_idx) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < edges;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = idx[e];
+        const int32_t p = pos[e];
+        if (u < hot_n) hot_idx[p] = u;
+        else cold_idx[e - p] = u;
+    }
+}
+
 // User programs: broadcaster bitmap of the owned rows from the per-vertex flag bytes (bit 0),
 // for the frontier compaction of a push superstep (ballot per warp).
 __global__ void k_bits_from_flags(const uint8_t* __restrict__ flags, int64_t rows,
