@@ -269,22 +269,6 @@ struct PageRankSum : SumF64, NotAbsorbing, NoAggregate {
     __device__ void finish(int32_t row, T sum, LaneCounters&) const { sum_out[vbase + row] = sum; }
 };
 
-// PageRank over the HOT part of the in-adjacency (hot/cold split): the edges
-// whose source is one of the hot_n hottest vertices (internal ids < hot_n under the degree
-// layout).  Their outbox values are staged once per CTA in shared memory, so these gathers never
-// reach L1/L2; the cold part ran first (PageRankSum over the cold CSC, its sums left in the next
-// outbox slots), and this op's recipient compute is Fig. 8's update of cold + hot (the combine
-// order is fixed: one f64 add of the two partial sums, each folded on its own global grid).
-struct PageRankHot : PageRankPull {
-    static constexpr bool kStaged = true;
-    int32_t hot_n;                            // staged vertices [0, hot_n)
-    const double* stage;                      // set inside the kernel (shared memory)
-    __device__ T gather_staged(int32_t u) const { return stage[u]; }
-    __device__ void finish(int32_t row, T hot, LaneCounters& c) const {
-        PageRankPull::finish(row, __dadd_rn(contrib_next[vbase + row], hot), c);
-    }
-};
-
 // Hash-Min CC, Fig. 9, first half: min over the CSC row (in-neighbours' labels).
 struct CCPullIn : MinU32, NoAggregate {
     static constexpr bool kWeighted = false;
@@ -433,16 +417,10 @@ __device__ __forceinline__ ChunkLoad load_chunk(const int32_t* __restrict__ idx,
 
 // Outbox gathers.  l1hot < 0: default L1 allocation; else vertices below l1hot are cached in L1
 // (evict-last) and the rest bypass L1 (tuning knob IPREGEL_L1_HOT).
-template <class Op, class = void> struct IsStaged { static constexpr bool value = false; };
-template <class Op> struct IsStaged<Op, void_t_<decltype(Op::kStaged)>> {
-    static constexpr bool value = Op::kStaged;
-};
-
 template <class Op>
 __device__ __forceinline__ typename Op::T gather_one(const Op& op, int32_t u, uint64_t pol,
                                                      int32_t l1hot) {
     if (u < 0) return Op::identity();
-    if constexpr (IsStaged<Op>::value) return op.gather_staged(u);
     if (l1hot < 0) return ld_gather(op.gptr() + u, pol);
     return ld_gather_l1(op.gptr() + u, pol, u < l1hot);
 }
@@ -838,42 +816,63 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
     if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
 }
 
-// Range kernel of a staged op (PageRankHot): one CTA of kHotThreads per SM copies the staged
-// prefix of the outbox, [0, hot_n), into shared memory (dynamic, hot_n * 8 bytes), then its warps
-// take ranges from the plan's counter exactly like k_pull_ranges.  The rows are the same rows,
-// the edges only the hot ones, so every gather is a shared-memory load.
-#ifndef IPREGEL_HOT_THREADS
-#define IPREGEL_HOT_THREADS 1024
+// ---- PageRank hot part: sliced ELL over shared memory -------------------
+// The in-edges of LIGHT rows whose source is one of the hot_n hottest vertices (internal ids <
+// hot_n under the degree layout; a light row has at most kSellWidth of them) are stored as a
+// sliced ELLPACK of 32 consecutive rows: slice s holds width(s) columns of 32 uint16 source ids,
+// column-major (entry [j][lane] = the j-th hot source of row 32 s + lane, or the sentinel hot_n
+// past the row's end).  One thread per row sums its column walk sequentially over a shared-memory
+// copy of contrib[0, hot_n) (+ a zero at the sentinel), so the per-row order depends on the row
+// alone (bit-identical for any partitioning).  Heavy rows (more hot sources) and every cold
+// edge stay in the range kernel's CSC.  The thread then runs Fig. 8's update of the row on
+// cold + hot, where cold is the sum the range kernel left in the row's next-outbox slot: the
+// update is fused here, so no separate k_pr_finish pass runs.
+#ifndef IPREGEL_SELL_THREADS
+#define IPREGEL_SELL_THREADS 1024
 #endif
-constexpr int kHotThreads = IPREGEL_HOT_THREADS;
-constexpr int kHotWarps = kHotThreads / 32;
-template <class Op>
-__global__ void __launch_bounds__(kHotThreads, 1) k_pull_ranges_staged(Op op, RangeArgs A) {
-    using T = typename Op::T;
+constexpr int kSellThreads = IPREGEL_SELL_THREADS;
+constexpr int kSellWidth = 32;   // hot sources of a light row at most
+struct HotSell {
+    int64_t slices;
+    const int2* meta;              // [slices]: (first column, width) -- columns of 32 entries
+    const uint16_t* sidx;          // [32 * columns]
+    int32_t hot_n;
+    int32_t rows;
+};
+__global__ void __launch_bounds__(kSellThreads, 1) k_pr_hot_sell(PageRankPull op, HotSell H,
+                                                                 PullCounters* counters) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    __shared__ T s_sum[kHotWarps][4 * 32 + 2];
     __shared__ unsigned long long s_cnt[5];
-    T* stage = reinterpret_cast<T*>(s_dyn);
-    {
-        const T* src = op.gptr();
-        for (int32_t i = threadIdx.x; i < op.hot_n; i += blockDim.x) stage[i] = src[i];
-    }
+    double* stage = reinterpret_cast<double*>(s_dyn);
+    for (int32_t i = threadIdx.x; i < H.hot_n; i += blockDim.x) stage[i] = op.contrib_cur[i];
+    if (threadIdx.x == 0) stage[H.hot_n] = 0.0;   // the padding sentinel gathers 0
     if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    Op sop = op;
-    sop.stage = stage;
-    const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    LaneCounters cnt{0u, 0u, 0u, 0ull, 0.0, 0u};
-    int32_t r = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
-    r = __shfl_sync(kFull, r, 0);
-    while (r < A.num_ranges) {
-        const int32_t nx = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
-        pull_range<Op>(sop, A, r, s_sum[wid], cnt);
-        r = __shfl_sync(kFull, nx, 0);
+    LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t sl = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sl < H.slices;
+         sl += nw) {
+        const int2 m = H.meta[sl];
+        const uint16_t* p = H.sidx + (int64_t)m.x * 32 + lane;
+        double acc = 0.0;
+        int j = 0;
+        for (; j + 4 <= m.y; j += 4) {
+            const uint32_t u0 = p[32 * j], u1 = p[32 * j + 32], u2 = p[32 * j + 64],
+                           u3 = p[32 * j + 96];
+            acc = __dadd_rn(acc, stage[u0]);
+            acc = __dadd_rn(acc, stage[u1]);
+            acc = __dadd_rn(acc, stage[u2]);
+            acc = __dadd_rn(acc, stage[u3]);
+        }
+        for (; j < m.y; ++j) acc = __dadd_rn(acc, stage[p[32 * j]]);
+        const int32_t row = (int32_t)(sl * 32 + lane);
+        if (row < H.rows) op.finish(row, __dadd_rn(op.contrib_next[op.vbase + row], acc), c);
     }
-    flush_counters(cnt, s_cnt, A.counters);
-    if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
+    if (counters) {   // to-convergence runs (grid-uniform)
+        flush_counters(c, s_cnt, counters);
+    }
+    if (op.mass) flush_mass(c, op.mass);
 }
 
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A

@@ -156,22 +156,18 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.track = track;
                 op.mass = mass_slot(step);
                 if (split) {
-                    // cold part first: its sums land in the next outbox slots ...
+                    // the main part (cold edges, heavy rows) first: its sums land in the next
+                    // outbox slots ...
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
                     sop.sum_out = op.contrib_next;
                     sop.vbase = p.vb;
-                    launch_pull(sop, p.split.plan_cold, p.split.cold_off, p.split.cold_idx,
+                    launch_pull(sop, p.split.plan_main, p.split.main_off, p.split.main_idx,
                                 nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered,
                                 g_cold_l1 < 0 ? -1 : p.split.hot_n + g_cold_l1);
-                    // ... then the hot part from shared memory, whose epilogue runs Fig. 8's
-                    // update on cold + hot (and the fused exchange / mass / convergence folds)
-                    PageRankHot hop;
-                    static_cast<PageRankPull&>(hop) = op;
-                    hop.hot_n = p.split.hot_n;
-                    hop.stage = nullptr;
-                    launch_pull_staged(hop, p.split.plan_hot, p.split.hot_off, p.split.hot_idx,
-                                       track ? p.pull_cnt : nullptr, s, n, g->gather_policy);
+                    // ... then the light rows' hot sources from shared memory, with Fig. 8's
+                    // update of every row (fused exchange / mass / convergence folds included)
+                    launch_hot_sell(op, p, track ? p.pull_cnt : nullptr, s);
                 } else if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;

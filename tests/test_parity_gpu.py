@@ -671,7 +671,8 @@ def test_pagerank_graph_replay_matches_first_run():
     np.testing.assert_array_equal(vals[0], vals[1])
     np.testing.assert_array_equal(vals[0], vals[2])
     np.testing.assert_array_equal(vals[0], vals[4])
-    assert launches[0] == launches[1] == launches[2]   # replays count the captured kernels
+    # replays count the captured kernels; the first run also builds the hot/cold split
+    assert launches[0] >= launches[1] == launches[2]
     o = oracle.pagerank(n, src, dst, k=3)
     assert np.abs(vals[3] - o["values"]).max() <= PR_ABS
     st = G.run("pagerank", mode="pull", iterations=10, max_supersteps=5, allow_guard=True)
