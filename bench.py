@@ -395,9 +395,8 @@ def main():
         mb16 = 12.0 * e + 16.0 * n if world == 1 else np.mean(mb) - 8.0 * (n / world)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(),
-                "kernel": "PageRank gather superstep: k_pull_ranges<PageRankSum> over the cold "
-                          "CSC + k_pull_fixup + k_pull_ranges_staged<PageRankHot> (hot sources "
-                          "from shared memory, Fig. 8 update) + k_pull_fixup",
+                "kernel": "PageRank gather superstep: k_pull_ranges<PageRankSum> + "
+                          "k_pull_fixup + k_pr_finish (Fig. 8 update)",
                 "bytes_per_launch": float(np.mean(mb)),
                 "model": "SURVEY.md 8(d): 12 B/edge (4 B index + 8 B gathered f64 outbox) + "
                          "24 B/vertex (CSC offset, out-degree, rank, next outbox)",
@@ -419,8 +418,8 @@ def main():
               "vertex_state_bytes": int(sb),
               "state_bytes_per_vertex": round(sb / (n / world), 2),
               "note": "vertex state is Theta(N) (single-slot mailboxes, PAPER.md:205-211, "
-                      ":476-480); library graph bytes are range plans + the PageRank hot/cold "
-                      "split of the CSC"}
+                      ":476-480); library graph bytes are the range plans (the graph arrays are "
+                      "borrowed)"}
 
     # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
     e2e = None

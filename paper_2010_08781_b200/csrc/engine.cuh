@@ -280,21 +280,6 @@ struct Partition {
     cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
     std::vector<int64_t> wc_bounds;
     AppState st[4];
-    // PageRank hot/cold split of the in-adjacency (built on the first pull run):
-    // the in-edges of light rows from the hot_n hottest sources as a sliced ELL (HotSell), and
-    // every other edge in the "main" CSC over the same rows with its own range plan.
-    struct {
-        int state = 0;              // 0 not built, 1 built
-        int32_t hot_n = 0;
-        int64_t main_edges = 0, main_ebase = 0, sell_edges = 0, sell_entries = 0;
-        int32_t* main_off = nullptr;
-        int32_t* main_idx = nullptr;
-        TilePlan plan_main;
-        int64_t slices = 0;
-        int2* meta = nullptr;
-        uint16_t* sidx = nullptr;
-        DeviceBuffers mem;
-    } split;
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
     unsigned long long* host_cnt = nullptr;   // pinned [16]
@@ -478,12 +463,11 @@ unsigned pull_grid(int64_t num_tiles) {
 template <class Op>
 void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int32_t* idx,
                  const uint32_t* w, PullCounters* cnt, cudaStream_t s, int64_t n_global,
-                 int policy, bool degree_ordered, int32_t l1hot = INT32_MIN) {
+                 int policy, bool degree_ordered) {
     using T = typename Op::T;
     if (P.num_tiles == 0) return;
     RangeArgs A = range_args(P, off, idx, w, cnt, s, op.gather_base(), n_global, sizeof(T), policy,
                              degree_ordered);
-    if (l1hot != INT32_MIN && g_l1_hot == -2) A.l1hot = l1hot;
     k_pull_ranges<Op><<<pull_grid<Op>(P.num_tiles), kPullThreads, 0, s>>>(op, A);
     LAUNCH_CHECK();
     if (P.num_groups) {
@@ -492,34 +476,6 @@ void launch_pull(const Op& op, const TilePlan& P, const int32_t* off, const int3
             static_cast<const T*>(P.head), cnt);
         LAUNCH_CHECK();
     }
-}
-
-// The PageRank hot part (k_pr_hot_sell): one CTA of kSellThreads per SM, hot_n + 1 staged f64.
-void launch_hot_sell(const PageRankPull& op, const Partition& p, PullCounters* cnt,
-                     cudaStream_t s) {
-    static int sms = 0;
-    static size_t attr_bytes = 0;
-    const size_t smem = (size_t)(p.split.hot_n + 1) * sizeof(double);
-    if (!sms) {
-        int dev = 0;
-        CU(cudaGetDevice(&dev));
-        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    if (smem > attr_bytes) {
-        CU(cudaFuncSetAttribute(k_pr_hot_sell, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        attr_bytes = smem;
-    }
-    HotSell H;
-    H.slices = p.split.slices;
-    H.meta = p.split.meta;
-    H.sidx = p.split.sidx;
-    H.hot_n = p.split.hot_n;
-    H.rows = (int32_t)p.rows;
-    const unsigned grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(sms, ceil_div(H.slices, kSellThreads / 32)));
-    k_pr_hot_sell<<<grid, kSellThreads, smem, s>>>(op, H, cnt);
-    LAUNCH_CHECK();
 }
 
 RangeArgs range_args(const TilePlan& P, const int32_t* off, const int32_t* idx, const uint32_t* w,
@@ -853,119 +809,6 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, nullptr, 0, n};
     p.push_cc = PushAdj{o1, i1, w1, o2, i2, w2, 0, n};
     p.push_view_ready = true;
-}
-
-// ---- PageRank hot/cold split ---------------------------------------------
-// Tuning knobs: IPREGEL_HOT_SPLIT (1: on, 0: one range kernel over the whole CSC + k_pr_finish),
-// IPREGEL_HOT_VERTICES (staged hottest vertices, default 16384 = 128 KiB of f64) and
-// IPREGEL_SELL_WIDTH (a light row has at most this many hot sources, default 32).
-int g_hot_split = getenv("IPREGEL_HOT_SPLIT") ? atoi(getenv("IPREGEL_HOT_SPLIT")) : 1;
-int32_t g_hot_vertices = getenv("IPREGEL_HOT_VERTICES") ? atoi(getenv("IPREGEL_HOT_VERTICES"))
-                                                        : 16384;
-int32_t g_sell_width = getenv("IPREGEL_SELL_WIDTH") ? atoi(getenv("IPREGEL_SELL_WIDTH"))
-                                                    : kSellWidth;
-// main kernel: sources [0, hot_n + IPREGEL_COLD_L1) are L1 evict-last (the heavy rows' hot
-// sources and the next hottest), the rest bypass L1 (-1: the default L1 policy for every gather)
-int32_t g_cold_l1 = getenv("IPREGEL_COLD_L1") ? atoi(getenv("IPREGEL_COLD_L1")) : 8192;
-constexpr int32_t kMaxHotVertices = (int32_t)(227 * 1024 / sizeof(double)) - 16;
-
-// Builds every partition's split (collective across ranks: the global edge bases of the main
-// CSC are all-gathered).  Returns false when the split is off.
-bool ensure_hot_split(ipregel_graph* g) {
-    if (!g_hot_split || g->parts.empty()) return false;
-    Partition& p0 = g->parts[0];
-    if (p0.split.state != 0) return true;
-    cudaStream_t s = g->stream;
-    const int32_t hot_n = (int32_t)std::max<int64_t>(
-        1, std::min<int64_t>({(int64_t)std::max(g_hot_vertices, 1), (int64_t)kMaxHotVertices,
-                              g->n, 65535}));
-    const int32_t width = std::max(1, std::min(g_sell_width, 255));
-    for (auto& p : g->parts) {
-        auto& S = p.split;
-        S.hot_n = hot_n;
-        DeviceBuffers tmp;
-        const int64_t E = p.csc_edges;
-        const unsigned eg = std::min<unsigned>(grid_for(E + 1, 256), 148 * 16);
-        // 1. hot sources per row
-        int32_t* pos = tmp.alloc<int32_t>(E + 1, s);
-        int32_t* hl_off = tmp.alloc<int32_t>(p.rows + 1, s);
-        k_hot_flags<<<eg, 256, 0, s>>>(p.csc_idx, E, hot_n, pos);
-        LAUNCH_CHECK();
-        exscan_i32(pos, E + 1, tmp, s);
-        k_gather_at<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(pos, p.csc_off, p.rows + 1, hl_off);
-        LAUNCH_CHECK();
-        // 2. light rows' hot edges only: the flags again, cleared over heavy rows
-        k_hot_flags<<<eg, 256, 0, s>>>(p.csc_idx, E, hot_n, pos);
-        k_clear_heavy<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csc_off, hl_off, p.rows, width, pos);
-        LAUNCH_CHECK();
-        exscan_i32(pos, E + 1, tmp, s);
-        k_gather_at<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(pos, p.csc_off, p.rows + 1, hl_off);
-        LAUNCH_CHECK();
-        int32_t* h = static_cast<int32_t*>(g->pinned.get(sizeof(int32_t), 1));
-        kernel_copy(h, pos + E, sizeof(int32_t), s);
-        CU(cudaStreamSynchronize(s));
-        S.sell_edges = *h;
-        S.main_edges = E - S.sell_edges;
-        // 3. stable partition: light-hot edges to a temporary array, the rest to the main CSC
-        S.main_off = S.mem.alloc<int32_t>(p.rows + 1, s);
-        S.main_idx = S.mem.alloc<int32_t>(S.main_edges, s);
-        int32_t* hl_idx = tmp.alloc<int32_t>(S.sell_edges, s);
-        k_main_offsets<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csc_off, hl_off, p.rows,
-                                                                 S.main_off);
-        k_split_scatter<<<eg, 256, 0, s>>>(p.csc_idx, E, pos, hl_idx, S.main_idx);
-        LAUNCH_CHECK();
-        // 4. sliced ELL: per slice of 32 rows its width (max light-hot degree) and first column
-        S.slices = ceil_div(p.rows, 32);
-        S.meta = S.mem.alloc<int2>(S.slices, s);
-        int32_t* col = tmp.alloc<int32_t>(S.slices + 1, s);
-        k_sell_width<<<grid_for(S.slices * 32, 256), 256, 0, s>>>(hl_off, p.rows, S.slices, col);
-        LAUNCH_CHECK();
-        exscan_i32(col, S.slices + 1, tmp, s);
-        kernel_copy(h, col + S.slices, sizeof(int32_t), s);
-        CU(cudaStreamSynchronize(s));
-        const int64_t columns = *h;
-        S.sell_entries = 32 * columns;
-        S.sidx = S.mem.alloc<uint16_t>(std::max<int64_t>(S.sell_entries, 1), s);
-        k_sell_fill<<<grid_for(S.slices * 32, 256), 256, 0, s>>>(hl_off, hl_idx, p.rows, S.slices,
-                                                                 col, hot_n, S.meta, S.sidx);
-        LAUNCH_CHECK();
-        CU(cudaStreamSynchronize(s));
-        tmp.release();
-    }
-    // global edge bases of the main CSC: partitions in order, then ranks in order
-    int64_t mb = 0;
-    for (auto& p : g->parts) {
-        p.split.main_ebase = mb;
-        mb += p.split.main_edges;
-    }
-    if (multi_rank(g)) {
-        DeviceBuffers tmp;
-        const int W = g->comm->world;
-        int64_t* d = tmp.alloc<int64_t>(1 + W, s);
-        CU(cudaMemcpyAsync(d, &p0.split.main_edges, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        NC(ncclAllGather(d, d + 1, 1, ncclInt64, g->comm->nccl, s));
-        std::vector<int64_t> all(W);
-        CU(cudaMemcpyAsync(all.data(), d + 1, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        tmp.release();
-        p0.split.main_ebase = 0;
-        for (int r = 0; r < g->comm->rank; ++r) p0.split.main_ebase += all[r];
-    }
-    for (auto& p : g->parts) {
-        auto& S = p.split;
-        build_plan(S.plan_main, S.main_off, S.main_idx, nullptr, p.rows, S.main_edges, p.vb,
-                   S.main_ebase, S.mem, s, g->pinned);
-        S.state = 1;
-        if (getenv("IPREGEL_TRACE_SPLIT"))
-            fprintf(stderr, "[ipregel split] rows %lld: main CSC %lld edges; hot part %lld edges in "
-                    "%lld sliced-ELL entries (%.2fx), hot_n %d, width <= %d\n",
-                    (long long)p.rows, (long long)S.main_edges, (long long)S.sell_edges,
-                    (long long)S.sell_entries,
-                    S.sell_edges ? (double)S.sell_entries / (double)S.sell_edges : 0.0, S.hot_n,
-                    width);
-    }
-    CU(cudaStreamSynchronize(s));
-    return true;
 }
 
 // ---- frontier machinery ------------------------------------------------------------------

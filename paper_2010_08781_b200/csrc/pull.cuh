@@ -816,65 +816,6 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
     if constexpr (HasMass<Op>::value) if (op.mass) flush_mass(cnt, op.mass);
 }
 
-// ---- PageRank hot part: sliced ELL over shared memory -------------------
-// The in-edges of LIGHT rows whose source is one of the hot_n hottest vertices (internal ids <
-// hot_n under the degree layout; a light row has at most kSellWidth of them) are stored as a
-// sliced ELLPACK of 32 consecutive rows: slice s holds width(s) columns of 32 uint16 source ids,
-// column-major (entry [j][lane] = the j-th hot source of row 32 s + lane, or the sentinel hot_n
-// past the row's end).  One thread per row sums its column walk sequentially over a shared-memory
-// copy of contrib[0, hot_n) (+ a zero at the sentinel), so the per-row order depends on the row
-// alone (bit-identical for any partitioning).  Heavy rows (more hot sources) and every cold
-// edge stay in the range kernel's CSC.  The thread then runs Fig. 8's update of the row on
-// cold + hot, where cold is the sum the range kernel left in the row's next-outbox slot: the
-// update is fused here, so no separate k_pr_finish pass runs.
-#ifndef IPREGEL_SELL_THREADS
-#define IPREGEL_SELL_THREADS 1024
-#endif
-constexpr int kSellThreads = IPREGEL_SELL_THREADS;
-constexpr int kSellWidth = 32;   // hot sources of a light row at most
-struct HotSell {
-    int64_t slices;
-    const int2* meta;              // [slices]: (first column, width) -- columns of 32 entries
-    const uint16_t* sidx;          // [32 * columns]
-    int32_t hot_n;
-    int32_t rows;
-};
-__global__ void __launch_bounds__(kSellThreads, 1) k_pr_hot_sell(PageRankPull op, HotSell H,
-                                                                 PullCounters* counters) {
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    __shared__ unsigned long long s_cnt[5];
-    double* stage = reinterpret_cast<double*>(s_dyn);
-    for (int32_t i = threadIdx.x; i < H.hot_n; i += blockDim.x) stage[i] = op.contrib_cur[i];
-    if (threadIdx.x == 0) stage[H.hot_n] = 0.0;   // the padding sentinel gathers 0
-    if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    LaneCounters c{0u, 0u, 0u, 0ull, 0.0, 0u};
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t sl = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sl < H.slices;
-         sl += nw) {
-        const int2 m = H.meta[sl];
-        const uint16_t* p = H.sidx + (int64_t)m.x * 32 + lane;
-        double acc = 0.0;
-        int j = 0;
-        for (; j + 4 <= m.y; j += 4) {
-            const uint32_t u0 = p[32 * j], u1 = p[32 * j + 32], u2 = p[32 * j + 64],
-                           u3 = p[32 * j + 96];
-            acc = __dadd_rn(acc, stage[u0]);
-            acc = __dadd_rn(acc, stage[u1]);
-            acc = __dadd_rn(acc, stage[u2]);
-            acc = __dadd_rn(acc, stage[u3]);
-        }
-        for (; j < m.y; ++j) acc = __dadd_rn(acc, stage[p[32 * j]]);
-        const int32_t row = (int32_t)(sl * 32 + lane);
-        if (row < H.rows) op.finish(row, __dadd_rn(op.contrib_next[op.vbase + row], acc), c);
-    }
-    if (counters) {   // to-convergence runs (grid-uniform)
-        flush_counters(c, s_cnt, counters);
-    }
-    if (op.mass) flush_mass(c, op.mass);
-}
-
 // Fig. 8's update of every owned row from the sum PageRankSum left in its next-outbox slot.  A
 // thread takes kPrFinishRows rows (block-strided, coalesced) with their sums loaded up front.
 #ifndef IPREGEL_PR_FINISH_ROWS

@@ -44,8 +44,6 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->pr_mass_cap = k + 1;
     }
     auto mass_slot = [&](uint32_t step) { return mass ? g->pr_mass + 2 * step : nullptr; };
-    // pull supersteps over the hot/cold split of the in-adjacency (built on the first pull run)
-    const bool split = P.mode != IPREGEL_MODE_PUSH && g_pr_split && ensure_hot_split(g);
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -155,20 +153,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.write_rank = write_rank;
                 op.track = track;
                 op.mass = mass_slot(step);
-                if (split) {
-                    // the main part (cold edges, heavy rows) first: its sums land in the next
-                    // outbox slots ...
-                    PageRankSum sop;
-                    sop.contrib_cur = op.contrib_cur;
-                    sop.sum_out = op.contrib_next;
-                    sop.vbase = p.vb;
-                    launch_pull(sop, p.split.plan_main, p.split.main_off, p.split.main_idx,
-                                nullptr, nullptr, s, n, g->gather_policy, g->degree_ordered,
-                                g_cold_l1 < 0 ? -1 : p.split.hot_n + g_cold_l1);
-                    // ... then the light rows' hot sources from shared memory, with Fig. 8's
-                    // update of every row (fused exchange / mass / convergence folds included)
-                    launch_hot_sell(op, p, track ? p.pull_cnt : nullptr, s);
-                } else if (g_pr_split) {
+                if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
                     sop.sum_out = op.contrib_next;

@@ -27,72 +27,6 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
     if (mass) flush_mass(c, mass);   // grid-uniform; whole warps (blocks of 256)
 }
 
-// ---- PageRank hot/cold split of the in-adjacency (built once, on the first pull run) --------
-// pos[e] = 1 if edge e's source is hot (< hot_n), pos[edges] = 0; an exclusive scan then makes
-// pos[e] the number of hot edges before e.
-__global__ void k_hot_flags(const int32_t* __restrict__ idx, int64_t edges, int32_t hot_n,
-                            int32_t* __restrict__ pos) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= edges;
-         e += (int64_t)gridDim.x * blockDim.x)
-        pos[e] = e < edges && idx[e] < hot_n ? 1 : 0;
-}
-// out[i] = a[at[i]] (row starts -> exclusive-scan values at them)
-__global__ void k_gather_at(const int32_t* __restrict__ a, const int32_t* __restrict__ at,
-                            int64_t n, int32_t* __restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = a[at[i]];
-}
-// Rows with more than `width` hot sources (hl_off: hot edges before each row) are heavy: their
-// hot edges stay in the main CSC (flags cleared).
-__global__ void k_clear_heavy(const int32_t* __restrict__ off, const int32_t* __restrict__ hl_off,
-                              int64_t rows, int32_t width, int32_t* __restrict__ pos) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows || hl_off[r + 1] - hl_off[r] <= width) return;
-    for (int32_t e = off[r]; e < off[r + 1]; ++e) pos[e] = 0;
-}
-// main CSC offsets: every edge not moved to the hot part
-__global__ void k_main_offsets(const int32_t* __restrict__ off, const int32_t* __restrict__ hl_off,
-                               int64_t rows, int32_t* __restrict__ main_off) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r <= rows) main_off[r] = off[r] - hl_off[r];
-}
-// Stable partition of every row by the scanned flags: flagged edges to hl_idx (in order), the
-// others to main_idx (in order).
-__global__ void k_split_scatter(const int32_t* __restrict__ idx, int64_t edges,
-                                const int32_t* __restrict__ pos, int32_t* __restrict__ hl_idx,
-                                int32_t* __restrict__ main_idx) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < edges;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t p = pos[e];
-        if (pos[e + 1] != p) hl_idx[p] = idx[e];
-        else main_idx[e - p] = idx[e];
-    }
-}
-// Width of each slice of 32 rows (its largest light-hot degree): one thread per row, warp max.
-__global__ void k_sell_width(const int32_t* __restrict__ hl_off, int64_t rows, int64_t slices,
-                             int32_t* __restrict__ col) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int32_t d = r < rows ? hl_off[r + 1] - hl_off[r] : 0;
-    const int32_t w = (int32_t)__reduce_max_sync(0xFFFFFFFFu, (uint32_t)d);
-    if ((threadIdx.x & 31) == 0 && r / 32 < slices) col[r / 32] = w;
-}
-// Column-major fill of each slice: entry [j][lane] = j-th light-hot source of row 32 s + lane,
-// or the sentinel hot_n past its end; meta[s] = (first column, width).
-__global__ void k_sell_fill(const int32_t* __restrict__ hl_off, const int32_t* __restrict__ hl_idx,
-                            int64_t rows, int64_t slices, const int32_t* __restrict__ col,
-                            int32_t hot_n, int2* __restrict__ meta, uint16_t* __restrict__ sidx) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t sl = r / 32;
-    if (sl >= slices) return;
-    const int lane = (int)(r & 31);
-    const int32_t c0 = col[sl], w = col[sl + 1] - c0;
-    if (lane == 0) meta[sl] = make_int2(c0, w);
-    const int32_t b = r < rows ? hl_off[r] : 0;
-    const int32_t d = r < rows ? hl_off[r + 1] - b : 0;
-    for (int32_t j = 0; j < w; ++j)
-        sidx[((int64_t)c0 + j) * 32 + lane] = (uint16_t)(j < d ? hl_idx[b + j] : hot_n);
-}
-
 // User programs: broadcaster bitmap of the owned rows from the per-vertex flag bytes (bit 0),
 // for the frontier compaction of a push superstep (ballot per warp).
 __global__ void k_bits_from_flags(const uint8_t* __restrict__ flags, int64_t rows,
