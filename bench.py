@@ -409,7 +409,7 @@ def main():
             e / (apps_out["pagerank"]["superstep_ms_median"] * 1e-3) / 1e9)
 
     # device-memory footprint (the Table 3 analog): the user's graph arrays
-    # (borrowed), the library's graph-side memory (plans, hot/cold split) and the vertex state
+    # (borrowed), the library's graph-side memory (range plans) and the vertex state
     gb, sb = G.memory_footprint()
     user_bytes = sum(int(t.numel()) * t.element_size() for t in
                      (part.csc_offsets, part.csc_indices, part.csc_weights, part.csr_offsets,
