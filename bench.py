@@ -145,14 +145,20 @@ def build_graph_device(cfg_name, rank, world):
     from inputs.gpu import config_graph_device
     cfg = inputs.CONFIGS[cfg_name]
     t = time.time()
+    if world == 1:
+        # the user's graph in its ORIGINAL numbering (CSC + weights); the library relabels it
+        # by out-degree during create (IPREGEL_LAYOUT_DEGREE) and derives the out-adjacency
+        g = config_graph_device(cfg, weighted=True, degree_order=False)
+        g["csr_off"] = g["csr_idx"] = g["csr_w"] = None
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        log(f"[rank {rank}] graph {cfg_name}: N={g['n']} E={g['e']} built in {time.time() - t:.1f}s")
+        part = ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], None, None,
+                                  g["csc_w"], None, layout=ipr.LAYOUT_DEGREE)
+        return g, part, np.array([0, g["n"]])
     g = config_graph_device(cfg, weighted=True, degree_order=True)
     torch.cuda.synchronize()
     log(f"[rank {rank}] graph {cfg_name}: N={g['n']} E={g['e']} built in {time.time() - t:.1f}s")
-    if world == 1:
-        part = ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
-                                  g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
-                                  degree_ordered=True)
-        return g, part, np.array([0, g["n"]])
     bounds = ipr.edge_balanced_bounds(g["csc_off"].cpu().numpy(), world, g["csr_off"].cpu().numpy())
     parts = ipr.split_partitions(g["n"], g["e"], bounds, g["csc_off"], g["csc_idx"], g["csr_off"],
                                  g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
@@ -437,7 +443,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
         "config": {"workload": f"{args.config}: R-MAT scale 26 ef 28 seed 5, "
                                f"{'+'.join(args.apps)} per step",
-                   "layout": "degree-ordered internal ids (results in original ids)",
+                   "layout": "original-id CSC relabelled by out-degree by the library "
+                             "(IPREGEL_LAYOUT_DEGREE, at create); results in original ids",
                    "n": n, "e": e, "parallelism": f"1D destination partition x{world}",
                    "l2": "inputs larger than L2 (7.5 GB per adjacency array), no flush",
                    "device": device_info(local),
@@ -539,16 +546,16 @@ def e2e_measure(g, args, msgs_per_step, stream):
     import paper_2010_08781_b200 as ipr
     host = {}
     h2d = 0
-    for k in ("csc_off", "csc_idx", "csc_w", "vertex_ids"):
+    for k in ("csc_off", "csc_idx", "csc_w"):
         t = g[k]
-        if t is None:
-            continue
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         host[k] = h.numpy()
         h2d += h.numel() * h.element_size()
-    part = ipr.Partition(g["n"], g["e"], 0, g["n"], host["csc_off"], host["csc_idx"], None, None,
-                         host["csc_w"], None, host["vertex_ids"], True)
+    # the graph as the user has it: its CSC in ORIGINAL ids + weights; the library uploads it,
+    # relabels it by out-degree (IPREGEL_LAYOUT_DEGREE) and derives the out-adjacency on the device
+    part = ipr.full_partition(g["n"], g["e"], host["csc_off"], host["csc_idx"], None, None,
+                              host["csc_w"], None, layout=ipr.LAYOUT_DEGREE)
     outs = {app: torch.empty(g["n"], dtype=torch.float64 if app == "pagerank" else torch.int32,
                              pin_memory=True) for app in args.apps}
     d2h = 0
@@ -587,9 +594,10 @@ def e2e_measure(g, args, msgs_per_step, stream):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "wall_ms_per_step": wall * 1e3,
             "ms_each_step": [round(x, 2) for x in each],
             "steps": steps,
-            "path": "ipregel_graph_create(IPREGEL_MEMORY_HOST, pinned CSC + weights + vertex ids; "
-                    "CSR derived on the device) + ipregel_run x apps, each followed by "
-                    "ipregel_get_values_async(pinned host) + ipregel_graph_sync + destroy"}
+            "path": "ipregel_graph_create(IPREGEL_MEMORY_HOST, pinned original-id CSC + weights, "
+                    "IPREGEL_LAYOUT_DEGREE: degree relabel + CSR derived on the device) + "
+                    "ipregel_run x apps, each followed by ipregel_get_values_async(pinned host) "
+                    "+ ipregel_graph_sync + destroy"}
 
 
 if __name__ == "__main__":

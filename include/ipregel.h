@@ -148,8 +148,22 @@ typedef struct {
      * pull gathers then keep the hot prefix of the outbox arrays L2-resident (evict-last address
      * range policy) and stream the rest.                                                       */
     int32_t degree_ordered;
-    int32_t reserved;           /* must be 0                                                    */
+    /* ipregel_layout.  IPREGEL_LAYOUT_AS_GIVEN (0): the arrays are used in the given numbering.
+     * IPREGEL_LAYOUT_DEGREE (1): the LIBRARY relabels the graph during create -- internal ids
+     * ascend by decreasing out-degree (ties by original id), the in-adjacency is rebuilt in
+     * library-owned memory with every row's sources in ascending internal order, and the
+     * out-adjacency is derived from it (csr_* may be NULL; if given, only its offsets are read,
+     * for the out-degrees).  The layout is what makes the hot senders' outbox values a
+     * contiguous, cache-resident prefix (the bandwidth pressure of PAPER.md:169); results, the
+     * SSSP source and program ids stay ORIGINAL ids, exactly as with vertex_ids.  Requires
+     * vertex_ids == NULL, degree_ordered == 0 and the whole graph in one partition without a
+     * communicator (else INVALID_ARGUMENT / UNSUPPORTED).  Cost at BASELINE cfg4 (1.88e9 edges):
+     * a degree sort of N keys, a 64-bit radix sort of the E relabelled edges and ~50 GB of
+     * temporary device memory during create.                                                   */
+    int32_t layout;
 } ipregel_graph_desc;
+
+typedef enum { IPREGEL_LAYOUT_AS_GIVEN = 0, IPREGEL_LAYOUT_DEGREE = 1 } ipregel_layout;
 
 typedef struct {
     int32_t mode;                  /* ipregel_mode, default AUTO                                */

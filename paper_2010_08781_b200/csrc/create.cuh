@@ -31,7 +31,18 @@ void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
              "deriving the CSR from the CSC needs the whole graph in one partition");
     if (d->memory != IPREGEL_MEMORY_DEVICE && d->memory != IPREGEL_MEMORY_HOST)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown memory kind %d", d->memory);
-    if (d->reserved != 0) fail(IPREGEL_ERR_INVALID_ARGUMENT, "reserved must be 0");
+    if (d->layout != IPREGEL_LAYOUT_AS_GIVEN && d->layout != IPREGEL_LAYOUT_DEGREE)
+        fail(IPREGEL_ERR_INVALID_ARGUMENT, "unknown layout %d", d->layout);
+    if (d->layout == IPREGEL_LAYOUT_DEGREE) {
+        if (d->vertex_ids || d->degree_ordered)
+            fail(IPREGEL_ERR_INVALID_ARGUMENT,
+                 "IPREGEL_LAYOUT_DEGREE computes the layout: vertex_ids must be NULL and "
+                 "degree_ordered 0");
+        if (d->vertex_begin != 0 || d->vertex_end != d->num_vertices ||
+            d->csc_edges != d->num_edges)
+            fail(IPREGEL_ERR_UNSUPPORTED,
+                 "IPREGEL_LAYOUT_DEGREE needs the whole graph in one partition");
+    }
     if (d->degree_ordered != 0 && d->degree_ordered != 1)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "degree_ordered must be 0 or 1");
     if ((d->vertex_end - d->vertex_begin) + std::max(d->csc_edges, d->csr_edges) > 2147483647LL)
@@ -54,6 +65,133 @@ void compute_fence(cudaStream_t s) {
 // windows of the CSC weights' upload when the CSR is derived (the last window's permutation is
 // all that remains after the upload)
 constexpr int kWeightWindows = 16;   // 8: +1.3 ms, 32: +18 ms (create at cfg4)
+
+// IPREGEL_LAYOUT_DEGREE (include/ipregel.h): internal ids by decreasing out-degree (ties by id),
+// the CSC rebuilt with every row's sources ascending, in library-owned memory; g->vertex_ids
+// becomes the internal -> original map, so results come back in original ids.  The whole graph
+// is one partition (validate_desc).
+void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n, E = p.csc_edges;
+    DeviceBuffers tmp;
+    g_ctrace.mark("relabel begin", s);
+    // 1. out-degrees and the degree order (stable: ties keep ascending ids)
+    uint32_t* deg = tmp.alloc<uint32_t>(n, s, true);
+    if (p.csr_off) {
+        k_degree_from_off<<<grid_for(n, 256), 256, 0, s>>>(p.csr_off, n, deg);
+    } else if (E) {
+        k_degree_hist<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(p.csc_idx, E,
+                                                                                   deg);
+    }
+    LAUNCH_CHECK();
+    int32_t* ids = tmp.alloc<int32_t>(n, s);
+    k_degree_keys<<<grid_for(n, 256), 256, 0, s>>>(deg, n, ids);
+    LAUNCH_CHECK();
+    uint32_t* deg2 = tmp.alloc<uint32_t>(n, s);
+    int32_t* old_of_new = g->graph_mem.alloc<int32_t>(n, s);
+    {
+        size_t tb = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, deg, deg2, ids, old_of_new, n, 0, 32, s));
+        void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
+        CU(cub::DeviceRadixSort::SortPairs(t, tb, deg, deg2, ids, old_of_new, n, 0, 32, s));
+    }
+    int32_t* new_of_old = tmp.alloc<int32_t>(n, s);
+    k_invert_perm<<<grid_for(n, 256), 256, 0, s>>>(old_of_new, n, new_of_old);
+    LAUNCH_CHECK();
+    g_ctrace.mark("relabel order", s);
+    // 2. relabelled edges sorted by (new destination, new source), weights carried along
+    int bits = 1;
+    while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+    int32_t* off = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+    int32_t* idx = p.graph_mem.alloc<int32_t>(std::max<int64_t>(E, 1), s);
+    uint32_t* w = p.csc_w ? p.graph_mem.alloc<uint32_t>(std::max<int64_t>(E, 1), s) : nullptr;
+    if (E) {
+        // every large temporary is allocated once here and reused by the CSR sort of step 4
+        unsigned long long* k0 = tmp.alloc<unsigned long long>(E, s);
+        unsigned long long* k1 = tmp.alloc<unsigned long long>(E, s);
+        int32_t* spare = tmp.alloc<int32_t>(E, s);
+        int32_t* row = tmp.alloc<int32_t>(E, s);
+        k_relabel_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(p.csc_off, p.csc_idx, p.rows,
+                                                                  new_of_old, bits, k0);
+        LAUNCH_CHECK();
+        cub::DoubleBuffer<unsigned long long> keys(k0, k1);
+        size_t tb = 0;
+        if (w) {
+            // the sort carries each edge's CSC position, so it needs the structure only (from
+            // host memory the weights are still uploading); the weights follow by a gather
+            uint32_t* pos0 = reinterpret_cast<uint32_t*>(spare);
+            uint32_t* pos1 = reinterpret_cast<uint32_t*>(row);
+            k_iota_u32<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(pos0, E);
+            LAUNCH_CHECK();
+            cub::DoubleBuffer<uint32_t> vals(pos0, pos1);
+            CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, E, 0, 2 * bits, s));
+            void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
+            CU(cub::DeviceRadixSort::SortPairs(t, tb, keys, vals, E, 0, 2 * bits, s));
+            if (d.memory == IPREGEL_MEMORY_HOST) CU(cudaStreamWaitEvent(s, p.up_w, 0));
+            k_gather_u32<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+                vals.Current(), E, p.csc_w, w);
+            LAUNCH_CHECK();
+        } else {
+            CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, E, 0, 2 * bits, s));
+            void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
+            CU(cub::DeviceRadixSort::SortKeys(t, tb, keys, E, 0, 2 * bits, s));
+        }
+        g_ctrace.mark("relabel sorted", s);
+        // 3. indices + offsets (run lengths of the sorted destinations, then a scan)
+        k_relabel_unpack<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+            keys.Current(), E, bits, idx, row);
+        LAUNCH_CHECK();
+        int32_t* st = tmp.alloc<int32_t>(n, s, true);
+        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(row, E, st,
+                                                                                  off);
+        k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, off);
+        LAUNCH_CHECK();
+        exscan_i32(off, n + 1, tmp, s);
+        g_ctrace.mark("relabel csc", s);
+        // 4. the out-adjacency: the same edges by (new source), a stable sort of the CSC order
+        //    (each CSR row lists its destinations ascending), in the buffers of step 2
+        int32_t* roff = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+        int32_t* ridx = p.graph_mem.alloc<int32_t>(E, s);
+        uint32_t* rw = w ? p.graph_mem.alloc<uint32_t>(E, s) : nullptr;
+        int32_t* kk0 = row;   // E int32 each
+        int32_t* kk1 = spare;
+        CU(cudaMemcpyAsync(kk0, idx, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, k0);
+        LAUNCH_CHECK();
+        cub::DoubleBuffer<int32_t> tkeys(kk0, kk1);
+        cub::DoubleBuffer<unsigned long long> tvals(k0, k1);
+        size_t tb2 = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys, tvals, E, 0, bits, s));
+        void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
+        CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, s));
+        k_transpose_unpack<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+            tvals.Current(), E, w, ridx, rw, nullptr);
+        LAUNCH_CHECK();
+        CU(cudaMemsetAsync(st, 0, n * sizeof(int32_t), s));
+        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+            tkeys.Current(), E, st, roff);
+        k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, roff);
+        LAUNCH_CHECK();
+        exscan_i32(roff, n + 1, tmp, s);
+        p.csr_off = roff;
+        p.csr_idx = ridx;
+        p.csr_w = rw;
+    } else {
+        p.csr_off = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+        p.csr_idx = p.graph_mem.alloc<int32_t>(1, s);
+        p.csr_w = w ? p.graph_mem.alloc<uint32_t>(1, s) : nullptr;
+    }
+    CU(cudaStreamSynchronize(s));
+    tmp.release();
+    p.csc_off = off;
+    p.csc_idx = idx;
+    p.csc_w = w;
+    p.csr_edges = E;
+    g->vertex_ids = old_of_new;
+    g->degree_ordered = true;
+    g->gather_policy = g_gather_policy >= 0 ? g_gather_policy : 3;
+    g_ctrace.mark("relabel done", s);
+}
 
 void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
     cudaStream_t s = g->stream;
@@ -94,9 +232,11 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         up(ridx_d, d.csr_indices, d.csr_edges * 4);
         CU(cudaEventRecord(p.up_idx, cs));
         g_ctrace.mark("uploaded structure", cs);
-        int windows = (derive && w_d && d.csc_edges >= (int64_t(1) << 24)) ? kWeightWindows : 1;
+        const bool relabel = d.layout == IPREGEL_LAYOUT_DEGREE;
+        int windows = (derive && !relabel && w_d && d.csc_edges >= (int64_t(1) << 24))
+                          ? kWeightWindows : 1;
         if (const char* e = getenv("IPREGEL_WEIGHT_WINDOWS"))   // test hook
-            if (derive && w_d) windows = std::max(1, std::min(atoi(e), 64));
+            if (derive && !relabel && w_d) windows = std::max(1, std::min(atoi(e), 64));
         p.wc_bounds.assign(1, 0);
         for (int c = 0; c < windows; ++c) {
             const int64_t lo = d.csc_edges * c / windows, hi = d.csc_edges * (c + 1) / windows;
@@ -155,14 +295,16 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
                  (h & 4) ? "index out of range" : "");
     }
     g_ctrace.mark("validated", s);
-    if (!d.csr_offsets && !d.csr_indices) {
+    const bool relabel = d.layout == IPREGEL_LAYOUT_DEGREE;
+    if (relabel) relabel_by_degree(g, p, d);
+    if (!relabel && !d.csr_offsets && !d.csr_indices) {
         // out-adjacency (and its weights) derived from the CSC on the device: the transpose of
         // the whole graph's in-edges (single partition, checked by validate_desc;
         // after the validation: the transpose indexes by the CSC sources)
         int32_t *o, *ix;
         uint32_t* wx = nullptr;
         transpose_rows(p, g->n, p.csc_off, p.csc_idx, p.csc_w, p.csc_edges, p.csc_w != nullptr, s,
-                       &o, &ix, &wx, d.memory == IPREGEL_MEMORY_HOST);
+                       &o, &ix, &wx, d.memory == IPREGEL_MEMORY_HOST && !relabel);
         p.csr_off = o;
         p.csr_idx = ix;
         p.csr_w = wx;

@@ -243,6 +243,67 @@ __global__ void k_transpose_unpack(const unsigned long long* __restrict__ vals, 
     }
 }
 
+// ---- IPREGEL_LAYOUT_DEGREE: the library's own degree relabel (create time) -----------------
+// out-degrees from CSR offsets, or counted over the CSC sources
+__global__ void k_degree_from_off(const int32_t* __restrict__ off, int64_t n,
+                                  uint32_t* __restrict__ deg) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) deg[v] = (uint32_t)(off[v + 1] - off[v]);
+}
+__global__ void k_degree_hist(const int32_t* __restrict__ idx, int64_t edges,
+                              uint32_t* __restrict__ deg) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < edges;
+         e += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(deg + idx[e], 1u);
+}
+// sort keys: ascending ~deg = descending degree; a stable sort keeps ties in id order
+__global__ void k_degree_keys(uint32_t* __restrict__ deg, int64_t n, int32_t* __restrict__ ids) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        deg[v] = ~deg[v];
+        ids[v] = (int32_t)v;
+    }
+}
+__global__ void k_invert_perm(const int32_t* __restrict__ old_of_new, int64_t n,
+                              int32_t* __restrict__ new_of_old) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) new_of_old[old_of_new[i]] = (int32_t)i;
+}
+__global__ void k_iota_u32(uint32_t* __restrict__ a, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+// out[i] = in[perm[i]]
+__global__ void k_gather_u32(const uint32_t* __restrict__ perm, int64_t n,
+                             const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[perm[i]];
+}
+// relabelled edge keys: (new destination << bits) | new source, one warp per CSC row
+__global__ void k_relabel_pack(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
+                               int64_t rows, const int32_t* __restrict__ new_of_old, int bits,
+                               unsigned long long* __restrict__ keys) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const unsigned long long hi = (unsigned long long)(uint32_t)new_of_old[r] << bits;
+    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32)
+        keys[e] = hi | (uint32_t)new_of_old[idx[e]];
+}
+// sorted keys -> new CSC indices + each edge's new row (for the run-length offsets)
+__global__ void k_relabel_unpack(const unsigned long long* __restrict__ keys, int64_t edges,
+                                 int bits, int32_t* __restrict__ idx, int32_t* __restrict__ row) {
+    const unsigned long long mask = (1ull << bits) - 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        idx[i] = (int32_t)(k & mask);
+        row[i] = (int32_t)(k >> bits);
+    }
+}
+
 // One window [lo, hi) of the deferred weight permutation: wx[i] = w[perm[i]] where perm[i] falls
 // in the window (the window's upload has landed; the others are written by their own passes).
 __global__ void k_permute_window(const int32_t* __restrict__ perm, int64_t edges, int64_t lo,

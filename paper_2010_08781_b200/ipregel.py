@@ -44,6 +44,7 @@ COMBINER_OF = {APP_PAGERANK: COMBINE_SUM, APP_HASHMIN_CC: COMBINE_MIN, APP_SSSP:
 MODES = {"auto": MODE_AUTO, "pull": MODE_PULL, "push": MODE_PUSH}
 RUN_EXCHANGE_COLLECTIVE, RUN_EXCHANGE_FUSED = 0x1, 0x2
 RUN_PAGERANK_MASS = 0x4
+LAYOUT_AS_GIVEN, LAYOUT_DEGREE = 0, 1
 EXCHANGES = {"auto": 0, "collective": RUN_EXCHANGE_COLLECTIVE, "fused": RUN_EXCHANGE_FUSED}
 EXCHANGE_NAMES = {0: "none", 1: "collective", 2: "fused"}
 
@@ -65,7 +66,7 @@ class GraphDesc(ctypes.Structure):
         ("csr_weights", ctypes.c_void_p),
         ("memory", ctypes.c_int32), ("validate", ctypes.c_int32),
         ("vertex_ids", ctypes.c_void_p), ("degree_ordered", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("layout", ctypes.c_int32),
     ]
 
 
@@ -304,6 +305,7 @@ class Partition:
     csr_weights: object = None
     vertex_ids: object = None        # original id of each internal vertex (full [N]) or None
     degree_ordered: bool = False
+    layout: int = 0                  # LAYOUT_DEGREE: the library relabels by out-degree
 
     def desc(self, validate: bool = False) -> GraphDesc:
         host = isinstance(self.csc_offsets, np.ndarray)
@@ -324,7 +326,7 @@ class Partition:
         d.validate = 1 if validate else 0
         d.vertex_ids = _ptr(self.vertex_ids)
         d.degree_ordered = 1 if self.degree_ordered else 0
-        d.reserved = 0
+        d.layout = int(self.layout)
         return d
 
 
@@ -465,10 +467,11 @@ class Graph:
 
 def full_partition(n: int, e: int, csc_offsets, csc_indices, csr_offsets, csr_indices,
                    csc_weights=None, csr_weights=None, vertex_ids=None,
-                   degree_ordered=False) -> Partition:
-    """The whole graph as one partition (single GPU)."""
+                   degree_ordered=False, layout: int = LAYOUT_AS_GIVEN) -> Partition:
+    """The whole graph as one partition (single GPU).  layout=LAYOUT_DEGREE: the library
+    relabels it by out-degree during create (vertex_ids None, degree_ordered False)."""
     return Partition(n, e, 0, n, csc_offsets, csc_indices, csr_offsets, csr_indices,
-                     csc_weights, csr_weights, vertex_ids, degree_ordered)
+                     csc_weights, csr_weights, vertex_ids, degree_ordered, layout)
 
 
 def split_partitions(n: int, e: int, bounds, csc_offsets, csc_indices, csr_offsets, csr_indices,

@@ -770,3 +770,93 @@ def test_get_values_async_matches_sync(ids, parts):
     for app in want:
         np.testing.assert_array_equal(got[app].numpy().view(want[app].dtype), want[app])
     G.close()
+
+
+# ------------------------------------------------------------------ library degree relabel
+
+@pytest.mark.parametrize("memory", ["device", "host"])
+@pytest.mark.parametrize("with_csr", [True, False])
+@pytest.mark.parametrize("seed", range(3))
+def test_layout_degree_matches_oracle(seed, memory, with_csr):
+    """IPREGEL_LAYOUT_DEGREE: the library relabels an original-id graph by out-degree during
+    create; every app's results (in original ids), counters and the SSSP source (an original id)
+    equal the oracle's, and the internal CSC it built is degree-ordered with sorted rows."""
+    import paper_2010_08781_b200 as ipr
+    rng = np.random.default_rng(5100 + seed)
+    n = int(rng.integers(2, 4000))
+    src, dst, w = checkers.random_graph(rng, n, int(rng.integers(0, 8 * n)), weighted=True)
+    g = csr_csc(n, src, dst, w)
+    host = memory == "host"
+    if host:
+        arr = {k: (None if g[k] is None else np.ascontiguousarray(g[k]).view(np.int32))
+               for k in ("csc_off", "csc_idx", "csc_w", "csr_off", "csr_idx", "csr_w")}
+    else:
+        from tests.graphs import to_device
+        arr = to_device(g)
+    p = ipr.full_partition(n, len(src), arr["csc_off"], arr["csc_idx"],
+                           arr["csr_off"] if with_csr else None,
+                           arr["csr_idx"] if with_csr else None, arr["csc_w"],
+                           arr["csr_w"] if with_csr else None, layout=ipr.LAYOUT_DEGREE)
+    G = ipr.Graph(p, validate=True)
+    source = int(rng.integers(0, n))
+    for app in ("pagerank", "cc", "sssp"):
+        G.run(app, mode="pull" if app == "pagerank" else "auto", source=source, mass=app == "pagerank")
+        v = G.values(host=True)
+        s = G.stats()
+        if app == "pagerank":
+            o = oracle.pagerank(n, src, dst, k=10)
+            assert np.abs(v - o["values"]).max() <= PR_ABS
+            assert (np.abs(v - o["values"]) / o["values"]).max() <= PR_REL
+            nd = int(np.count_nonzero(np.bincount(np.asarray(src, np.int64), minlength=n)))
+            checkers.assert_pagerank_mass(s, n, nd)
+        else:
+            o = oracle.run(oracle.APP_HASHMIN_CC if app == "cc" else oracle.APP_SSSP, n, src, dst,
+                           w if app == "sssp" else None, source=source)
+            np.testing.assert_array_equal(v, o["values"])
+        assert s["supersteps"] == o["supersteps"]
+        np.testing.assert_array_equal(s["changed"], o["changed"])
+        np.testing.assert_array_equal(s["messages"], o["messages"])
+    G.close()
+
+
+def test_layout_degree_equals_fixture_layout_bitwise():
+    """The library's relabel and the fixture's degree-ordered layout (inputs/gpu.py, the same
+    order: decreasing out-degree, ties by id) give bit-identical PageRank values."""
+    import paper_2010_08781_b200 as ipr
+    from inputs.gpu import config_graph_device
+    g0 = config_graph_device("cfg0", weighted=False, degree_order=False)
+    g1 = config_graph_device("cfg0", weighted=False, degree_order=True)
+    Ga = ipr.Graph(ipr.full_partition(g0["n"], g0["e"], g0["csc_off"], g0["csc_idx"], None, None,
+                                      layout=ipr.LAYOUT_DEGREE))
+    Gb = ipr.Graph(ipr.full_partition(g1["n"], g1["e"], g1["csc_off"], g1["csc_idx"],
+                                      g1["csr_off"], g1["csr_idx"], None, None, g1["vertex_ids"],
+                                      degree_ordered=True))
+    Ga.run("pagerank", mode="pull")
+    Gb.run("pagerank", mode="pull")
+    np.testing.assert_array_equal(Ga.values(host=True), Gb.values(host=True))
+    Ga.close()
+    Gb.close()
+
+
+def test_layout_degree_rejects_bad_combinations():
+    import ctypes
+
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    n = 10
+    src = np.array([0, 1, 2], np.int64)
+    dst = np.array([1, 2, 3], np.int64)
+    d = to_device(csr_csc(n, src, dst, None))
+    ids = __import__("torch").arange(n, dtype=__import__("torch").int32, device="cuda")
+    for kw in ({"vertex_ids": ids}, {"degree_ordered": True}):
+        p = ipr.full_partition(n, 3, d["csc_off"], d["csc_idx"], None, None,
+                               layout=ipr.LAYOUT_DEGREE, **kw)
+        h = ctypes.c_void_p()
+        st = ipr.load().ipregel_graph_create(ctypes.byref(p.desc()), None, None, ctypes.byref(h))
+        assert st == ipr.ERR_INVALID_ARGUMENT
+    bad = ipr.full_partition(n, 3, d["csc_off"], d["csc_idx"], None, None)
+    desc = bad.desc()
+    desc.layout = 7
+    h = ctypes.c_void_p()
+    assert ipr.load().ipregel_graph_create(ctypes.byref(desc), None, None,
+                                           ctypes.byref(h)) == ipr.ERR_INVALID_ARGUMENT
