@@ -45,7 +45,10 @@ void validate_desc(const ipregel_graph_desc* d, int64_t* n_out) {
     }
     if (d->degree_ordered != 0 && d->degree_ordered != 1)
         fail(IPREGEL_ERR_INVALID_ARGUMENT, "degree_ordered must be 0 or 1");
-    if ((d->vertex_end - d->vertex_begin) + std::max(d->csc_edges, d->csr_edges) > 2147483647LL)
+    // the range kernels walk int32 merge coordinates and look up to 3 chunks (3 * 128 edges)
+    // past the current one: keep a margin of 4 chunks below INT32_MAX
+    if ((d->vertex_end - d->vertex_begin) + std::max(d->csc_edges, d->csr_edges) >
+        2147483647LL - 4 * kChunk)
         fail(IPREGEL_ERR_UNSUPPORTED, "rows + edges of a partition beyond int32 merge coordinates");
     *n_out = d->num_vertices;
 }
@@ -80,7 +83,7 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     if (p.csr_off) {
         k_degree_from_off<<<grid_for(n, 256), 256, 0, s>>>(p.csr_off, n, deg);
     } else if (E) {
-        k_degree_hist<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(p.csc_idx, E,
+        k_degree_hist<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(p.csc_idx, E,
                                                                                    deg);
     }
     LAUNCH_CHECK();
@@ -121,14 +124,14 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
             // host memory the weights are still uploading); the weights follow by a gather
             uint32_t* pos0 = reinterpret_cast<uint32_t*>(spare);
             uint32_t* pos1 = reinterpret_cast<uint32_t*>(row);
-            k_iota_u32<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(pos0, E);
+            k_iota_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(pos0, E);
             LAUNCH_CHECK();
             cub::DoubleBuffer<uint32_t> vals(pos0, pos1);
             CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, E, 0, 2 * bits, s));
             void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
             CU(cub::DeviceRadixSort::SortPairs(t, tb, keys, vals, E, 0, 2 * bits, s));
             if (d.memory == IPREGEL_MEMORY_HOST) CU(cudaStreamWaitEvent(s, p.up_w, 0));
-            k_gather_u32<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+            k_gather_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
                 vals.Current(), E, p.csc_w, w);
             LAUNCH_CHECK();
         } else {
@@ -138,11 +141,11 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         }
         g_ctrace.mark("relabel sorted", s);
         // 3. indices + offsets (run lengths of the sorted destinations, then a scan)
-        k_relabel_unpack<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+        k_relabel_unpack<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
             keys.Current(), E, bits, idx, row);
         LAUNCH_CHECK();
         int32_t* st = tmp.alloc<int32_t>(n, s, true);
-        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(row, E, st,
+        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(row, E, st,
                                                                                   off);
         k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, off);
         LAUNCH_CHECK();
@@ -164,11 +167,11 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys, tvals, E, 0, bits, s));
         void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
         CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, s));
-        k_transpose_unpack<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+        k_transpose_unpack<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
             tvals.Current(), E, w, ridx, rw, nullptr);
         LAUNCH_CHECK();
         CU(cudaMemsetAsync(st, 0, n * sizeof(int32_t), s));
-        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), 148 * 16), 256, 0, s>>>(
+        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
             tkeys.Current(), E, st, roff);
         k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, roff);
         LAUNCH_CHECK();
@@ -315,7 +318,7 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
             if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
             for (size_t c = 0; c + 1 < p.wc_bounds.size(); ++c) {
                 CU(cudaStreamWaitEvent(g->aux_stream, p.up_wc[c], 0));
-                k_permute_window<<<148 * 8, 256, 0, g->aux_stream>>>(
+                k_permute_window<<<sm_grid(8), 256, 0, g->aux_stream>>>(
                     p.pend.perm, p.pend.edges, p.wc_bounds[c], p.wc_bounds[c + 1], p.pend.w,
                     p.pend.wx);
                 LAUNCH_CHECK();

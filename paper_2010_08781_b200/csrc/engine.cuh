@@ -51,6 +51,19 @@ std::atomic<unsigned long long> g_launches{0};
         CU(cudaGetLastError());                          \
     } while (0)
 
+// SM count of a device (cached): grid-stride kernels launch a few CTAs per SM.
+int device_sms(int device = -1) {
+    static int cache[64] = {};
+    if (device < 0) CU(cudaGetDevice(&device));
+    if (device >= 0 && device < 64 && cache[device]) return cache[device];
+    int v = 0;
+    CU(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    if (device >= 0 && device < 64) cache[device] = v;
+    return v;
+}
+// grid of `per_sm` CTAs on every SM of the current device
+inline unsigned sm_grid(int per_sm) { return (unsigned)(device_sms() * per_sm); }
+
 // Tuning knob read once per process: L2 policy of the pull gathers (-1 = per graph: range policy
 // for degree-ordered layouts, else evict_last).
 int read_gather_policy() {
@@ -374,7 +387,7 @@ void kernel_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (bytes == 0) return;
     if (bytes % 4) fail(IPREGEL_ERR_INVALID_ARGUMENT, "kernel_copy of %zu bytes", bytes);
     const int64_t n = (int64_t)(bytes / 4);
-    k_copy_words<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, s>>>(
+    k_copy_words<<<std::min<unsigned>(grid_for(n, 256), sm_grid(8)), 256, 0, s>>>(
         static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), n);
     LAUNCH_CHECK();
 }
@@ -763,12 +776,12 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
             p.pend.wx = wx;
             p.pend.edges = edges;
         }
-        k_transpose_unpack<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
+        k_transpose_unpack<<<std::min<unsigned>(grid_for(edges, 256), sm_grid(16)), 256, 0, s>>>(
             vals.Current(), edges, w, ix, wx, perm);
         LAUNCH_CHECK();
         // offsets from the sorted sources: run lengths, then an exclusive scan
         int32_t* st = tmp.alloc<int32_t>(n, s, true);
-        k_run_bounds<<<std::min<unsigned>(grid_for(edges, 256), 148 * 16), 256, 0, s>>>(
+        k_run_bounds<<<std::min<unsigned>(grid_for(edges, 256), sm_grid(16)), 256, 0, s>>>(
             keys.Current(), edges, st, o);
         k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, o);
         LAUNCH_CHECK();

@@ -58,7 +58,7 @@ template <class Op> struct PullMinBlocks<Op, void_t_<decltype(Op::kMinBlocks)>> 
 #ifndef IPREGEL_PULL_THREADS
 #define IPREGEL_PULL_THREADS 256
 #endif
-constexpr int kPullThreads = IPREGEL_PULL_THREADS;  // 8 warps per CTA
+constexpr int kPullThreads = IPREGEL_PULL_THREADS;  // range-kernel CTA size (build knob)
 constexpr int kWarpsPerCta = kPullThreads / 32;
 constexpr int kChunk = 128;                       // edges per warp step
 #ifndef IPREGEL_RANGE_ITEMS

@@ -403,7 +403,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 const PushAdj& adj = cc ? p.push_cc : p.push_sssp;
                 build_expand_list(g, p, S, adj, S.g_id, S.g_val, S.g_len, (int64_t)frontier_len);
                 const unsigned grid = (unsigned)std::min<int64_t>(
-                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), 148 * 8);
+                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), sm_grid(8));
                 if (cc)
                     k_expand<1><<<grid, kExpandThreads, 0, s>>>(
                         adj, S.e_id, S.e_val, S.e_pre, &p.front_cnt->list_len,
@@ -447,7 +447,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 build_expand_list(g, p, S, own, S.f_id, nullptr, &p.front_cnt->changed,
                                   (int64_t)p.host_cnt[4]);
                 const unsigned grid = (unsigned)std::min<int64_t>(
-                    std::max<int64_t>(ceil_div((int64_t)p.host_cnt[5], kExpandItems), 1), 148 * 8);
+                    std::max<int64_t>(ceil_div((int64_t)p.host_cnt[5], kExpandItems), 1), sm_grid(8));
                 k_rowlist_min<<<grid, kExpandThreads, 0, s>>>(
                     own, S.e_id, S.e_pre, &p.front_cnt->list_len, &p.front_cnt->list_edges,
                     S.val[cur], S.val[1 - cur]);

@@ -33,6 +33,7 @@ struct ipregel_program {
     std::string lowered[PK_COUNT];
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k[PK_COUNT] = {};
+    int pull_per_sm[2] = {1, 1};   // resident CTAs per SM of the loaded range kernels
 };
 
 namespace {
@@ -153,15 +154,28 @@ void compile_program(ipregel_program* pr, const ipregel_program_desc& d) {
                              kJitHeaderBodies, kJitHeaderNames);
     if (r != NVRTC_SUCCESS) fail(IPREGEL_ERR_CUDA, "nvrtcCreateProgram: %s", N.err(r));
     for (int i = 0; i < PK_COUNT; ++i) N.add_name(prog, kProgKernelNames[i]);
-    // IEEE arithmetic as written (no FMA contraction), the oracle's convention (R7)
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                          "-default-device", "--ptxas-options=-v",
-                          "-DIPREGEL_JIT=1", nullptr};
-    // tuning knob: one extra NVRTC option (e.g. -DIPREGEL_PROG_MINBLOCKS8=3)
+    // IEEE arithmetic as written (no FMA contraction), the oracle's convention (R7).
+    // Every build-time knob of the range kernels is passed on, so the JIT kernels are the same
+    // shape as the host launches them (CTA size, warps per CTA, range size, unroll, paths).
+    const std::string knobs[] = {
+        "-DIPREGEL_PULL_THREADS=" + std::to_string(kPullThreads),
+        "-DIPREGEL_PULL_MINBLOCKS=" + std::to_string(IPREGEL_PULL_MINBLOCKS),
+        "-DIPREGEL_PROG_MINBLOCKS8=" + std::to_string(IPREGEL_PROG_MINBLOCKS8),
+        "-DIPREGEL_RANGE_ITEMS=" + std::to_string(kRangeItems),
+        "-DIPREGEL_CHUNK_UNROLL=" + std::to_string(kChunkUnroll),
+        "-DIPREGEL_U32_ONE_END=" + std::to_string(IPREGEL_U32_ONE_END),
+        "-DIPREGEL_IDX_PREFETCH=" + std::to_string(IPREGEL_IDX_PREFETCH),
+        "-DIPREGEL_GATHER_HINT=" + std::to_string(IPREGEL_GATHER_HINT),
+        "-DIPREGEL_STREAM_CS=" + std::to_string(IPREGEL_STREAM_CS)};
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false",
+                                     "-lineinfo", "-default-device", "--ptxas-options=-v",
+                                     "-DIPREGEL_JIT=1"};
+    for (const std::string& k : knobs) opts.push_back(k.c_str());
+    // tuning knob: one extra NVRTC option (e.g. -DIPREGEL_PROG_MINBLOCKS8=3 -- the launch reads
+    // the resident CTAs of the loaded kernel, so it stays consistent)
     const char* extra = getenv("IPREGEL_NVRTC_OPT");
-    int nopts = (int)(sizeof(opts) / sizeof(opts[0])) - 1;
-    if (extra && *extra) opts[nopts++] = extra;
-    r = N.compile(prog, nopts, opts);
+    if (extra && *extra) opts.push_back(extra);
+    r = N.compile(prog, (int)opts.size(), opts.data());
     size_t ls = 0;
     N.log_size(prog, &ls);
     std::string log(ls, '\0');
@@ -193,6 +207,19 @@ void ensure_program_loaded(ipregel_program* pr) {
     CU(cudaLibraryLoadData(&pr->lib, pr->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     for (int i = 0; i < PK_COUNT; ++i)
         CU(cudaLibraryGetKernel(&pr->k[i], pr->lib, pr->lowered[i].c_str()));
+    // the range kernels launch with kPullThreads: check the loaded kernels accept that, and take
+    // their resident CTAs per SM from the occupancy of the kernel actually loaded
+    for (int pass = 0; pass < 2; ++pass) {
+        cudaFuncAttributes fa;
+        CU(cudaFuncGetAttributes(&fa, (const void*)pr->k[PK_PULL0 + pass]));
+        if (fa.maxThreadsPerBlock < kPullThreads)
+            fail(IPREGEL_ERR_UNSUPPORTED, "program range kernel takes %d threads per CTA, the "
+                 "launch needs %d", fa.maxThreadsPerBlock, kPullThreads);
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, (const void*)pr->k[PK_PULL0 + pass], kPullThreads, 0));
+        pr->pull_per_sm[pass] = std::max(per_sm, 1);
+    }
 }
 
 void launch_jit(cudaKernel_t k, unsigned grid, unsigned block, void** args, cudaStream_t s) {
@@ -256,11 +283,9 @@ void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, 
     RangeArgs A = range_args(P, off, idx, w, cnt, g->stream, a.out_cur, g->n, sizeof(V),
                              g->gather_policy, g->degree_ordered);
     void* args[] = {&a, &A};
-    // resident CTAs per SM = the op's launch bound (the JIT kernels carry the same bounds)
-    static int sms = 0;
-    if (!sms) CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    // resident CTAs per SM of the loaded JIT kernel (its occupancy, ensure_program_loaded)
     const int64_t need = ceil_div(P.num_tiles, kWarpsPerCta);
-    const int64_t resident = (int64_t)sms * (sizeof(V) == 8 ? IPREGEL_PROG_MINBLOCKS8 : IPREGEL_PULL_MINBLOCKS);
+    const int64_t resident = (int64_t)device_sms(g->device) * pr->pull_per_sm[pass];
     const unsigned grid = (unsigned)(g_pull_waves == 0 || !A.range_ctr
                                          ? need : std::min<int64_t>(need, resident * g_pull_waves));
     launch_jit(pr->k[PK_PULL0 + pass], grid, kPullThreads,
@@ -433,7 +458,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
         ProgArgs<V> a = args_for(p, 0, 1);   // out_next = buffer 0
         PullCounters* cnt = p.pull_cnt;
         void* args[] = {&a, &cnt};
-        launch_jit(pr->k[PK_INIT], std::min<unsigned>(grid_for(p.rows, 256), 148 * 16), 256, args, s);
+        launch_jit(pr->k[PK_INIT], std::min<unsigned>(grid_for(p.rows, 256), sm_grid(16)), 256, args, s);
     }
     T0.kend();
     exchange(0);
@@ -491,7 +516,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
                 build_expand_list(g, p, S, adj, S.g_id, nullptr, S.g_len, (int64_t)frontier_len);
                 ProgArgs<V> a = args_for(p, step, cur);
                 const unsigned grid = (unsigned)std::min<int64_t>(
-                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), 148 * 8);
+                    std::max<int64_t>(ceil_div((int64_t)messages, kExpandItems), 1), sm_grid(8));
                 PushAdj ad = adj;
                 const int32_t* eid = S.e_id;
                 const long long* epre = S.e_pre;
@@ -535,7 +560,7 @@ ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max
                 PullCounters* cnt = p.pull_cnt;
                 void* args[] = {&a, &cnt};
                 launch_jit(pr->k[PK_PULL_APPLY],
-                           std::min<unsigned>(grid_for(ceil_div(p.rows, kProgPullRows), 256), 148 * 16),
+                           std::min<unsigned>(grid_for(ceil_div(p.rows, kProgPullRows), 256), sm_grid(16)),
                            256, args, s);
             }
             T.kend();

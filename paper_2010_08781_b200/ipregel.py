@@ -354,11 +354,13 @@ class Graph:
         _check(st, "ipregel_graph_create")
         self.handle = h
         self.last_app = None
+        self._pending = []   # host tensors of values_async copies in flight
 
     def close(self):
         if getattr(self, "handle", None):
-            load().ipregel_graph_destroy(self.handle)
+            load().ipregel_graph_destroy(self.handle)   # waits for the async copies
             self.handle = None
+        self._pending = []
 
     def __del__(self):
         try:
@@ -401,15 +403,31 @@ class Graph:
         return st
 
     def values_async(self, out):
-        """Start copying the last run's values into `out` (a pinned CPU torch tensor of N
-        elements); complete after sync()."""
+        """Start copying the last run's values into `out` (a pinned, contiguous CPU torch tensor
+        of N elements of the last run's value type); complete after sync().  The graph keeps a
+        reference to `out` until sync() or close(), so the copy never writes freed memory."""
+        import torch
+        if self.last_app is None:
+            raise IpregelError(ERR_STATE, "values_async", "no completed run")
+        if self.last_app == APP_PROGRAM:
+            want = _NP_DTYPES[self._last_vt]
+        else:
+            want = np.float64 if self.last_app == APP_PAGERANK else np.uint32
+        esz = np.dtype(want).itemsize
+        if (not isinstance(out, torch.Tensor) or out.device.type != "cpu" or not out.is_pinned()
+                or not out.is_contiguous() or out.numel() != self.n or out.element_size() != esz):
+            raise IpregelError(ERR_INVALID_ARGUMENT, "values_async",
+                               f"out must be a pinned contiguous CPU tensor of {self.n} "
+                               f"{esz}-byte elements")
         _check(load().ipregel_get_values_async(self.handle, out.data_ptr(),
                                                out.numel() * out.element_size()),
                "ipregel_get_values_async")
+        self._pending.append(out)
         return out
 
     def sync(self):
         _check(load().ipregel_graph_sync(self.handle), "ipregel_graph_sync")
+        self._pending.clear()
 
     def values(self, out=None, host: bool = False):
         """Full N-vector of the last run: torch CUDA tensor (default) or numpy (host=True)."""
