@@ -177,10 +177,11 @@ def build_graph_device(cfg_name, rank, world):
     return g, own, bounds
 
 
-def run_step(G, apps, iterations=10):
+def run_step(G, apps, iterations=10, exchange="auto"):
     out = {}
     for app in apps:
-        G.run(app, mode="pull" if app == "pagerank" else "auto", iterations=iterations)
+        G.run(app, mode="pull" if app == "pagerank" else "auto", iterations=iterations,
+              exchange=exchange)
         out[app] = G.stats()
     return out
 
@@ -305,6 +306,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--comm", action="store_true",
                     help="use the NCCL communicator path even on one rank (tests the N>1 path)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "collective"],
+                    help="pull-superstep exchange between ranks: fused epilogue stores over "
+                         "CUDA-IPC-mapped peer replicas, or the collective AllGatherv (auto: "
+                         "fused when every peer maps, else collective, logged)")
     args = ap.parse_args()
     args.apps = [a for a in args.apps.split(",") if a]
 
@@ -323,6 +328,9 @@ def main():
     torch.cuda.set_device(local)
     ipr.device_check(local)
     use_comm = world > 1 or args.comm
+    if world > 1:
+        # NCCL's INFO lines (ranks, rings, NVLS) stay in the log of a multi-GPU run
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if use_comm:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     g, part, bounds = build_graph_device(args.config, rank, world)
@@ -339,7 +347,7 @@ def main():
     # warm-up
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            run_step(G, args.apps)
+            run_step(G, args.apps, exchange=args.exchange)
     torch.cuda.synchronize()
 
     # timed region: K steps, events on the library's stream, barrier + sync on both sides
@@ -352,7 +360,7 @@ def main():
         start.record(stream)
         with torch.cuda.stream(stream):
             for _ in range(args.steps):
-                per_step.append(run_step(G, args.apps))
+                per_step.append(run_step(G, args.apps, exchange=args.exchange))
         stop.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -446,6 +454,7 @@ def main():
                    "layout": "original-id CSC relabelled by out-degree by the library "
                              "(IPREGEL_LAYOUT_DEGREE, at create); results in original ids",
                    "n": n, "e": e, "parallelism": f"1D destination partition x{world}",
+                   "exchange_requested": args.exchange,
                    "l2": "inputs larger than L2 (7.5 GB per adjacency array), no flush",
                    "device": device_info(local),
                    "apps": apps_out},
@@ -501,7 +510,7 @@ def e2e_measure_ranks(part, n, e, args, msgs_per_step, stream, comm, world):
         G = ipr.Graph(hpart, comm=comm, stream=stream)
         lib = ipr.load()
         for app in args.apps:
-            G.run(app, mode="pull" if app == "pagerank" else "auto")
+            G.run(app, mode="pull" if app == "pagerank" else "auto", exchange=args.exchange)
             o = outs[app]
             assert lib.ipregel_get_values(G.handle, o.data_ptr(), o.numel() * o.element_size(),
                                           0) == 0, ipr.last_error()

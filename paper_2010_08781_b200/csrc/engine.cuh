@@ -1018,10 +1018,15 @@ bool use_fused_exchange(ipregel_graph* g, int app, uint32_t flags) {
     if (flags & IPREGEL_RUN_EXCHANGE_COLLECTIVE) return false;
     const bool require = (flags & IPREGEL_RUN_EXCHANGE_FUSED) != 0;
     if (multi_rank(g)) {
+        const bool first = g->parts[0].st[app].peers_state == 0;
         setup_ipc_peers(g, app);
         if (g->parts[0].st[app].peers_state == 1) return true;
         if (require)
             fail(IPREGEL_ERR_UNSUPPORTED, "fused exchange: peer replicas not reachable (CUDA IPC)");
+        if (first && g->comm->world > 1)   // once per app: say which exchange the run takes
+            fprintf(stderr, "[ipregel rank %d] fused exchange unavailable for app %d (peer "
+                    "replicas not mapped by CUDA IPC): using the collective exchange "
+                    "(ncclBroadcast AllGatherv)\n", g->comm->rank, app);
         return false;
     }
     const int np = (int)g->parts.size();
