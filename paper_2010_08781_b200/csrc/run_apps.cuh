@@ -500,7 +500,8 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 if (cc) {
                     CCPullIn a;
                     a.cur = S.val[cur]; a.next = S.val[1 - cur]; a.vbase = p.vb;
-                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
+                    // counters: only its gathered edges (the CSR pass counts the changes)
+                    launch_pull(a, p.plan_csc, p.csc_off, p.csc_idx, nullptr, p.pull_cnt, s, n,
                                 g->gather_policy, g->degree_ordered);
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
