@@ -81,6 +81,8 @@ uint64_t g_hot_bytes = read_hot_bytes();
 // persisting access-policy window over the hot prefix (IPREGEL_PERSIST_BYTES, 0 = off).
 // -1 (default): 64 KiB worth of the hottest vertices for degree-ordered layouts, else off.
 int32_t g_l1_hot = getenv("IPREGEL_L1_HOT") ? atoi(getenv("IPREGEL_L1_HOT")) : -2;
+// Diagnostic: per-kernel events of PageRank supersteps (IPREGEL_TRACE_KERNELS=1, stderr)
+int g_trace_kernels = getenv("IPREGEL_TRACE_KERNELS") ? atoi(getenv("IPREGEL_TRACE_KERNELS")) : 0;
 // Tuning knob: PageRank update split out of the range kernel (IPREGEL_PR_SPLIT=1).
 int g_pr_split = getenv("IPREGEL_PR_SPLIT") ? atoi(getenv("IPREGEL_PR_SPLIT")) : 1;
 // Range kernels: a grid of IPREGEL_PULL_WAVES x the resident CTAs (0: one warp per range),

@@ -236,18 +236,19 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
             c.dmax = d > c.dmax ? d : c.dmax;
         }
         if (write_rank) rank[row] = r;
-        if (broadcast || mass) {
+        if (broadcast) {
             const int32_t deg = out_off[row + 1] - out_off[row];
-            if (mass) {   // the invariant sum r_s = 0.15 + 0.85 sum_{outdeg>0} r_{s-1} (tests)
-                c.m0 += r;
-                if (deg > 0) c.m1 += r;
-            }
-            if (broadcast) {
-                const double x = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
-                contrib_next[vbase + row] = x;
-                peers.store(vbase + row, x);
-            }
+            const double x = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
+            contrib_next[vbase + row] = x;
+            peers.store(vbase + row, x);
         }
+        if (mass) mass_fold(row, r, c);
+    }
+    // the invariant sum r_s = 0.15 + 0.85 sum_{outdeg>0} r_{s-1} (IPREGEL_RUN_PAGERANK_MASS);
+    // out of line: folded into finish it doubled k_pr_finish's instructions
+    __device__ __noinline__ void mass_fold(int32_t row, double r, LaneCounters& c) const {
+        c.m0 += r;
+        if (out_off[row + 1] > out_off[row]) c.m1 += r;
     }
 };
 
@@ -852,10 +853,21 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
 #define IPREGEL_PR_FINISH_ROWS 4
 #endif
 constexpr int kPrFinishRows = IPREGEL_PR_FINISH_ROWS;
+// kMode: 0 general (runtime flags: to-convergence / mass-check runs), 1 broadcast only
+// (supersteps 1 .. k-1 of a fixed-k run), 2 rank only (superstep k).  The fixed-k variants fix
+// the flags at compile time: with them at run time the compiler versioned the row loop and the
+// kernel ran 2.3x the instructions (0.31 vs 0.16 ms at cfg4).
+template <int kMode>
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
     __shared__ unsigned long long s_cnt[5];
-    if (counters && threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
+    if (kMode == 0 && counters && threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
+    if constexpr (kMode != 0) {
+        op.broadcast = kMode == 1;
+        op.write_rank = kMode == 2;
+        op.track = 0;
+        op.mass = nullptr;
+    }
     LaneCounters c{0u, 0u, 0u, 0ull};
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * kPrFinishRows + threadIdx.x;
     double sum[kPrFinishRows];
@@ -869,11 +881,13 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
         const int64_t row = base + (int64_t)j * blockDim.x;
         if (row < rows) op.finish((int32_t)row, sum[j], c);
     }
-    if (counters) {   // to-convergence runs only (grid-uniform)
-        __syncthreads();
-        flush_counters(c, s_cnt, counters);
+    if constexpr (kMode == 0) {
+        if (counters) {   // to-convergence runs only (grid-uniform)
+            __syncthreads();
+            flush_counters(c, s_cnt, counters);
+        }
+        if (op.mass) flush_mass(c, op.mass);
     }
-    if (op.mass) flush_mass(c, op.mass);
 }
 
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is

@@ -7,6 +7,21 @@ namespace {
 // =============================================================================================
 // PageRank (Fig. 8)
 // =============================================================================================
+// IPREGEL_TRACE_KERNELS=1: per gather superstep of a PageRank pull run, the time of the range
+// kernel + fixup, of k_pr_finish, and what the superstep adds around them (events on the run
+// stream, the same clocks), printed to stderr -- the attribution of a superstep's time.
+void trace_pr_kernels(ipregel_graph* g, uint32_t k) {
+    for (uint32_t s = 1; s < g->steps.size() && s <= k; ++s) {
+        float a = 0, b = 0, t = 0;
+        CU(cudaEventElapsedTime(&a, ev(g, 4 * s + 1), ev(g, 4 * (k + 1) + s)));
+        CU(cudaEventElapsedTime(&b, ev(g, 4 * (k + 1) + s), ev(g, 4 * s + 2)));
+        CU(cudaEventElapsedTime(&t, ev(g, 4 * s + 0), ev(g, 4 * s + 3)));
+        fprintf(stderr, "[ipregel pagerank] superstep %u: range kernel + fixup %.4f ms, "
+                "k_pr_finish %.4f ms, superstep %.4f ms (other %.4f ms)\n", s, a, b, t,
+                t - a - b);
+    }
+}
+
 // Mass check: the per-superstep device sums into the step records (summed over ranks).
 void read_mass(ipregel_graph* g) {
     cudaStream_t s = g->stream;
@@ -71,11 +86,12 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->last_exchange = G.exchange;
         finalize_times(g);
         if (mass) read_mass(g);
+        if (g_trace_kernels && g_pr_split && !push) trace_pr_kernels(g, k);
         return G.status;
     }
     const unsigned long long launches0 = g_launches.load(std::memory_order_relaxed);
     if (graphable) {
-        for (uint32_t i = 0; i <= 4 * (k + 1); ++i) ev(g, i);   // events exist before capture
+        for (uint32_t i = 0; i <= 5 * (k + 1); ++i) ev(g, i);   // events exist before capture
         // capture on a private stream (the caller's may be the legacy default stream, which
         // cannot be captured); the graph is then launched on the caller's stream
         if (!g->capture_stream)
@@ -160,8 +176,14 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                     sop.vbase = p.vb;
                     launch_pull(sop, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
                                 g->gather_policy, g->degree_ordered);
-                    k_pr_finish<<<grid_for(ceil_div(p.rows, kPrFinishRows), 256), 256, 0, s>>>(
-                        op, p.rows, track ? p.pull_cnt : nullptr);
+                    if (g_trace_kernels) T.rec(4 * (k + 1) + step);   // range kernel + fixup done
+                    const unsigned fg = grid_for(ceil_div(p.rows, kPrFinishRows), 256);
+                    if (track || mass || (broadcast && write_rank))
+                        k_pr_finish<0><<<fg, 256, 0, s>>>(op, p.rows, track ? p.pull_cnt : nullptr);
+                    else if (broadcast)
+                        k_pr_finish<1><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
+                    else
+                        k_pr_finish<2><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
                     LAUNCH_CHECK();
                 } else {
                     launch_pull(op, p.plan_csc, p.csc_off, p.csc_idx, nullptr,
@@ -231,6 +253,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     }
     finalize_times(g);
     if (mass) read_mass(g);
+    if (g_trace_kernels && g_pr_split && !push) trace_pr_kernels(g, k);
     return status;
 }
 
