@@ -194,6 +194,7 @@ struct PeerSlots {
     T* p[kMaxPeers];
     int n;
     __device__ __forceinline__ void store(int64_t i, T v) const {
+        if (n == 0) return;   // one partition: no other replica (the common case, one test)
 #pragma unroll
         for (int k = 0; k < kMaxPeers; ++k)
             if (k < n) p[k][i] = v;
@@ -229,6 +230,13 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     __device__ bool absorbed(int32_t) const { return false; }
     __device__ static T message(T g, uint32_t) { return g; }
     __device__ void finish(int32_t row, T sum, LaneCounters& c) const {
+        const int32_t deg = (broadcast || mass) ? out_off[row + 1] - out_off[row] : 0;
+        finish_deg(row, sum, deg, c);
+    }
+    // The update with the row's out-degree given (k_pr_finish loads the degrees of all its rows
+    // up front, so those loads overlap instead of serialising per row).
+    __device__ __forceinline__ void finish_deg(int32_t row, T sum, int32_t deg,
+                                               LaneCounters& c) const {
         const double r = __dadd_rn(ratio, __dmul_rn(0.85, sum));
         if (track) {   // max aggregator of the per-vertex change (reading R27)
             const unsigned long long d =
@@ -237,18 +245,14 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
         }
         if (write_rank) rank[row] = r;
         if (broadcast) {
-            const int32_t deg = out_off[row + 1] - out_off[row];
             const double x = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
             contrib_next[vbase + row] = x;
             peers.store(vbase + row, x);
         }
-        if (mass) mass_fold(row, r, c);
-    }
-    // the invariant sum r_s = 0.15 + 0.85 sum_{outdeg>0} r_{s-1} (IPREGEL_RUN_PAGERANK_MASS);
-    // out of line: folded into finish it doubled k_pr_finish's instructions
-    __device__ __noinline__ void mass_fold(int32_t row, double r, LaneCounters& c) const {
-        c.m0 += r;
-        if (out_off[row + 1] > out_off[row]) c.m1 += r;
+        if (mass) {   // the invariant sum r_s = 0.15 + 0.85 sum_{outdeg>0} r_{s-1} (tests)
+            c.m0 += r;
+            if (deg > 0) c.m1 += r;
+        }
     }
 };
 
@@ -870,16 +874,19 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
     }
     LaneCounters c{0u, 0u, 0u, 0ull};
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * kPrFinishRows + threadIdx.x;
+    const bool need_deg = op.broadcast || op.mass;
     double sum[kPrFinishRows];
+    int32_t deg[kPrFinishRows];
 #pragma unroll
     for (int j = 0; j < kPrFinishRows; ++j) {
         const int64_t row = base + (int64_t)j * blockDim.x;
         sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+        deg[j] = row < rows && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
     }
 #pragma unroll
     for (int j = 0; j < kPrFinishRows; ++j) {
         const int64_t row = base + (int64_t)j * blockDim.x;
-        if (row < rows) op.finish((int32_t)row, sum[j], c);
+        if (row < rows) op.finish_deg((int32_t)row, sum[j], deg[j], c);
     }
     if constexpr (kMode == 0) {
         if (counters) {   // to-convergence runs only (grid-uniform)
