@@ -159,7 +159,8 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         int32_t* kk0 = row;   // E int32 each
         int32_t* kk1 = spare;
         CU(cudaMemcpyAsync(kk0, idx, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, k0);
+        if (w) k_transpose_pack_w<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, w, k0);
+        else k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, k0);
         LAUNCH_CHECK();
         cub::DoubleBuffer<int32_t> tkeys(kk0, kk1);
         cub::DoubleBuffer<unsigned long long> tvals(k0, k1);
@@ -167,8 +168,8 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys, tvals, E, 0, bits, s));
         void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
         CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, s));
-        k_transpose_unpack<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
-            tvals.Current(), E, w, ridx, rw, nullptr);
+        k_unpack_w<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
+            tvals.Current(), E, ridx, rw);
         LAUNCH_CHECK();
         CU(cudaMemsetAsync(st, 0, n * sizeof(int32_t), s));
         k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(

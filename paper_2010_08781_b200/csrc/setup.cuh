@@ -214,6 +214,28 @@ __global__ void k_transpose_pack(const int32_t* __restrict__ off, int64_t rows, 
         vals[e] = v | ((unsigned long long)(uint32_t)e << 32);
 }
 
+// As k_transpose_pack with the edge's weight in the high half instead of its position (the
+// relabel's CSR: the weights are already in place, so no gather after the sort)
+__global__ void k_transpose_pack_w(const int32_t* __restrict__ off, int64_t rows, int64_t vbase,
+                                   const uint32_t* __restrict__ w,
+                                   unsigned long long* __restrict__ vals) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const unsigned long long v = (unsigned long long)(uint32_t)(vbase + r);
+    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32)
+        vals[e] = v | ((unsigned long long)w[e] << 32);
+}
+__global__ void k_unpack_w(const unsigned long long* __restrict__ vals, int64_t edges,
+                           int32_t* __restrict__ out_idx, uint32_t* __restrict__ out_w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = vals[i];
+        out_idx[i] = (int32_t)(uint32_t)x;
+        if (out_w) out_w[i] = (uint32_t)(x >> 32);
+    }
+}
+
 // Run boundaries of the sorted sources: start[k] = first position of source k, end[k] = one past
 // its last (both 0 for sources without edges); then count[k] = end[k] - start[k] in place.
 __global__ void k_run_bounds(const int32_t* __restrict__ keys, int64_t edges,
