@@ -168,6 +168,48 @@ __global__ void __launch_bounds__(256) k_v1(const int* __restrict__ idx, int64_t
     out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// v5..: indices kD chunks ahead in a register ring, gathers one chunk ahead
+template <int kBlk, int kD>
+__global__ void __launch_bounds__(256) k_vd(const int* __restrict__ idx, int64_t nchunks,
+                                            const double* __restrict__ vals, double* out,
+                                            int* ctr) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol = pol_first();
+    double acc = 0;
+    for (;;) {
+        int q = lane == 0 ? atomicAdd(ctr, 1) : 0;
+        q = __shfl_sync(0xffffffffu, q, 0);
+        const int64_t c0 = (int64_t)q * kBlk;
+        if (c0 >= nchunks) break;
+        const int64_t c1 = c0 + kBlk < nchunks ? c0 + kBlk : nchunks;
+        int ring[kD][4];
+#pragma unroll
+        for (int d = 0; d < kD; ++d)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                ring[d][k] = c0 + d < c1 ? ld_idx(idx + (c0 + d) * kChunk + 32 * k + lane, pol) : 0;
+        double g[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g[k] = ld_val(vals + ring[0][k]);
+        for (int64_t c = c0; c < c1; ++c) {
+            double gn[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gn[k] = c + 1 < c1 ? ld_val(vals + ring[1][k]) : 0.0;
+#pragma unroll
+            for (int d = 0; d + 1 < kD; ++d)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ring[d][k] = ring[d + 1][k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                ring[kD - 1][k] = c + kD < c1 ? ld_idx(idx + (c + kD) * kChunk + 32 * k + lane, pol) : 0;
+            acc += (g[0] + g[1]) + (g[2] + g[3]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) g[k] = gn[k];
+        }
+    }
+    out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 template <class F>
 static float timeit(F launch, int* ctr, int reps) {
     cudaEvent_t a, b;
@@ -206,6 +248,14 @@ extern "C" float tma_lab(int variant, const int* idx, int64_t e, const double* v
             return timeit([&] { k_v0<2><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
         case 4:
             return timeit([&] { k_v0<256><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
+        case 5:
+            return timeit([&] { k_vd<64, 2><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
+        case 6:
+            return timeit([&] { k_vd<64, 3><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
+        case 7:
+            return timeit([&] { k_vd<64, 4><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
+        case 8:
+            return timeit([&] { k_vd<64, 6><<<grid, 256, pad>>>(idx, nchunks, vals, out, ctr); }, ctr, reps);
         default:
             return -2.0f;
     }

@@ -30,7 +30,7 @@ old_of_new, new_of_old = degree_order_device(cfg.scale, cfg.edgefactor, cfg.seed
 off, idx, _ = rmat_adjacency_device(cfg.scale, cfg.edgefactor, cfg.seed, True, False, new_of_old)
 del old_of_new, new_of_old, off
 n = cfg.n
-cold = torch.masked_select(idx, idx >= a.H)
+cold = torch.masked_select(idx, idx >= a.H) if a.H > 0 else idx
 del idx
 torch.cuda.synchronize()
 e = cold.numel()
@@ -39,8 +39,10 @@ out = torch.zeros(148 * 16 * 256, dtype=torch.float64, device="cuda")
 ctr = torch.zeros(1, dtype=torch.int32, device="cuda")
 print(f"cold edges {e}", flush=True)
 names = {0: "regs pipeline, warp blocks of 64 chunks", 1: "blocks of 16 chunks",
-         2: "blocks of 4 chunks", 3: "blocks of 2 chunks", 4: "blocks of 256 chunks"}
-for v in range(5):
+         2: "blocks of 4 chunks", 3: "blocks of 2 chunks", 4: "blocks of 256 chunks",
+         5: "ring: idx 2 ahead", 6: "ring: idx 3 ahead", 7: "ring: idx 4 ahead",
+         8: "ring: idx 6 ahead"}
+for v in (0, 5, 6, 7, 8):
     for c in (2, 3, 4):
         ms = lib.tma_lab(v, cold.data_ptr(), e, vals.data_ptr(), out.data_ptr(), ctr.data_ptr(), c, 5)
         print(f"v{v} {names[v]:36s} {c} CTAs/SM ({8 * c} warps): {ms:.3f} ms", flush=True)
