@@ -388,7 +388,6 @@ void destroy_graph(ipregel_graph* g) {
             S.mem.release();
         }
         p.graph_mem.release();
-        p.bins.mem.release();
         for (cudaEvent_t e : {p.up_idx, p.up_w, p.up_all})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : p.up_wc) cudaEventDestroy(e);

@@ -295,21 +295,6 @@ struct Partition {
     cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
     std::vector<int64_t> wc_bounds;
     AppState st[4];
-    // PageRank short-row bin (built on the first pull run): rows of in-degree
-    // <= t as a sliced ELL (k_pr_short), the other rows' in-edges in the "main" CSC over the same
-    // rows (short rows empty there) with its own range plan on its own global grid
-    struct {
-        int state = 0;              // 0 not built, 1 built
-        int32_t t = 0;
-        int64_t main_edges = 0, main_ebase = 0, short_edges = 0, slices = 0, columns = 0;
-        int32_t* main_off = nullptr;
-        int32_t* main_idx = nullptr;
-        TilePlan plan_main;
-        int2* meta = nullptr;
-        int32_t* sidx = nullptr;
-        int32_t* perm = nullptr;    // [slices * 32]: the row in each slot, -1 past the end
-        DeviceBuffers mem;
-    } bins;
     PullCounters* pull_cnt = nullptr;         // device
     FrontierCounters* front_cnt = nullptr;    // device
     unsigned long long* host_cnt = nullptr;   // pinned [16]
@@ -839,123 +824,6 @@ void ensure_push_view(ipregel_graph* g, Partition& p) {
     p.push_sssp = PushAdj{o1, i1, w1, nullptr, nullptr, nullptr, 0, n};
     p.push_cc = PushAdj{o1, i1, w1, o2, i2, w2, 0, n};
     p.push_view_ready = true;
-}
-
-// ---- PageRank short-row bin ------------------------------------------------
-// IPREGEL_SHORT_DEGREE: rows with at most this many in-edges go to the thread-per-row sliced ELL
-// (0: off -- one range kernel over the whole CSC + k_pr_finish)
-int32_t g_short_degree = getenv("IPREGEL_SHORT_DEGREE") ? atoi(getenv("IPREGEL_SHORT_DEGREE")) : 64;
-
-// Builds every partition's bin (collective across ranks: the main CSC's global edge bases are
-// all-gathered).  Returns false when the bin is off.
-bool ensure_short_bins(ipregel_graph* g) {
-    if (g_short_degree <= 0 || g->parts.empty()) return false;
-    Partition& p0 = g->parts[0];
-    if (p0.bins.state != 0) return true;
-    cudaStream_t s = g->stream;
-    const int32_t t = g_short_degree;
-    for (auto& p : g->parts) {
-        auto& B = p.bins;
-        B.t = t;
-        DeviceBuffers tmp;
-        int32_t* h = static_cast<int32_t*>(g->pinned.get(2 * sizeof(int32_t), 1));
-        // the main CSC: long rows keep their in-edges
-        B.main_off = B.mem.alloc<int32_t>(p.rows + 1, s);
-        k_long_degree<<<grid_for(p.rows + 1, 256), 256, 0, s>>>(p.csc_off, p.rows, t, B.main_off);
-        LAUNCH_CHECK();
-        exscan_i32(B.main_off, p.rows + 1, tmp, s);
-        kernel_copy(h, B.main_off + p.rows, sizeof(int32_t), s);
-        CU(cudaStreamSynchronize(s));
-        B.main_edges = h[0];
-        B.short_edges = p.csc_edges - B.main_edges;
-        B.main_idx = B.mem.alloc<int32_t>(std::max<int64_t>(B.main_edges, 1), s);
-        if (p.rows)
-            k_copy_long_rows<<<sm_grid(16), 256, 0, s>>>(p.csc_off, p.csc_idx, p.rows, t,
-                                                         B.main_off, B.main_idx);
-        LAUNCH_CHECK();
-        // the sliced ELL of the short rows, rows sorted by degree inside windows of 256
-        const int64_t windows = ceil_div(p.rows, kShortWindow);
-        B.slices = windows * (kShortWindow / 32);
-        B.perm = B.mem.alloc<int32_t>(std::max<int64_t>(windows * kShortWindow, 1), s);
-        B.meta = B.mem.alloc<int2>(std::max<int64_t>(B.slices, 1), s);
-        int32_t* col = tmp.alloc<int32_t>(B.slices + 1, s);
-        if (windows) {
-            k_short_sigma<<<(unsigned)windows, kShortWindow, 0, s>>>(p.csc_off, p.rows, t, B.perm);
-            k_short_width<<<grid_for(B.slices * 32, 256), 256, 0, s>>>(p.csc_off, B.perm, t,
-                                                                      B.slices, col);
-        }
-        LAUNCH_CHECK();
-        exscan_i32(col, B.slices + 1, tmp, s);
-        kernel_copy(h, col + B.slices, sizeof(int32_t), s);
-        CU(cudaStreamSynchronize(s));
-        B.columns = h[0];
-        B.sidx = B.mem.alloc<int32_t>(std::max<int64_t>(32 * B.columns, 1), s);
-        if (B.slices)
-            k_short_fill<<<grid_for(B.slices * 32, 256), 256, 0, s>>>(
-                p.csc_off, p.csc_idx, B.perm, t, B.slices, col, B.meta, B.sidx);
-        LAUNCH_CHECK();
-        CU(cudaStreamSynchronize(s));
-        tmp.release();
-    }
-    // global edge bases of the main CSC: partitions in order, then ranks in order
-    int64_t mb = 0;
-    for (auto& p : g->parts) {
-        p.bins.main_ebase = mb;
-        mb += p.bins.main_edges;
-    }
-    if (multi_rank(g)) {
-        DeviceBuffers tmp;
-        const int W = g->comm->world;
-        int64_t* d = tmp.alloc<int64_t>(1 + W, s);
-        CU(cudaMemcpyAsync(d, &p0.bins.main_edges, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        NC(ncclAllGather(d, d + 1, 1, ncclInt64, g->comm->nccl, s));
-        std::vector<int64_t> all(W);
-        CU(cudaMemcpyAsync(all.data(), d + 1, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        tmp.release();
-        p0.bins.main_ebase = 0;
-        for (int r = 0; r < g->comm->rank; ++r) p0.bins.main_ebase += all[r];
-    }
-    for (auto& p : g->parts) {
-        auto& B = p.bins;
-        build_plan(B.plan_main, B.main_off, B.main_idx, nullptr, p.rows, B.main_edges, p.vb,
-                   B.main_ebase, B.mem, s, g->pinned);
-        B.state = 1;
-        if (getenv("IPREGEL_TRACE_BINS"))
-            fprintf(stderr, "[ipregel bins] rows %lld: main CSC %lld edges; short rows (<= %d "
-                    "in-edges) %lld edges in %lld sliced-ELL entries (%.2fx)\n",
-                    (long long)p.rows, (long long)B.main_edges, t, (long long)B.short_edges,
-                    (long long)(32 * B.columns),
-                    B.short_edges ? 32.0 * (double)B.columns / (double)B.short_edges : 0.0);
-    }
-    CU(cudaStreamSynchronize(s));
-    return true;
-}
-
-void launch_pr_short(const PageRankPull& op, const Partition& p, int kmode, PullCounters* cnt,
-                     int policy, bool degree_ordered, int64_t n_global, cudaStream_t s) {
-    const TilePlan& P = p.bins.plan_main;
-    // the range kernels' gather caching, from the same helper
-    RangeArgs A = range_args(P, p.bins.main_off, p.bins.main_idx, nullptr, nullptr, s,
-                             op.contrib_cur, n_global, sizeof(double), policy, degree_ordered);
-    ShortSell S;
-    S.slices = p.bins.slices;
-    S.meta = p.bins.meta;
-    S.sidx = p.bins.sidx;
-    S.perm = p.bins.perm;
-    S.rows = (int32_t)p.rows;
-    S.gather_policy = A.gather_policy;
-    S.gbase = A.gbase;
-    S.ghot = A.ghot;
-    S.gtotal = A.gtotal;
-    S.l1hot = A.l1hot;
-    if (S.slices == 0) return;
-    const unsigned grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(S.slices, 8), (int64_t)sm_grid(8)));
-    if (kmode == 1) k_pr_short<1><<<grid, 256, 0, s>>>(op, S, nullptr);
-    else if (kmode == 2) k_pr_short<2><<<grid, 256, 0, s>>>(op, S, nullptr);
-    else k_pr_short<0><<<grid, 256, 0, s>>>(op, S, cnt);
-    LAUNCH_CHECK();
 }
 
 // ---- frontier machinery ------------------------------------------------------------------

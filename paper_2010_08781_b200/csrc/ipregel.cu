@@ -312,7 +312,7 @@ ipregel_status ipregel_memory_footprint(ipregel_graph* g, uint64_t* graph_bytes,
     if (!g) fail(IPREGEL_ERR_INVALID_ARGUMENT, "graph is NULL");
     uint64_t gb = 0, sb = 0;
     for (auto& p : g->parts) {
-        gb += p.graph_mem.bytes + p.bins.mem.bytes;
+        gb += p.graph_mem.bytes;
         for (auto& S : p.st) sb += S.mem.bytes;
     }
     if (graph_bytes) *graph_bytes = gb;

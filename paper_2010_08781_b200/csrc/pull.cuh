@@ -897,72 +897,6 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
     }
 }
 
-// ---- PageRank short rows: degree-binned, one thread per row ---------------
-// Rows with at most `short_degree` in-edges are taken out of the merge-path CSC: their in-edges
-// form a sliced ELLPACK (SELL-32-sigma: inside windows of 256 rows the rows are sorted by
-// degree, slice s = 32 of them: width(s) columns of 32 source ids, column-major, -1 past a
-// row's end), one thread per row sums its column walk sequentially (the order depends on the
-// row alone: bit-identical for any partitioning).  The range kernel runs
-// over the other rows and leaves every row's sum in its next-outbox slot (0 for short rows);
-// this kernel then runs Fig. 8's update of EVERY row on long sum + short sum -- one of the two
-// is exactly 0, so each row's sum is its own fold -- replacing k_pr_finish.  It targets the
-// range kernel's slow path: at cfg4, rows of in-degree <= 64 hold 15 % of the edges and 18 % of
-// the superstep (profiles/r02/short_rows_lab.log).
-struct ShortSell {
-    int64_t slices;
-    const int2* meta;          // [slices]: (first column, width) -- columns of 32 entries
-    const int32_t* sidx;       // [32 * columns]: global source ids, -1 = padding
-    const int32_t* perm;       // [32 * slices]: the row in each slot (-1: none)
-    int32_t rows;
-    int gather_policy;         // the range kernels' gather caching (RangeArgs)
-    const void* gbase;
-    uint32_t ghot, gtotal;
-    int32_t l1hot;
-};
-template <int kMode>   // as k_pr_finish: 0 runtime flags, 1 broadcast only, 2 rank only
-__global__ void __launch_bounds__(256) k_pr_short(PageRankPull op, ShortSell S,
-                                                  PullCounters* counters) {
-    __shared__ unsigned long long s_cnt[5];
-    if (kMode == 0 && counters && threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
-    if constexpr (kMode != 0) {
-        op.broadcast = kMode == 1;
-        op.write_rank = kMode == 2;
-        op.track = 0;
-        op.mass = nullptr;
-    }
-    const int lane = threadIdx.x & 31;
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_g = policy_for(S.gather_policy, S.gbase, S.ghot, S.gtotal);
-    const bool need_deg = op.broadcast || op.mass;
-    LaneCounters c{0u, 0u, 0u, 0ull};
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t sl = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sl < S.slices;
-         sl += nw) {
-        const int2 m = S.meta[sl];
-        const int32_t row = S.perm[sl * 32 + lane];
-        const bool live = row >= 0;
-        // the row-level loads first, so they overlap the gathers
-        const double lsum = live ? op.contrib_next[op.vbase + row] : 0.0;
-        const int32_t deg = live && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
-        const int32_t* p = S.sidx + (int64_t)m.x * 32 + lane;
-        const double* cv = op.contrib_cur;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int32_t j = 0; j < m.y; ++j) {
-            const int32_t u = ld_stream(p + 32 * j, pol_s);
-            if (u >= 0) acc = __dadd_rn(acc, ld_gather(cv + u, pol_g));   // in edge order
-        }
-        if (live) op.finish_deg(row, __dadd_rn(lsum, acc), deg, c);
-    }
-    if constexpr (kMode == 0) {
-        if (counters) {   // to-convergence runs only (grid-uniform)
-            __syncthreads();
-            flush_counters(c, s_cnt, counters);
-        }
-        if (op.mass) flush_mass(c, op.mass);
-    }
-}
-
 // Rows cut by range boundaries: boundaries a..b (1 <= a <= b) carry row r; its value is
 // carry[a-1] (+) carry[a] (+) ... (+) carry[b-1] (+) head[b], folded in a fixed order that
 // depends on the span only (ranges sit on the global grid, so on every partitioning alike):

@@ -59,8 +59,6 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->pr_mass_cap = k + 1;
     }
     auto mass_slot = [&](uint32_t step) { return mass ? g->pr_mass + 2 * step : nullptr; };
-    // pull supersteps over the short-row bin (built on the first pull run)
-    const bool bins = P.mode != IPREGEL_MODE_PUSH && g_pr_split && ensure_short_bins(g);
     // PageRank broadcasters: vertices with out-degree > 0, summed over partitions / ranks
     int64_t nondangling = 0;
     for (auto& p : g->parts) nondangling += p.nondangling;
@@ -171,21 +169,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.write_rank = write_rank;
                 op.track = track;
                 op.mass = mass_slot(step);
-                const int kmode = (track || mass || (broadcast && write_rank)) ? 0
-                                  : broadcast ? 1 : 2;   // k_pr_finish / k_pr_short variants
-                if (bins) {
-                    // long rows through the range kernel (sums in the next-outbox slots, 0 for
-                    // short rows), then short rows + Fig. 8's update of every row
-                    PageRankSum sop;
-                    sop.contrib_cur = op.contrib_cur;
-                    sop.sum_out = op.contrib_next;
-                    sop.vbase = p.vb;
-                    launch_pull(sop, p.bins.plan_main, p.bins.main_off, p.bins.main_idx, nullptr,
-                                nullptr, s, n, g->gather_policy, g->degree_ordered);
-                    if (g_trace_kernels) T.rec(4 * (k + 1) + step);
-                    launch_pr_short(op, p, kmode, track ? p.pull_cnt : nullptr, g->gather_policy,
-                                    g->degree_ordered, n, s);
-                } else if (g_pr_split) {
+                if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
                     sop.sum_out = op.contrib_next;
@@ -194,9 +178,9 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                                 g->gather_policy, g->degree_ordered);
                     if (g_trace_kernels) T.rec(4 * (k + 1) + step);   // range kernel + fixup done
                     const unsigned fg = grid_for(ceil_div(p.rows, kPrFinishRows), 256);
-                    if (kmode == 0)
+                    if (track || mass || (broadcast && write_rank))
                         k_pr_finish<0><<<fg, 256, 0, s>>>(op, p.rows, track ? p.pull_cnt : nullptr);
-                    else if (kmode == 1)
+                    else if (broadcast)
                         k_pr_finish<1><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
                     else
                         k_pr_finish<2><<<fg, 256, 0, s>>>(op, p.rows, nullptr);

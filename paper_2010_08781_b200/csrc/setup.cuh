@@ -1,8 +1,6 @@
 // paper_2010_08781_b200/csrc/setup.cuh -- superstep 0, validation, push-view construction and
 // small utility kernels.
 #pragma once
-#include <cub/block/block_radix_sort.cuh>
-
 #include "common.cuh"
 #include "pull.cuh"
 
@@ -27,74 +25,6 @@ __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t row
         }
     }
     if (mass) flush_mass(c, mass);   // grid-uniform; whole warps (blocks of 256)
-}
-
-// ---- PageRank short-row bin (built on the first pull run) ----------------------------------
-// ldeg[r] = in-degree of row r if it stays in the merge-path CSC (> t), else 0; ldeg[rows] = 0
-__global__ void k_long_degree(const int32_t* __restrict__ off, int64_t rows, int32_t t,
-                              int32_t* __restrict__ ldeg) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r > rows) return;
-    const int32_t d = r < rows ? off[r + 1] - off[r] : 0;
-    ldeg[r] = d > t ? d : 0;
-}
-// the long rows' in-edges into the main CSC, one warp per row (grid-stride over rows)
-__global__ void k_copy_long_rows(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                                 int64_t rows, int32_t t, const int32_t* __restrict__ main_off,
-                                 int32_t* __restrict__ main_idx) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-        const int32_t b = off[r], d = off[r + 1] - b;
-        if (d <= t) continue;
-        const int32_t o = main_off[r];
-        for (int32_t j = lane; j < d; j += 32) main_idx[o + j] = idx[b + j];
-    }
-}
-// Row order of the sliced ELL: inside every window of kShortWindow consecutive rows, the rows by
-// decreasing short in-degree (stable, a block radix sort), so each slice of 32 holds rows of
-// similar degree and pads little; perm[slot] = row, -1 past the last row.
-constexpr int kShortWindow = 256;
-__global__ void __launch_bounds__(kShortWindow) k_short_sigma(const int32_t* __restrict__ off,
-                                                             int64_t rows, int32_t t,
-                                                             int32_t* __restrict__ perm) {
-    using Sort = cub::BlockRadixSort<uint32_t, kShortWindow, 1, int32_t>;
-    __shared__ typename Sort::TempStorage tmp;
-    const int64_t r = (int64_t)blockIdx.x * kShortWindow + threadIdx.x;
-    int32_t d = r < rows ? off[r + 1] - off[r] : -1;
-    if (d > t) d = 0;
-    uint32_t key[1] = {(uint32_t)(d + 1)};   // rows past the end (d = -1) sort last
-    int32_t val[1] = {r < rows ? (int32_t)r : -1};
-    Sort(tmp).SortDescending(key, val);
-    perm[(int64_t)blockIdx.x * kShortWindow + threadIdx.x] = val[0];
-}
-// width of each slice of 32 slots: its largest short-row in-degree (thread per slot, warp max)
-__global__ void k_short_width(const int32_t* __restrict__ off, const int32_t* __restrict__ perm,
-                              int32_t t, int64_t slices, int32_t* __restrict__ col) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int32_t r = q < slices * 32 ? perm[q] : -1;
-    int32_t d = r >= 0 ? off[r + 1] - off[r] : 0;
-    if (d > t) d = 0;
-    const int32_t w = (int32_t)__reduce_max_sync(0xFFFFFFFFu, (uint32_t)d);
-    if ((threadIdx.x & 31) == 0 && q / 32 < slices) col[q / 32] = w;
-}
-// column-major fill: entry [j][lane] = j-th in-edge source of the short row in slot
-// 32 s + lane, else -1
-__global__ void k_short_fill(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
-                             const int32_t* __restrict__ perm, int32_t t, int64_t slices,
-                             const int32_t* __restrict__ col, int2* __restrict__ meta,
-                             int32_t* __restrict__ sidx) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t sl = q / 32;
-    if (sl >= slices) return;
-    const int lane = (int)(q & 31);
-    const int32_t c0 = col[sl], w = col[sl + 1] - c0;
-    if (lane == 0) meta[sl] = make_int2(c0, w);
-    const int32_t r = perm[q];
-    const int32_t b = r >= 0 ? off[r] : 0;
-    int32_t d = r >= 0 ? off[r + 1] - b : 0;
-    if (d > t) d = 0;
-    for (int32_t j = 0; j < w; ++j) sidx[((int64_t)c0 + j) * 32 + lane] = j < d ? idx[b + j] : -1;
 }
 
 // User programs: broadcaster bitmap of the owned rows from the per-vertex flag bytes (bit 0),
