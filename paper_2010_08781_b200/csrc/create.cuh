@@ -101,6 +101,12 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     int32_t* new_of_old = tmp.alloc<int32_t>(n, s);
     k_invert_perm<<<grid_for(n, 256), 256, 0, s>>>(old_of_new, n, new_of_old);
     LAUNCH_CHECK();
+    // the out-adjacency's offsets come from the sorted degrees already: PageRank's pull (which
+    // needs only out-degrees) can run before the CSR's indices exist (step 4)
+    int32_t* roff = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+    k_degree_from_keys<<<grid_for(n, 256), 256, 0, s>>>(deg2, n, roff);
+    LAUNCH_CHECK();
+    exscan_i32(roff, n + 1, tmp, s);
     g_ctrace.mark("relabel order", s);
     // 2. relabelled edges sorted by (new destination, new source), weights carried along
     int bits = 1;
@@ -151,40 +157,48 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         LAUNCH_CHECK();
         exscan_i32(off, n + 1, tmp, s);
         g_ctrace.mark("relabel csc", s);
-        // 4. the out-adjacency: the same edges by (new source), a stable sort of the CSC order
-        //    (each CSR row lists its destinations ascending), in the buffers of step 2
-        int32_t* roff = p.graph_mem.alloc<int32_t>(n + 1, s, true);
+        // 4. the out-adjacency's indices: the same edges by (new source), a stable sort of the
+        //    CSC order (each CSR row lists its destinations ascending), in the buffers of step 2,
+        //    on the aux stream -- create returns without waiting; whatever reads the CSR's
+        //    indices first waits for p.csr_done (wait_csr).  Its offsets are roff already.
         int32_t* ridx = p.graph_mem.alloc<int32_t>(E, s);
         uint32_t* rw = w ? p.graph_mem.alloc<uint32_t>(E, s) : nullptr;
+        size_t tb2 = 0;
+        {
+            cub::DoubleBuffer<int32_t> tk(row, spare);
+            cub::DoubleBuffer<unsigned long long> tv(k0, k1);
+            CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tk, tv, E, 0, bits, s));
+        }
+        void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
+        if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+        cudaStream_t a = g->aux_stream;
+        if (!p.csr_done) CU(cudaEventCreateWithFlags(&p.csr_done, cudaEventDisableTiming));
+        CU(cudaEventRecord(p.csr_done, s));   // the CSC and every temporary are in place
+        CU(cudaStreamWaitEvent(a, p.csr_done, 0));
         int32_t* kk0 = row;   // E int32 each
         int32_t* kk1 = spare;
-        CU(cudaMemcpyAsync(kk0, idx, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        if (w) k_transpose_pack_w<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, w, k0);
-        else k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, s>>>(off, n, 0, k0);
+        CU(cudaMemcpyAsync(kk0, idx, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, a));
+        if (w) k_transpose_pack_w<<<grid_for(n * 32, 256), 256, 0, a>>>(off, n, 0, w, k0);
+        else k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, a>>>(off, n, 0, k0);
         LAUNCH_CHECK();
         cub::DoubleBuffer<int32_t> tkeys(kk0, kk1);
         cub::DoubleBuffer<unsigned long long> tvals(k0, k1);
-        size_t tb2 = 0;
-        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys, tvals, E, 0, bits, s));
-        void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
-        CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, s));
-        k_unpack_w<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
+        CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, a));
+        k_unpack_w<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, a>>>(
             tvals.Current(), E, ridx, rw);
         LAUNCH_CHECK();
-        CU(cudaMemsetAsync(st, 0, n * sizeof(int32_t), s));
-        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
-            tkeys.Current(), E, st, roff);
-        k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, roff);
-        LAUNCH_CHECK();
-        exscan_i32(roff, n + 1, tmp, s);
-        p.csr_off = roff;
+        CU(cudaEventRecord(p.csr_done, a));
+        g_ctrace.mark("relabel csr (aux)", a);
+        p.csr_pending = true;
+        // the temporaries are freed on the aux stream, after the CSR sort
+        for (auto& b : tmp.blocks) b.s = a;
         p.csr_idx = ridx;
         p.csr_w = rw;
     } else {
-        p.csr_off = p.graph_mem.alloc<int32_t>(n + 1, s, true);
         p.csr_idx = p.graph_mem.alloc<int32_t>(1, s);
         p.csr_w = w ? p.graph_mem.alloc<uint32_t>(1, s) : nullptr;
     }
+    p.csr_off = roff;
     CU(cudaStreamSynchronize(s));
     tmp.release();
     p.csc_off = off;
@@ -393,6 +407,8 @@ void destroy_graph(ipregel_graph* g) {
         for (cudaEvent_t e : p.up_wc) cudaEventDestroy(e);
         if (p.perm_done) cudaEventDestroy(p.perm_done);
         p.perm_done = nullptr;
+        if (p.csr_done) cudaEventDestroy(p.csr_done);
+        p.csr_done = nullptr;
         p.up_wc.clear();
         p.pend.tmp.release();
         pinned_release(p.host_cnt);

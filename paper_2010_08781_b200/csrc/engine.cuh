@@ -293,6 +293,10 @@ struct Partition {
     } pend;
     std::vector<cudaEvent_t> up_wc;   // one per weight window (copy stream)
     cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
+    // IPREGEL_LAYOUT_DEGREE: the CSR's indices / weights are built on the aux stream after create
+    // returns; csr_off is ready.  wait_csr() orders the run stream after them (first use).
+    cudaEvent_t csr_done = nullptr;
+    bool csr_pending = false;
     std::vector<int64_t> wc_bounds;
     AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device
@@ -798,9 +802,20 @@ void transpose_rows(Partition& p, int64_t n, const int32_t* off, const int32_t* 
     if (out_w) *out_w = wx;
 }
 
+// Orders the run stream after a pending CSR build (IPREGEL_LAYOUT_DEGREE, create.cuh): called
+// by every path that reads the CSR's indices or weights.
+void wait_csr(ipregel_graph* g) {
+    for (auto& p : g->parts)
+        if (p.csr_pending) {
+            CU(cudaStreamWaitEvent(g->stream, p.csr_done, 0));
+            p.csr_pending = false;
+        }
+}
+
 // Push adjacency of one partition.  One partition: the graph's own CSR (+ CSC for CC).  Several:
 // transposes of the owned CSC (and, for CC, owned CSR) rows, over all N sources.
 void ensure_push_view(ipregel_graph* g, Partition& p) {
+    wait_csr(g);
     if (p.push_view_ready) return;
     cudaStream_t s = g->stream;
     const int64_t n = g->n;

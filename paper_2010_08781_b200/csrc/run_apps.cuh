@@ -316,6 +316,7 @@ double rowlist_edges(ipregel_graph* g, int app, int cur) {
 }
 
 ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipregel_run_params& P) {
+    wait_csr(g);   // Hash-Min gathers over the CSR; push expands over it
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
     const bool cc = app == IPREGEL_APP_HASHMIN_CC;

@@ -303,6 +303,7 @@ void launch_pull_program(ipregel_graph* g, const ipregel_program* pr, int pass, 
 template <class V>
 ipregel_status run_program_t(ipregel_graph* g, ipregel_program* pr, uint32_t max_steps,
                              const ipregel_run_params& P, const double* params, int nparams) {
+    wait_csr(g);   // symmetric pulls and push read the CSR
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
     const int app = kAppProgram;

@@ -286,6 +286,13 @@ __global__ void k_degree_keys(uint32_t* __restrict__ deg, int64_t n, int32_t* __
         ids[v] = (int32_t)v;
     }
 }
+// out-degrees in the new order from the sorted keys (~degree), into roff[0..n); roff[n] = 0
+__global__ void k_degree_from_keys(const uint32_t* __restrict__ keys, int64_t n,
+                                   int32_t* __restrict__ roff) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) roff[i] = (int32_t)~keys[i];
+    else if (i == n) roff[i] = 0;
+}
 __global__ void k_invert_perm(const int32_t* __restrict__ old_of_new, int64_t n,
                               int32_t* __restrict__ new_of_old) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
