@@ -89,6 +89,9 @@ int g_pr_split = getenv("IPREGEL_PR_SPLIT") ? atoi(getenv("IPREGEL_PR_SPLIT")) :
 // warps taking ranges from an atomic counter (IPREGEL_PULL_DYNAMIC=1) or striding (0).
 int g_pull_dynamic = getenv("IPREGEL_PULL_DYNAMIC") ? atoi(getenv("IPREGEL_PULL_DYNAMIC")) : 1;
 int g_pull_waves = getenv("IPREGEL_PULL_WAVES") ? std::max(atoi(getenv("IPREGEL_PULL_WAVES")), 0) : 1;
+// Range kernels: preferred shared-memory carveout in percent (IPREGEL_PULL_CARVEOUT; -1: the
+// driver's default)
+int g_pull_carveout = getenv("IPREGEL_PULL_CARVEOUT") ? atoi(getenv("IPREGEL_PULL_CARVEOUT")) : -1;
 // Hash-Min row-list pull when the rows not yet at label 0 hold fewer than this fraction of the
 // symmetrised edges (IPREGEL_ROWLIST; 0 = never).
 double g_rowlist = getenv("IPREGEL_ROWLIST") ? atof(getenv("IPREGEL_ROWLIST")) : 0.05;
@@ -470,6 +473,10 @@ unsigned pull_grid(int64_t num_tiles) {
         int dev = 0;
         CU(cudaGetDevice(&dev));
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (g_pull_carveout >= 0)   // shared-memory share of the unified L1 (percent; knob)
+            CU(cudaFuncSetAttribute(k_pull_ranges<Op>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    g_pull_carveout));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull_ranges<Op>, kPullThreads, 0));
         per_sm = std::max(per_sm, 1);
     }
