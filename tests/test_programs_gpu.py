@@ -374,3 +374,32 @@ def test_push_superstep_clears_stale_outbox(parts, exchange):
     want = np.bincount(dst[even], weights=(src[even] + 1), minlength=n).astype(np.uint32)
     np.testing.assert_array_equal(G.values(host=True), want)
     G.close()
+
+
+@pytest.mark.parametrize("mode", ["pull", "push", "auto"])
+def test_programs_on_library_relabel(mode):
+    """User programs on a graph the library relabelled itself (IPREGEL_LAYOUT_DEGREE): the CSR is
+    still being built on the library's aux stream when the first program runs; ids seen by the
+    programs (ipr_ctx.id, ipr_send targets, the SSSP source parameter) are original ids."""
+    import paper_2010_08781_b200 as ipr
+    from tests.graphs import to_device
+    n, src, dst, w = graph(913)
+    d = to_device(csr_csc(n, src, dst, w))
+    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], None, None,
+                                     d["csc_w"], None, layout=ipr.LAYOUT_DEGREE))
+    G.run_program(prog("hashmin_cc"), mode=mode)
+    np.testing.assert_array_equal(G.values(host=True), oracle.hashmin_cc(n, src, dst)["values"])
+    G.run_program(prog("sssp"), params=[11], mode=mode)
+    np.testing.assert_array_equal(G.values(host=True),
+                                  oracle.sssp(n, src, dst, w, source=11)["values"])
+    G.run_program(prog("pagerank"), params=[10], mode="pull" if mode == "auto" else mode)
+    o = oracle.pagerank(n, src, dst, k=10)
+    assert np.abs(G.values(host=True) - o["values"]).max() <= PR_ABS
+    G.close()
+    G = ipr.Graph(ipr.full_partition(n, d["e"], d["csc_off"], d["csc_idx"], None, None,
+                                     layout=ipr.LAYOUT_DEGREE))
+    G.run_program(prog("heap_children_sum"), mode="push")
+    ids = np.arange(n)
+    want = np.where(2 * ids + 1 < n, 2 * ids + 1, 0) + np.where(2 * ids + 2 < n, 2 * ids + 2, 0)
+    np.testing.assert_array_equal(G.values(host=True).astype(np.int64), want)
+    G.close()
