@@ -317,6 +317,8 @@ struct CCPullOut : MinU32, NoAggregate {
     const int32_t* __restrict__ out_off;  // owned CSR offsets
     int64_t vbase;
     PeerSlots<uint32_t> peers;            // fused exchange: other replicas of `next`
+    int count_all_zero;                   // aux: every row at label 0 (1), or only the rows that
+                                          // reached it in this superstep (0; the host adds them up)
     const void* gather_base() const { return cur; }
     __device__ const T* gptr() const { return cur; }
     __device__ bool absorbed(int32_t row) const { return next[vbase + row] == 0u; }
@@ -327,13 +329,19 @@ struct CCPullOut : MinU32, NoAggregate {
         v = m < v ? m : v;
         next[vbase + row] = v;
         peers.store(vbase + row, v);
-        const uint32_t deg = (uint32_t)(in_off[row + 1] - in_off[row]) +
-                             (uint32_t)(out_off[row + 1] - out_off[row]);
-        if (v < old) {
-            c.changed += 1;
-            c.messages += deg;
+        // degrees only where a counter needs them: the changed rows (messages) and, for the
+        // row-list decision, rows at label 0 -- all of them, or only those new at 0 (most rows
+        // sit at 0 unchanged after superstep 1: their four offset loads were most of the
+        // CSR pass of superstep 2)
+        if (v < old || (count_all_zero && v == 0u)) {
+            const uint32_t deg = (uint32_t)(in_off[row + 1] - in_off[row]) +
+                                 (uint32_t)(out_off[row + 1] - out_off[row]);
+            if (v < old) {
+                c.changed += 1;
+                c.messages += deg;
+            }
+            if (v == 0u) c.aux += deg;   // rows at label 0 (row-list pull decision)
         }
-        if (v == 0u) c.aux += deg;   // absorbed rows (row-list pull decision)
     }
 };
 

@@ -530,6 +530,7 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                     CCPullOut b;
                     b.cur = S.val[cur]; b.next = S.val[1 - cur]; b.in_off = p.csc_off;
                     b.out_off = p.csr_off; b.vbase = p.vb;
+                    b.count_all_zero = prev_mode != 1;   // else zero_edges is kept up to date
                     b.peers = peer_slots<uint32_t>(S, 1 - cur, fused);
                     launch_pull(b, p.plan_csr, p.csr_off, p.csr_idx, nullptr, p.pull_cnt, s, n,
                                 g->gather_policy, g->degree_ordered);
@@ -551,7 +552,8 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 exchange_owned<uint32_t>(g, [app, nx](Partition& p) { return p.st[app].val[nx]; });
             unsigned long long c[5];
             reduce_counters(g, false, c, 5);
-            zero_edges = c[3];
+            // rows at label 0 stay there: after a plain pull superstep only the new ones count
+            zero_edges = prev_mode != 1 ? c[3] : zero_edges + c[3];
             if (!cc) m_prev = (uint32_t)(kInf - (uint32_t)reduce_max_delta(g));
             T.end();
             StepRecord& R = g->steps.back();
