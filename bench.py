@@ -396,6 +396,7 @@ def main():
     if "pagerank" in args.apps:
         sts = [step["pagerank"] for step in per_step]
         k_ms = np.concatenate([s["kernel_ms"][1:] for s in sts])
+        rk_ms = np.concatenate([s["part_ms"][1:] for s in sts])
         mb = np.concatenate([s["model_bytes"][1:] for s in sts]).astype(np.float64)
         t_ms = float(np.mean(k_ms))
         if world > 1:
@@ -415,6 +416,10 @@ def main():
                 "model": "SURVEY.md 8(d): 12 B/edge (4 B index + 8 B gathered f64 outbox) + "
                          "24 B/vertex (CSC offset, out-degree, rank, next outbox)",
                 "avg_launch_ms": t_ms, "peak_source": peak_src,
+                # attribution of the superstep (library events, same stream and clocks): the
+                # range kernel + fixup, and the update pass (k_pr_finish)
+                "range_kernel_ms": float(np.mean(rk_ms)),
+                "update_pass_ms": float(np.mean(k_ms - rk_ms)),
                 "frac_of_8TBps": achieved / 8000.0,
                 "frac_16N": float(mb16 / (t_ms * 1e-3) / 1e9) / peak}
         apps_out["pagerank"]["superstep_ms_median"] = float(np.median(

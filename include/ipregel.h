@@ -225,6 +225,8 @@ typedef struct {
                                  else 0                                                         */
     double* pagerank_mass;    /* PageRank with IPREGEL_RUN_PAGERANK_MASS: sum_v r_s(v), else 0  */
     double* pagerank_mass_nd; /*   and sum of r_s(v) over vertices with out-degree > 0          */
+    float* part_ms;           /* PageRank pull supersteps: time of the range kernel + fixup alone
+                                 (the rest of kernel_ms is the update pass, k_pr_finish); 0 else */
 } ipregel_stats;
 
 /* ---- errors / device ---------------------------------------------------------------------- */

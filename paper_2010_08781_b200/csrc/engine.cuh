@@ -314,6 +314,7 @@ struct StepRecord {
     uint64_t changed = 0, messages = 0, edges_scanned = 0, model_bytes = 0;
     double delta = 0.0;   // PageRank: max_v |r_s(v) - r_{s-1}(v)| (to-convergence runs)
     double mass[2] = {0.0, 0.0};   // PageRank mass check: sum r_s, sum over outdeg > 0
+    float part_ms = 0;             // PageRank pull: range kernel + fixup (kernel_ms - update)
 };
 
 }  // namespace

@@ -641,6 +641,7 @@ ipregel_status ipregel_get_stats(ipregel_graph* g, ipregel_stats* st) {
         if (st->pagerank_delta) st->pagerank_delta[i] = R.delta;
         if (st->pagerank_mass) st->pagerank_mass[i] = R.mass[0];
         if (st->pagerank_mass_nd) st->pagerank_mass_nd[i] = R.mass[1];
+        if (st->part_ms) st->part_ms[i] = R.part_ms;
     }
     return IPREGEL_OK;
     ABI_END

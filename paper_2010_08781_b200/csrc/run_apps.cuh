@@ -7,6 +7,15 @@ namespace {
 // =============================================================================================
 // PageRank (Fig. 8)
 // =============================================================================================
+// part_ms of every gather superstep of a PageRank pull run (after finalize_times).
+void fill_part_ms(ipregel_graph* g, uint32_t k) {
+    for (uint32_t s = 1; s < g->steps.size() && s <= k; ++s) {
+        float a = 0;
+        CU(cudaEventElapsedTime(&a, ev(g, 4 * s + 1), ev(g, 4 * (k + 1) + s)));
+        g->steps[s].part_ms = a;
+    }
+}
+
 // IPREGEL_TRACE_KERNELS=1: per gather superstep of a PageRank pull run, the time of the range
 // kernel + fixup, of k_pr_finish, and what the superstep adds around them (events on the run
 // stream, the same clocks), printed to stderr -- the attribution of a superstep's time.
@@ -86,7 +95,10 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         g->last_exchange = G.exchange;
         finalize_times(g);
         if (mass) read_mass(g);
-        if (g_trace_kernels && g_pr_split && !push) trace_pr_kernels(g, k);
+        if (g_pr_split && !push && !track) {
+            fill_part_ms(g, k);
+            if (g_trace_kernels) trace_pr_kernels(g, k);
+        }
         return G.status;
     }
     const unsigned long long launches0 = g_launches.load(std::memory_order_relaxed);
@@ -176,7 +188,7 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                     sop.vbase = p.vb;
                     launch_pull(sop, p.plan_csc, p.csc_off, p.csc_idx, nullptr, nullptr, s, n,
                                 g->gather_policy, g->degree_ordered);
-                    if (g_trace_kernels) T.rec(4 * (k + 1) + step);   // range kernel + fixup done
+                    T.rec(4 * (k + 1) + step);   // range kernel + fixup done (stats part_ms)
                     const unsigned fg = grid_for(ceil_div(p.rows, kPrFinishRows), 256);
                     if (track || mass || (broadcast && write_rank))
                         k_pr_finish<0><<<fg, 256, 0, s>>>(op, p.rows, track ? p.pull_cnt : nullptr);
@@ -253,7 +265,10 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     }
     finalize_times(g);
     if (mass) read_mass(g);
-    if (g_trace_kernels && g_pr_split && !push) trace_pr_kernels(g, k);
+    if (g_pr_split && !push && !track) {
+        fill_part_ms(g, k);
+        if (g_trace_kernels) trace_pr_kernels(g, k);
+    }
     return status;
 }
 

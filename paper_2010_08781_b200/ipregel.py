@@ -83,7 +83,8 @@ class Stats(ctypes.Structure):
                 ("mode", ctypes.c_void_p), ("changed", ctypes.c_void_p),
                 ("messages", ctypes.c_void_p), ("edges_scanned", ctypes.c_void_p),
                 ("model_bytes", ctypes.c_void_p), ("pagerank_delta", ctypes.c_void_p),
-                ("pagerank_mass", ctypes.c_void_p), ("pagerank_mass_nd", ctypes.c_void_p)]
+                ("pagerank_mass", ctypes.c_void_p), ("pagerank_mass_nd", ctypes.c_void_p),
+                ("part_ms", ctypes.c_void_p)]
 
 
 class ProgramDesc(ctypes.Structure):
@@ -463,6 +464,7 @@ class Graph:
             "pagerank_delta": np.zeros(capacity, np.float64),
             "pagerank_mass": np.zeros(capacity, np.float64),
             "pagerank_mass_nd": np.zeros(capacity, np.float64),
+            "part_ms": np.zeros(capacity, np.float32),
         }
         st = Stats()
         st.capacity = capacity
