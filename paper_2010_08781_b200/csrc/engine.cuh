@@ -230,6 +230,7 @@ struct AppState {
     double* acc = nullptr;                     // PageRank push accumulator (owned)
     uint32_t* val[2] = {nullptr, nullptr};     // CC/SSSP value replicas [N] (current / next)
     uint32_t* bits = nullptr;                  // owned bitmap of broadcasters
+    uint32_t* nbr = nullptr;                   // Hash-Min: owned rows with a neighbour (bitmap)
     int32_t* f_id = nullptr;                   // owned frontier (ascending ids) + snapshots
     uint32_t* f_val = nullptr;
     int32_t* g_id = nullptr;                   // global frontier (== f_* on one partition)

@@ -404,9 +404,19 @@ k_rowlist_min(PushAdj adj, const int32_t* __restrict__ e_id, const long long* __
 
 // Owned rows whose value is not `v0` (ballot per warp).
 __global__ void k_bits_ne(const uint32_t* __restrict__ vals, int64_t rows, uint32_t v0,
-                          uint32_t* __restrict__ bits) {
+                          const uint32_t* __restrict__ mask, uint32_t* __restrict__ bits) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool pred = i < rows && vals[i] != v0;
+    const uint32_t b = __ballot_sync(kFull, pred);
+    if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = mask ? b & mask[i >> 5] : b;
+}
+// Rows with at least one neighbour in the symmetrised graph (CSC or CSR row not empty), one bit
+// per owned row: the others never receive a message and keep their label, so the Hash-Min row
+// list leaves them out (a third of cfg4's vertices are isolated).
+__global__ void k_nbr_bits(const int32_t* __restrict__ in_off, const int32_t* __restrict__ out_off,
+                           int64_t rows, uint32_t* __restrict__ bits) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool pred = i < rows && (in_off[i + 1] > in_off[i] || out_off[i + 1] > out_off[i]);
     const uint32_t b = __ballot_sync(kFull, pred);
     if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
 }

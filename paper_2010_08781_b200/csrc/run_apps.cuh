@@ -309,8 +309,14 @@ double rowlist_edges(ipregel_graph* g, int app, int cur) {
     cudaStream_t s = g->stream;
     for (auto& p : g->parts) {
         AppState& S = p.st[app];
+        if (p.rows && !S.nbr) {   // once per graph: rows that have a neighbour at all
+            S.nbr = S.mem.alloc<uint32_t>(words_of(p.rows), s);
+            k_nbr_bits<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csc_off, p.csr_off, p.rows, S.nbr);
+            LAUNCH_CHECK();
+        }
         if (p.rows)
-            k_bits_ne<<<grid_for(p.rows, 256), 256, 0, s>>>(S.val[cur] + p.vb, p.rows, 0u, S.bits);
+            k_bits_ne<<<grid_for(p.rows, 256), 256, 0, s>>>(S.val[cur] + p.vb, p.rows, 0u, S.nbr,
+                                                           S.bits);
         LAUNCH_CHECK();
         compact_bitmap(g, p, S, S.val[cur], true);
         CU(cudaMemcpyAsync(p.host_cnt + 4, p.front_cnt, 16, cudaMemcpyDeviceToHost, s));
