@@ -421,6 +421,24 @@ __global__ void k_nbr_bits(const int32_t* __restrict__ in_off, const int32_t* __
     if ((threadIdx.x & 31) == 0 && i < rows) bits[i >> 5] = b;
 }
 
+// Hash-Min row-list superstep: only the listed rows (global ids, `len` of them) can have
+// changed; mark those whose label decreased in the (zeroed) owned bitmap.
+__global__ void k_bits_from_list_diff(const int32_t* __restrict__ ids,
+                                      const unsigned long long* __restrict__ len,
+                                      const uint32_t* __restrict__ before,
+                                      const uint32_t* __restrict__ after, int64_t vbase,
+                                      uint32_t* __restrict__ bits) {
+    const int64_t n = (int64_t)*len;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ids[i];
+        if (after[v] < before[v]) {
+            const int64_t r = v - vbase;
+            atomicOr(bits + (r >> 5), 1u << (r & 31));
+        }
+    }
+}
+
 // Pull -> push switch: the broadcasters of a pull superstep are the vertices whose value
 // decreased; mark them in the bitmap (owned range, ballot per warp).
 __global__ void k_bitmap_from_diff(const uint32_t* __restrict__ before,

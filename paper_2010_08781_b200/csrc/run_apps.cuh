@@ -499,11 +499,15 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                 LAUNCH_CHECK();
             }
             T.kend();
-            // broadcasters = rows whose label decreased; their count and symmetrised degrees
+            // broadcasters = rows whose label decreased (only listed rows can): their count and
+            // symmetrised degrees
             for (auto& p : g->parts) {
                 AppState& S = p.st[app];
-                k_bitmap_from_diff<<<grid_for(std::max<int64_t>(p.rows, 1), 256), 256, 0, s>>>(
-                    S.val[cur], S.val[1 - cur], p.vb, p.rows, S.bits);
+                CU(cudaMemsetAsync(S.bits, 0, words_of(p.rows) * sizeof(uint32_t), s));
+                k_bits_from_list_diff<<<std::max<unsigned>(1u, std::min<unsigned>(
+                                            grid_for((int64_t)p.host_cnt[4], 256), sm_grid(8))),
+                                        256, 0, s>>>(S.f_id, &p.front_cnt->changed, S.val[cur],
+                                                     S.val[1 - cur], p.vb, S.bits);
                 LAUNCH_CHECK();
                 compact_bitmap(g, p, S, S.val[1 - cur], true);
             }
