@@ -524,7 +524,10 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
             changed = c[0];
             messages = c[1];
             cur = 1 - cur;
-            lists_ready = false;
+            // the broadcasters were compacted above (ids + new labels): on one partition that
+            // is the next push superstep's frontier as it stands (ranks / loopback partitions
+            // still need the frontier exchange, done by the push branch)
+            lists_ready = !multi;
         } else {
             // ---- pull: gather over CSC (and CSR for CC), value[next] = min(value, gathered)
             if (!cc && prev_mode == 2) {
