@@ -315,8 +315,9 @@ double rowlist_edges(ipregel_graph* g, int app, int cur) {
             LAUNCH_CHECK();
         }
         if (p.rows)
-            k_bits_ne<<<grid_for(p.rows, 256), 256, 0, s>>>(S.val[cur] + p.vb, p.rows, 0u, S.nbr,
-                                                           S.bits);
+            k_bits_ne<<<std::max<unsigned>(1u, std::min<unsigned>(
+                            grid_for(ceil_div(p.rows, 1024) * 32, 256), sm_grid(16))),
+                        256, 0, s>>>(S.val[cur] + p.vb, p.rows, 0u, S.nbr, S.bits);
         LAUNCH_CHECK();
         compact_bitmap(g, p, S, S.val[cur], true);
         CU(cudaMemcpyAsync(p.host_cnt + 4, p.front_cnt, 16, cudaMemcpyDeviceToHost, s));
@@ -434,7 +435,9 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
                         k_fill_bits<<<grid_for(words_of(p.rows), 256), 256, 0, s>>>(S.bits, p.rows);
                     } else {
                         // pull -> push: broadcasters = vertices whose value decreased
-                        k_bitmap_from_diff<<<grid_for(p.rows, 256), 256, 0, s>>>(
+                        k_bitmap_from_diff<<<std::max<unsigned>(1u, std::min<unsigned>(
+                                                 grid_for(ceil_div(p.rows, 1024) * 32, 256),
+                                                 sm_grid(16))), 256, 0, s>>>(
                             S.val[1 - cur], S.val[cur], p.vb, p.rows, S.bits);
                     }
                     LAUNCH_CHECK();
