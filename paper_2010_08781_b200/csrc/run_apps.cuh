@@ -121,7 +121,8 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
     for (auto& p : g->parts) {
         AppState& S = p.st[IPREGEL_APP_PAGERANK];
         if (p.rows == 0) continue;
-        k_init_pagerank<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csr_off, p.rows, p.vb, inv_n,
+        k_init_pagerank<<<grid_for(ceil_div(p.rows, kInitRows), 256), 256, 0, s>>>(
+                                                              p.csr_off, p.rows, p.vb, inv_n,
                                                               k > 0, last == 0 || track, S.rank,
                                                               S.contrib[0], mass_slot(0));
         LAUNCH_CHECK();
@@ -372,8 +373,9 @@ ipregel_status run_min(ipregel_graph* g, int app, uint32_t max_steps, const ipre
     T0.kbegin();
     for (auto& p : g->parts) {
         AppState& S = p.st[app];
-        if (cc) k_init_cc<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, g->vertex_ids);
-        else k_init_sssp<<<grid_for(n, 256), 256, 0, s>>>(S.val[0], n, source);
+        const unsigned ig = std::min<unsigned>(grid_for(ceil_div(n, 4), 256), sm_grid(16));
+        if (cc) k_init_cc<<<ig, 256, 0, s>>>(S.val[0], n, g->vertex_ids);
+        else k_init_sssp<<<ig, 256, 0, s>>>(S.val[0], n, source);
         LAUNCH_CHECK();
     }
     T0.kend();

@@ -9,19 +9,30 @@ namespace ipr {
 // ---- superstep 0 (the `ip_is_first_superstep()` branches of Figs. 8-10) --------------------
 // PageRank, Fig. 8 / PAPER.md:322: value = 1/N and, if superstep 0 < k, broadcast value/outdeg
 // (a vertex without out-neighbours does not broadcast, reading R4).
+// 4 rows per thread (block-strided, coalesced), their out-degrees loaded before any division
+// (the loads then overlap; as k_pr_finish)
+constexpr int kInitRows = 4;
 __global__ void k_init_pagerank(const int32_t* __restrict__ out_off, int64_t rows, int64_t vbase,
                                 double inv_n, int broadcast, int write_rank,
                                 double* __restrict__ rank, double* __restrict__ contrib,
                                 double* __restrict__ mass) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kInitRows + threadIdx.x;
     LaneCounters c;
-    if (i < rows) {
+    int32_t deg[kInitRows];
+#pragma unroll
+    for (int j = 0; j < kInitRows; ++j) {
+        const int64_t i = base + (int64_t)j * blockDim.x;
+        deg[j] = i < rows && (broadcast || mass) ? out_off[i + 1] - out_off[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kInitRows; ++j) {
+        const int64_t i = base + (int64_t)j * blockDim.x;
+        if (i >= rows) continue;
         if (write_rank) rank[i] = inv_n;
-        if (broadcast || mass) {
-            const int32_t deg = out_off[i + 1] - out_off[i];
-            if (broadcast) contrib[vbase + i] = deg > 0 ? __ddiv_rn(inv_n, (double)deg) : 0.0;
-            c.m0 = inv_n;
-            c.m1 = deg > 0 ? inv_n : 0.0;
+        if (broadcast) contrib[vbase + i] = deg[j] > 0 ? __ddiv_rn(inv_n, (double)deg[j]) : 0.0;
+        if (mass) {
+            c.m0 += inv_n;
+            if (deg[j] > 0) c.m1 += inv_n;
         }
     }
     if (mass) flush_mass(c, mass);   // grid-uniform; whole warps (blocks of 256)
@@ -106,8 +117,25 @@ __global__ void k_invert_ids(const int32_t* __restrict__ ids, int64_t n, int32_t
 // Hash-Min CC, Fig. 9: value = id, the ORIGINAL id under a relabelled layout (every replica
 // initialises all N locally -- no exchange).
 __global__ void k_init_cc(uint32_t* __restrict__ val, int64_t n, const int32_t* __restrict__ ids) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) val[i] = ids ? (uint32_t)ids[i] : (uint32_t)i;
+    // grid-stride, 16-byte loads and stores where both arrays allow (pool allocations are
+    // 256-byte aligned; caller-provided vertex_ids may not be)
+    const bool vec = ids == nullptr || (reinterpret_cast<uintptr_t>(ids) & 15) == 0;
+    const int64_t n4 = vec ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint4* v4 = reinterpret_cast<uint4*>(val);
+    for (int64_t i = t; i < n4; i += stride) {
+        uint4 x;
+        if (ids) {
+            const int4 y = reinterpret_cast<const int4*>(ids)[i];
+            x = make_uint4((uint32_t)y.x, (uint32_t)y.y, (uint32_t)y.z, (uint32_t)y.w);
+        } else {
+            x = make_uint4((uint32_t)(4 * i), (uint32_t)(4 * i + 1), (uint32_t)(4 * i + 2),
+                           (uint32_t)(4 * i + 3));
+        }
+        v4[i] = x;
+    }
+    for (int64_t i = (n4 << 2) + t; i < n; i += stride) val[i] = ids ? (uint32_t)ids[i] : (uint32_t)i;
 }
 
 // internal id of original vertex `orig` (vertex_ids is a permutation)
@@ -137,8 +165,20 @@ __global__ void k_count_ids(const int32_t* __restrict__ ids, int64_t n, int32_t*
 
 // SSSP, Fig. 10: source = 0, everyone else INF.
 __global__ void k_init_sssp(uint32_t* __restrict__ val, int64_t n, int64_t source) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) val[i] = i == source ? 0u : kInf;
+    // grid-stride, 16-byte stores (val is 256-byte aligned: a pool allocation)
+    uint4* v4 = reinterpret_cast<uint4*>(val);
+    const int64_t n4 = n >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint4 x = make_uint4(kInf, kInf, kInf, kInf);
+        if ((source >> 2) == i) (&x.x)[source & 3] = 0u;
+        v4[i] = x;
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < (n & 3)) {
+        const int64_t i = (n4 << 2) + t;
+        val[i] = i == source ? 0u : kInf;
+    }
 }
 
 __global__ void k_fill_bits(uint32_t* __restrict__ bits, int64_t rows) {
