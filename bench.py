@@ -328,8 +328,11 @@ def main():
     torch.cuda.set_device(local)
     ipr.device_check(local)
     use_comm = world > 1 or args.comm
+    if use_comm:
+        # NCCL logs to stderr, never into the JSON line on stdout; a multi-GPU run keeps its
+        # INFO lines (ranks, rings, NVLS) there
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if world > 1:
-        # NCCL's INFO lines (ranks, rings, NVLS) stay in the log of a multi-GPU run
         os.environ.setdefault("NCCL_DEBUG", "INFO")
     if use_comm:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -505,7 +508,8 @@ def e2e_measure_ranks(part, n, e, args, msgs_per_step, stream, comm, world):
     hpart = ipr.Partition(n, e, part.vertex_begin, part.vertex_end,
                           *[None if hs[k] is None else hs[k].numpy() for k in
                             ("csc_offsets", "csc_indices", "csr_offsets", "csr_indices",
-                             "csc_weights", "csr_weights", "vertex_ids")], True)
+                             "csc_weights", "csr_weights", "vertex_ids")],
+                          part.degree_ordered, part.layout)
     outs = {app: torch.empty(n, dtype=torch.float64 if app == "pagerank" else torch.int32,
                              pin_memory=True) for app in args.apps}
     d2h = sum(o.numel() * o.element_size() for o in outs.values())
