@@ -440,8 +440,9 @@ def main():
               "vertex_state_bytes": int(sb),
               "state_bytes_per_vertex": round(sb / (n / world), 2),
               "note": "vertex state is Theta(N) (single-slot mailboxes, PAPER.md:205-211, "
-                      ":476-480); library graph bytes are the range plans (the graph arrays are "
-                      "borrowed)"}
+                      ":476-480); library graph bytes: the relabelled CSC and the derived CSR "
+                      "(IPREGEL_LAYOUT_DEGREE) plus the range plans; the user's arrays are "
+                      "borrowed"}
 
     # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
     e2e = None
