@@ -465,6 +465,7 @@ struct RangeArgs {
     uint32_t ghot, gtotal;
     int32_t l1hot;
     int32_t* range_ctr;   // non-null: warps take ranges from this zeroed counter (dynamic)
+    int32_t order;        // dynamic range order (knob IPREGEL_RANGE_ORDER, see k_pull_ranges)
 };
 
 // counters: warp reduce, one shared atomic per warp, one global atomic per CTA
@@ -845,9 +846,23 @@ __global__ void __launch_bounds__(kPullThreads, PullMinBlocks<Op>::value) k_pull
         const int lane = threadIdx.x & 31;
         int32_t r = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
         r = __shfl_sync(kFull, r, 0);
-        while (r < A.num_ranges) {
+        const int32_t per = A.order >= 2 ? (A.num_ranges + A.order - 1) / A.order : 0;
+        const int32_t limit = A.order >= 2 ? per * A.order : A.num_ranges;
+        while (r < limit) {
             const int32_t nx = lane == 0 ? atomicAdd(A.range_ctr, 1) : 0;
-            pull_range<Op>(op, A, r, s_sum[wid], cnt);
+            // order of the ranges in time (knob): 1 = alternate between the two ends of the
+            // plan, so long-row ranges (low ids under the degree layout) and short-row ranges
+            // run side by side; the result of every range is the same either way
+            int32_t q = r;
+            if (A.order == 1) {
+                q = (r & 1) ? A.num_ranges - 1 - (r >> 1) : (r >> 1);
+            } else if (A.order >= 2) {
+                // A.order interleaved streams over equal slices of the plan (a bijection of
+                // [0, per * order) onto slice-major positions; those past the plan are skipped)
+                q = (r % A.order) * per + r / A.order;
+                if (q >= A.num_ranges) q = -1;
+            }
+            if (q >= 0) pull_range<Op>(op, A, q, s_sum[wid], cnt);
             r = __shfl_sync(kFull, nx, 0);
         }
     } else {
