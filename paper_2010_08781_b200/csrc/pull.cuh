@@ -10,7 +10,8 @@
 // RANGES of kRangeItems items (merge path), so every range holds the same number of edges + rows
 // whatever the degree distribution (hub rows of in-degree ~1.5M at scale 26, long runs of rows
 // without in-edges) -- no degree binning pass, no shared-memory staging, no block barrier.  One
-// resident wave of CTAs runs; each warp takes range after range from an atomic counter.  A warp
+// resident wave of CTAs runs; each warp takes range after range from an atomic counter,
+// alternately from the two ends of the plan (long-row and short-row ranges side by side).  A warp
 // walks the edges of its range in CHUNKS of 128 (4 per lane):
 //   1. column indices arrive with coalesced L2-evict-first loads two chunks ahead and the
 //      outbox values are gathered one chunk ahead (software pipeline, 8 gathers in flight per
@@ -614,8 +615,9 @@ __device__ __forceinline__ void pull_range(const Op& op, const RangeArgs& A, int
             // the open row is settled and runs on for several chunks: jump straight to the
             // chunk holding its end (or the range's last chunk) and restart the pipeline there
             // instead of stepping through chunks whose gathers are all skipped.  Hash-Min only:
-            // measured at cfg4, Hash-Min 16.96 -> 16.6 ms, while the same code in the SSSP op
-            // costs it 13.3 -> 15.2 ms (its register allocation), jump or not.
+            // measured at cfg4, Hash-Min 16.96 -> 16.6 ms, while SSSP (settled rows are shorter,
+            // each jump exposes the restarted pipeline's latency) went 12.8 -> 14.4-14.8 ms at
+            // 4, 5 or 6 CTAs per SM.
             if (absorbed && r < x1 && e0 >= 0) {
                 const int32_t t = (Ec < y1 ? Ec : y1) - 1;
                 const int32_t ej = t - ((t + A.cphase) & (kChunk - 1));
