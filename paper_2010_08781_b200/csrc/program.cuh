@@ -562,11 +562,20 @@ struct ProgDeliver {
     V* mbox;
     uint32_t* recv;
     int64_t vbase;
-    __device__ __forceinline__ void operator()(int32_t u, uint32_t, int32_t v, uint32_t w) const {
+    // (the sender's broadcast value, the recipient's received-bits word: a filter for the OR)
+    struct Pre {
+        V m;
+        uint32_t r;
+    };
+    __device__ __forceinline__ Pre pre(int32_t u, uint32_t, int32_t v, uint32_t) const {
         const int64_t lv = (int64_t)v - vbase;
-        ProgComb<V, P::kCombiner>::atomic(mbox + lv, P::edge(out_cur[u], w));
+        return Pre{out_cur[u], recv[lv >> 5]};
+    }
+    __device__ __forceinline__ void fin(const Pre& p, int32_t, uint32_t, int32_t v, uint32_t w) const {
+        const int64_t lv = (int64_t)v - vbase;
+        ProgComb<V, P::kCombiner>::atomic(mbox + lv, P::edge(p.m, w));
         const uint32_t bit = 1u << (lv & 31);
-        if (!(recv[lv >> 5] & bit)) atomicOr(recv + (lv >> 5), bit);
+        if (!(p.r & bit)) atomicOr(recv + (lv >> 5), bit);
     }
 };
 

@@ -245,7 +245,9 @@ k_list_write(const int32_t* __restrict__ f_id, const uint32_t* __restrict__ f_va
 // Edge-balanced over the expand list: per chunk of kExpandItems edges, the frontier entries it
 // touches, each with its adjacency bases resolved once, and an owner table (edge slot -> entry)
 // from a block scan of the entries' start flags -- no per-edge search, no per-edge offset loads.
-// `deliver(u, snapshot, v, w)` folds the message of edge (u -> v, w) into v's slot.
+// The message of edge (u -> v, w) with the sender's snapshot is folded into v's slot in two
+// steps: `p = deliver.pre(u, snapshot, v, w)` issues the loads (plain reads that only filter or
+// feed the fold), `deliver.fin(p, u, snapshot, v, w)` the atomics.
 template <class Deliver>
 __device__ __forceinline__ void expand_edges(const PushAdj& adj, const int32_t* __restrict__ e_id,
                                              const uint32_t* __restrict__ e_val,
@@ -268,15 +270,24 @@ __device__ __forceinline__ void expand_edges(const PushAdj& adj, const int32_t* 
          e0 += (int64_t)gridDim.x * kExpandItems) {
         const int64_t e1 = e0 + kExpandItems < total ? e0 + kExpandItems : total;
         const int span = (int)(e1 - e0);
-        if (threadIdx.x < 2) {
-            // entry owning edge e: last i with e_pre[i] <= e
-            const int64_t target = threadIdx.x == 0 ? e0 : e1 - 1;
+        if (warp < 2) {
+            // entry owning edge e: last i with e_pre[i] <= e (e_pre[0] = 0 <= e).  A 32-way
+            // search by one warp per end: each step probes 32 evenly spaced entries of [lo, hi]
+            // at once, so the dependent load chain is log32(n) long instead of log2(n)
+            const int64_t target = warp == 0 ? e0 : e1 - 1;
             int64_t lo = 0, hi = n - 1;
             while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (e_pre[mid] <= target) lo = mid; else hi = mid - 1;
+                const int64_t len = hi - lo + 1;
+                const int64_t stride = (len + 31) >> 5;
+                const int64_t p = lo + (int64_t)lane * stride;
+                const bool le = p <= hi && e_pre[p] <= target;
+                const int k = __popc(__ballot_sync(kFull, le)) - 1;   // lane 0 probes lo: k >= 0
+                lo += (int64_t)k * stride;
+                if (stride == 1) break;
+                const int64_t h = lo + stride - 1;
+                hi = h < hi ? h : hi;
             }
-            s_range[threadIdx.x] = (int)lo;
+            if (lane == 0) s_range[warp] = (int)lo;
         }
         for (int j = threadIdx.x; j < kExpandItems; j += kExpandThreads) s_owner[j] = 0;
         __syncthreads();
@@ -319,20 +330,38 @@ __device__ __forceinline__ void expand_edges(const PushAdj& adj, const int32_t* 
             s_owner[threadIdx.x * kPer + k] = (uint16_t)pre;
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < span; j += kExpandThreads) {
-            const int o = s_owner[j];
-            const int32_t pos = j - s_start[o];
-            int32_t v;
-            uint32_t w = 1u;
-            if (pos < s_d1[o]) {
-                v = adj.idx1[s_b1[o] + pos];
-                if (adj.w1) w = adj.w1[s_b1[o] + pos];
-            } else {
-                v = adj.idx2[s_b2[o] + (pos - s_d1[o])];
-                if (adj.w2) w = adj.w2[s_b2[o] + (pos - s_d1[o])];
+        // a thread's kPer edges in three batched phases -- all destination (and weight) loads,
+        // then the deliveries' loads, then their atomics -- so kPer independent requests are in
+        // flight per phase instead of one load-atomic chain per edge
+        int32_t v[kPer];
+        uint32_t w[kPer];
+        int ow[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = threadIdx.x + k * kExpandThreads;
+            ow[k] = -1;
+            v[k] = 0;
+            w[k] = 1u;
+            if (j < span) {
+                const int o = s_owner[j];
+                const int32_t pos = j - s_start[o];
+                ow[k] = o;
+                if (pos < s_d1[o]) {
+                    v[k] = adj.idx1[s_b1[o] + pos];
+                    if (adj.w1) w[k] = adj.w1[s_b1[o] + pos];
+                } else {
+                    v[k] = adj.idx2[s_b2[o] + (pos - s_d1[o])];
+                    if (adj.w2) w[k] = adj.w2[s_b2[o] + (pos - s_d1[o])];
+                }
             }
-            deliver(s_id[o], s_val[o], v, w);
         }
+        typename Deliver::Pre pv[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (ow[k] >= 0) pv[k] = deliver.pre(s_id[ow[k]], s_val[ow[k]], v[k], w[k]);
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (ow[k] >= 0) deliver.fin(pv[k], s_id[ow[k]], s_val[ow[k]], v[k], w[k]);
         __syncthreads();
     }
 }
@@ -341,6 +370,15 @@ __device__ __forceinline__ void expand_edges(const PushAdj& adj, const int32_t* 
 // (SSSP); atomicMin into the live value of the recipient; a successful decrease marks the
 // recipient in the next bitmap.  Sum program (PageRank push): atomicAdd of the sender's
 // contribution into the accumulator.
+template <bool B, class A, class C>
+struct PickT {
+    using type = A;
+};
+template <class A, class C>
+struct PickT<false, A, C> {
+    using type = C;
+};
+
 template <int kProgram>
 struct BuiltinDeliver {
     int64_t dst_base;
@@ -348,14 +386,21 @@ struct BuiltinDeliver {
     uint32_t* bits;
     const double* contrib;
     double* acc;
-    __device__ __forceinline__ void operator()(int32_t u, uint32_t snap, int32_t v,
-                                               uint32_t w) const {
+    // PageRank: the sender's contribution; min programs: the recipient's current value (a cheap
+    // filter read before the atomics -- the atomic decides)
+    using Pre = typename PickT<kProgram == 0, double, uint32_t>::type;
+    __device__ __forceinline__ Pre pre(int32_t u, uint32_t, int32_t v, uint32_t) const {
+        if constexpr (kProgram == 0) return contrib[u];
+        else return val[v];
+    }
+    __device__ __forceinline__ void fin(Pre p, int32_t, uint32_t snap, int32_t v,
+                                        uint32_t w) const {
         const int64_t lv = (int64_t)v - dst_base;
-        if (kProgram == 0) {
-            atomicAdd(acc + lv, contrib[u]);
+        if constexpr (kProgram == 0) {
+            atomicAdd(acc + lv, p);
         } else {
             const uint32_t msg = kProgram == 2 ? sat_add(snap, w) : snap;
-            if (msg < val[v]) {  // cheap filter; the atomic decides
+            if (msg < p) {
                 const uint32_t old = atomicMin(val + v, msg);
                 if (msg < old) atomicOr(bits + (lv >> 5), 1u << (lv & 31));
             }
@@ -386,9 +431,12 @@ k_expand(PushAdj adj, const int32_t* __restrict__ e_id, const uint32_t* __restri
 struct RowMinDeliver {
     const uint32_t* cur;   // labels after superstep s-1 (replica, global ids)
     uint32_t* next;        // next[u] = cur[u] on entry (owned rows), min over neighbours on exit
-    __device__ __forceinline__ void operator()(int32_t u, uint32_t, int32_t v, uint32_t) const {
-        const uint32_t m = cur[v];
-        if (m < next[u]) atomicMin(next + u, m);
+    using Pre = uint2;     // (neighbour's label, row's next value before this batch)
+    __device__ __forceinline__ Pre pre(int32_t u, uint32_t, int32_t v, uint32_t) const {
+        return make_uint2(cur[v], next[u]);
+    }
+    __device__ __forceinline__ void fin(Pre p, int32_t u, uint32_t, int32_t, uint32_t) const {
+        if (p.x < p.y) atomicMin(next + u, p.x);
     }
 };
 
