@@ -151,7 +151,9 @@ typedef struct {
     /* ipregel_layout.  IPREGEL_LAYOUT_AS_GIVEN (0): the arrays are used in the given numbering.
      * IPREGEL_LAYOUT_DEGREE (1): the LIBRARY relabels the graph during create -- internal ids
      * ascend by decreasing out-degree (ties by original id), the in-adjacency is rebuilt in
-     * library-owned memory with every row's sources in ascending internal order, and the
+     * library-owned memory with every row's sources in ascending internal order (above 2^20
+     * vertices: ascending by a monotone class of the internal id -- exact for the low, hot ids,
+     * the top bit and the 40 - 5 - ceil(log2 N) bits below it for the others), and the
      * out-adjacency is derived from it (csr_* may be NULL; if given, only its offsets are read,
      * for the out-degrees).  The layout is what makes the hot senders' outbox values a
      * contiguous, cache-resident prefix (the bandwidth pressure of PAPER.md:169); results, the

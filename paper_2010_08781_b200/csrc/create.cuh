@@ -67,7 +67,15 @@ void compute_fence(cudaStream_t s) {
 
 // windows of the CSC weights' upload when the CSR is derived (the last window's permutation is
 // all that remains after the upload)
-constexpr int kWeightWindows = 16;   // 8: +1.3 ms, 32: +18 ms (create at cfg4)
+constexpr int kWeightWindows = 16;
+// IPREGEL_LAYOUT_DEGREE: bits of the relabel's edge sort key (destination + source class)
+constexpr int kRelabelKeyBits = 40;   // 8: +1.3 ms, 32: +18 ms (create at cfg4)
+
+// The library's side stream for create-time work that overlaps the run stream (the derived
+// CSR's sort, weight permutations).
+void ensure_aux_stream(ipregel_graph* g) {
+    if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+}
 
 // IPREGEL_LAYOUT_DEGREE (include/ipregel.h): internal ids by decreasing out-degree (ties by id),
 // the CSC rebuilt with every row's sources ascending, in library-owned memory; g->vertex_ids
@@ -108,9 +116,15 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     LAUNCH_CHECK();
     exscan_i32(roff, n + 1, tmp, s);
     g_ctrace.mark("relabel order", s);
-    // 2. relabelled edges sorted by (new destination, new source), weights carried along
+    // 2. relabelled edges sorted by (new destination, new source), their CSC positions carried
+    //    along.  The key holds the source's id when 2 x bits <= kRelabelKeyBits (every row
+    //    fully sorted), else a monotone class of it in kRelabelKeyBits - bits bits
+    //    (source_class): at cfg4 a 40-bit sort (5 radix passes) instead of 52 (7) -- rows keep
+    //    the hot sources' exact order, and the gather supersteps run as fast as on fully sorted
+    //    rows (profiles/r02/README.md)
     int bits = 1;
     while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+    const int cbits = std::min(bits, std::max(kRelabelKeyBits - bits, 6));
     int32_t* off = p.graph_mem.alloc<int32_t>(n + 1, s, true);
     int32_t* idx = p.graph_mem.alloc<int32_t>(std::max<int64_t>(E, 1), s);
     uint32_t* w = p.csc_w ? p.graph_mem.alloc<uint32_t>(std::max<int64_t>(E, 1), s) : nullptr;
@@ -120,80 +134,79 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
         unsigned long long* k1 = tmp.alloc<unsigned long long>(E, s);
         int32_t* spare = tmp.alloc<int32_t>(E, s);
         int32_t* row = tmp.alloc<int32_t>(E, s);
+        DeviceBuffers tsrc;   // renamed sources in the old CSC order, until the unpack
+        int32_t* new_src = tsrc.alloc<int32_t>(E, s);
         k_relabel_pack<<<grid_for(p.rows * 32, 256), 256, 0, s>>>(p.csc_off, p.csc_idx, p.rows,
-                                                                  new_of_old, bits, k0);
+                                                                  new_of_old, bits, cbits, k0,
+                                                                  new_src);
         LAUNCH_CHECK();
         cub::DoubleBuffer<unsigned long long> keys(k0, k1);
-        size_t tb = 0;
-        if (w) {
-            // the sort carries each edge's CSC position, so it needs the structure only (from
-            // host memory the weights are still uploading); the weights follow by a gather
-            uint32_t* pos0 = reinterpret_cast<uint32_t*>(spare);
-            uint32_t* pos1 = reinterpret_cast<uint32_t*>(row);
-            k_iota_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(pos0, E);
-            LAUNCH_CHECK();
-            cub::DoubleBuffer<uint32_t> vals(pos0, pos1);
-            CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, E, 0, 2 * bits, s));
-            void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
-            CU(cub::DeviceRadixSort::SortPairs(t, tb, keys, vals, E, 0, 2 * bits, s));
-            if (d.memory == IPREGEL_MEMORY_HOST) CU(cudaStreamWaitEvent(s, p.up_w, 0));
-            k_gather_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
-                vals.Current(), E, p.csc_w, w);
-            LAUNCH_CHECK();
-        } else {
-            CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, E, 0, 2 * bits, s));
-            void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
-            CU(cub::DeviceRadixSort::SortKeys(t, tb, keys, E, 0, 2 * bits, s));
-        }
-        g_ctrace.mark("relabel sorted", s);
-        // 3. indices + offsets (run lengths of the sorted destinations, then a scan)
-        k_relabel_unpack<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
-            keys.Current(), E, bits, idx, row);
+        // the sort carries each edge's CSC position, so it needs the structure only (from host
+        // memory the weights are still uploading); sources and weights follow by gathers
+        uint32_t* pos0 = reinterpret_cast<uint32_t*>(spare);
+        uint32_t* pos1 = reinterpret_cast<uint32_t*>(row);
+        k_iota_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(pos0, E);
         LAUNCH_CHECK();
+        cub::DoubleBuffer<uint32_t> vals(pos0, pos1);
+        size_t tb = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, E, 0, bits + cbits, s));
+        void* t = tmp.alloc<uint8_t>((int64_t)tb, s);
+        CU(cub::DeviceRadixSort::SortPairs(t, tb, keys, vals, E, 0, bits + cbits, s));
+        g_ctrace.mark("relabel sorted", s);
+        // 3. indices + offsets (run lengths of the sorted destinations, then a scan); each
+        //    edge's new row goes to the position buffer the sort did not end in
+        const uint32_t* pos = vals.Current();
+        int32_t* rows_of = pos == pos0 ? row : spare;
+        k_relabel_unpack<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
+            keys.Current(), pos, E, cbits, new_src, idx, rows_of);
+        LAUNCH_CHECK();
+        tsrc.release();
         int32_t* st = tmp.alloc<int32_t>(n, s, true);
-        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(row, E, st,
-                                                                                  off);
+        k_run_bounds<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(rows_of, E,
+                                                                                  st, off);
         k_run_counts<<<grid_for(n, 256), 256, 0, s>>>(st, n, off);
         LAUNCH_CHECK();
         exscan_i32(off, n + 1, tmp, s);
         g_ctrace.mark("relabel csc", s);
+        if (w) {
+            // the weights last: from host memory they land while the steps above run
+            if (d.memory == IPREGEL_MEMORY_HOST) CU(cudaStreamWaitEvent(s, p.up_w, 0));
+            k_gather_u32<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
+                pos, E, p.csc_w, w);
+            LAUNCH_CHECK();
+            g_ctrace.mark("relabel weights", s);
+        }
         // 4. the out-adjacency's indices: the same edges by (new source), a stable sort of the
         //    CSC order (each CSR row lists its destinations ascending), in the buffers of step 2,
-        //    on the aux stream -- create returns without waiting; whatever reads the CSR's
-        //    indices first waits for p.csr_done (wait_csr).  Its offsets are roff already.
-        int32_t* ridx = p.graph_mem.alloc<int32_t>(E, s);
-        uint32_t* rw = w ? p.graph_mem.alloc<uint32_t>(E, s) : nullptr;
-        size_t tb2 = 0;
+        //    on the aux stream -- launched by launch_relabel_csr once the tile plans are built
+        //    (their small kernels would otherwise queue behind the sort's), and create returns
+        //    without waiting; whatever reads the CSR's indices first waits for p.csr_done
+        //    (wait_csr).  Its offsets are roff already.
+        RelabelCsr& R = p.relabel_csr;
+        R.ridx = p.graph_mem.alloc<int32_t>(E, s);
+        R.rw = w ? p.graph_mem.alloc<uint32_t>(E, s) : nullptr;
         {
             cub::DoubleBuffer<int32_t> tk(row, spare);
             cub::DoubleBuffer<unsigned long long> tv(k0, k1);
-            CU(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tk, tv, E, 0, bits, s));
+            CU(cub::DeviceRadixSort::SortPairs(nullptr, R.tb, tk, tv, E, 0, bits, s));
         }
-        void* t2 = tmp.alloc<uint8_t>((int64_t)tb2, s);
-        if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
-        cudaStream_t a = g->aux_stream;
-        if (!p.csr_done) CU(cudaEventCreateWithFlags(&p.csr_done, cudaEventDisableTiming));
-        CU(cudaEventRecord(p.csr_done, s));   // the CSC and every temporary are in place
-        CU(cudaStreamWaitEvent(a, p.csr_done, 0));
-        int32_t* kk0 = row;   // E int32 each
-        int32_t* kk1 = spare;
-        CU(cudaMemcpyAsync(kk0, idx, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, a));
-        if (w) k_transpose_pack_w<<<grid_for(n * 32, 256), 256, 0, a>>>(off, n, 0, w, k0);
-        else k_transpose_pack<<<grid_for(n * 32, 256), 256, 0, a>>>(off, n, 0, k0);
-        LAUNCH_CHECK();
-        cub::DoubleBuffer<int32_t> tkeys(kk0, kk1);
-        cub::DoubleBuffer<unsigned long long> tvals(k0, k1);
-        CU(cub::DeviceRadixSort::SortPairs(t2, tb2, tkeys, tvals, E, 0, bits, a));
-        k_unpack_w<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, a>>>(
-            tvals.Current(), E, ridx, rw);
-        LAUNCH_CHECK();
-        CU(cudaEventRecord(p.csr_done, a));
-        g_ctrace.mark("relabel csr (aux)", a);
+        R.t = tmp.alloc<uint8_t>((int64_t)R.tb, s);
+        R.n = n;
+        R.E = E;
+        R.bits = bits;
+        R.off = off;
+        R.idx = idx;
+        R.w = w;
+        R.k0 = k0;
+        R.k1 = k1;
+        R.row = row;
+        R.spare = spare;
+        R.tmp = tmp;   // the temporaries live on until the CSR sort is done
+        tmp.blocks.clear();
+        R.armed = true;
         p.csr_pending = true;
-        // the temporaries are freed on the aux stream, after the CSR sort
-        for (auto& b : tmp.blocks) b.s = a;
-        p.csr_idx = ridx;
-        p.csr_w = rw;
+        p.csr_idx = R.ridx;
+        p.csr_w = R.rw;
     } else {
         p.csr_idx = p.graph_mem.alloc<int32_t>(1, s);
         p.csr_w = w ? p.graph_mem.alloc<uint32_t>(1, s) : nullptr;
@@ -209,6 +222,37 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     g->degree_ordered = true;
     g->gather_policy = g_gather_policy >= 0 ? g_gather_policy : 3;
     g_ctrace.mark("relabel done", s);
+}
+
+// Step 4 of relabel_by_degree on the aux stream (after the tile plans): the CSR's indices and
+// weights by a stable sort of the new CSC by source; the temporaries are freed on the aux stream
+// after it.
+void launch_relabel_csr(ipregel_graph* g, Partition& p) {
+    RelabelCsr& R = p.relabel_csr;
+    if (!R.armed) return;
+    R.armed = false;
+    cudaStream_t s = g->stream;
+    ensure_aux_stream(g);
+    cudaStream_t a = g->aux_stream;
+    if (!p.csr_done) CU(cudaEventCreateWithFlags(&p.csr_done, cudaEventDisableTiming));
+    CU(cudaEventRecord(p.csr_done, s));   // the CSC and every temporary are in place
+    CU(cudaStreamWaitEvent(a, p.csr_done, 0));
+    int32_t* kk0 = R.row;   // E int32 each
+    int32_t* kk1 = R.spare;
+    CU(cudaMemcpyAsync(kk0, R.idx, R.E * sizeof(int32_t), cudaMemcpyDeviceToDevice, a));
+    if (R.w) k_transpose_pack_w<<<grid_for(R.n * 32, 256), 256, 0, a>>>(R.off, R.n, 0, R.w, R.k0);
+    else k_transpose_pack<<<grid_for(R.n * 32, 256), 256, 0, a>>>(R.off, R.n, 0, R.k0);
+    LAUNCH_CHECK();
+    cub::DoubleBuffer<int32_t> tkeys(kk0, kk1);
+    cub::DoubleBuffer<unsigned long long> tvals(R.k0, R.k1);
+    CU(cub::DeviceRadixSort::SortPairs(R.t, R.tb, tkeys, tvals, R.E, 0, R.bits, a));
+    k_unpack_w<<<std::min<unsigned>(grid_for(R.E, 256), sm_grid(16)), 256, 0, a>>>(
+        tvals.Current(), R.E, R.ridx, R.rw);
+    LAUNCH_CHECK();
+    CU(cudaEventRecord(p.csr_done, a));
+    g_ctrace.mark("relabel csr (aux)", a);
+    for (auto& b : R.tmp.blocks) b.s = a;
+    R.tmp.release();
 }
 
 void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d) {
@@ -330,7 +374,7 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         if (p.pend.perm) {
             // permute each weight window as it lands, on a side stream (the run stream goes
             // on with the tile plans); transpose_rows returned with perm complete
-            if (!g->aux_stream) CU(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+            ensure_aux_stream(g);
             for (size_t c = 0; c + 1 < p.wc_bounds.size(); ++c) {
                 CU(cudaStreamWaitEvent(g->aux_stream, p.up_wc[c], 0));
                 k_permute_window<<<sm_grid(8), 256, 0, g->aux_stream>>>(

@@ -172,6 +172,23 @@ struct DeviceBuffers {
     }
 };
 
+// IPREGEL_LAYOUT_DEGREE: what the deferred CSR sort of relabel_by_degree needs (create.cuh).
+struct RelabelCsr {
+    bool armed = false;
+    DeviceBuffers tmp;
+    int64_t n = 0, E = 0;
+    int bits = 0;
+    const int32_t* off = nullptr;
+    const int32_t* idx = nullptr;
+    const uint32_t* w = nullptr;
+    unsigned long long *k0 = nullptr, *k1 = nullptr;
+    int32_t *row = nullptr, *spare = nullptr;
+    void* t = nullptr;
+    size_t tb = 0;
+    int32_t* ridx = nullptr;
+    uint32_t* rw = nullptr;
+};
+
 // Pinned host blocks, cached for the process: cudaMallocHost / cudaFreeHost cost milliseconds
 // (page pinning, a device synchronisation) and showed up as tens of ms of jitter per graph
 // create / destroy, so blocks go back to this cache instead of being freed.
@@ -305,6 +322,7 @@ struct Partition {
     // returns; csr_off is ready.  wait_csr() orders the run stream after them (first use).
     cudaEvent_t csr_done = nullptr;
     bool csr_pending = false;
+    RelabelCsr relabel_csr;           // its launch, deferred to after the tile plans
     std::vector<int64_t> wc_bounds;
     AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device

@@ -280,6 +280,7 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
         for (int i = 0; i < np; ++i) init_partition(g, g->parts[i], descs[i]);
         build_plans(g);
         g_ctrace.mark("plans built", g->stream);
+        for (auto& p : g->parts) launch_relabel_csr(g, p);
         for (auto& p : g->parts) finish_uploads(g, p);
         CU(cudaStreamSynchronize(g->stream));
         g_ctrace.mark("create end", g->stream);

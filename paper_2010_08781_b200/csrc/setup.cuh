@@ -350,26 +350,44 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ perm, int64_t n,
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = in[perm[i]];
 }
-// relabelled edge keys: (new destination << bits) | new source, one warp per CSC row
+// Sort key of a relabelled source inside its row: the id itself when cbits >= bits (rows fully
+// sorted), else a monotone cbits-bit class -- ids below 2^sub exactly, above that the position
+// of the top bit and the sub = cbits - 5 bits below it -- so the hot low ids (a handful per
+// 128-B line) keep their exact order and only cold ids, one per line anyway, share a class.
+__device__ __forceinline__ uint32_t source_class(uint32_t s, int bits, int cbits) {
+    if (cbits >= bits) return s;
+    const int sub = cbits - 5;
+    if (s < (1u << sub)) return s;
+    const int hb = 32 - __clz(s);   // > sub
+    return ((uint32_t)(hb - sub) << sub) | ((s >> (hb - 1 - sub)) & ((1u << sub) - 1u));
+}
+// relabelled edge keys: (new destination << cbits) | class of the new source, one warp per CSC
+// row (the edge's CSC position travels as the sort's value)
 __global__ void k_relabel_pack(const int32_t* __restrict__ off, const int32_t* __restrict__ idx,
                                int64_t rows, const int32_t* __restrict__ new_of_old, int bits,
-                               unsigned long long* __restrict__ keys) {
+                               int cbits, unsigned long long* __restrict__ keys,
+                               int32_t* __restrict__ new_src) {
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
-    const unsigned long long hi = (unsigned long long)(uint32_t)new_of_old[r] << bits;
-    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32)
-        keys[e] = hi | (uint32_t)new_of_old[idx[e]];
+    const unsigned long long hi = (unsigned long long)(uint32_t)new_of_old[r] << cbits;
+    for (int32_t e = off[r] + lane; e < off[r + 1]; e += 32) {
+        const int32_t u = new_of_old[idx[e]];
+        new_src[e] = u;
+        keys[e] = hi | source_class((uint32_t)u, bits, cbits);
+    }
 }
-// sorted keys -> new CSC indices + each edge's new row (for the run-length offsets)
-__global__ void k_relabel_unpack(const unsigned long long* __restrict__ keys, int64_t edges,
-                                 int bits, int32_t* __restrict__ idx, int32_t* __restrict__ row) {
-    const unsigned long long mask = (1ull << bits) - 1;
+// sorted (key, CSC position) -> new CSC indices (the renamed source at each position, written
+// by k_relabel_pack) + each edge's new row (for the run-length offsets)
+__global__ void k_relabel_unpack(const unsigned long long* __restrict__ keys,
+                                 const uint32_t* __restrict__ pos, int64_t edges, int cbits,
+                                 const int32_t* __restrict__ new_src, int32_t* __restrict__ idx,
+                                 int32_t* __restrict__ row) {
+    // pos[i] lies in the old CSC row of i's row: the gather reads within one row's block
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < edges;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
-        idx[i] = (int32_t)(k & mask);
-        row[i] = (int32_t)(k >> bits);
+        idx[i] = new_src[pos[i]];
+        row[i] = (int32_t)(keys[i] >> cbits);
     }
 }
 

@@ -1,6 +1,6 @@
 """Parity at BASELINE.json's sizes (configs[0..4]) through the C ABI, in the launch
-configuration bench.py times (degree-ordered layout, PageRank pull, CC/SSSP AUTO) and in the
-original layout.
+configuration bench.py times (the library's degree relabel of the original-id CSC, PageRank pull,
+CC/SSSP AUTO), in the fixture's degree-ordered layout and in the original layout.
 
 configs[0..3]: against the oracle run live on the box's CPU (seconds to ~20 s each).
 configs[4] (1.88e9 edges): against tests/golden/cfg4_oracle.json, written by
@@ -30,8 +30,16 @@ def _cuda():
 
 
 def device_graph(cfg, order):
+    """order: True -- the fixture's degree-ordered layout with vertex_ids; False -- original ids;
+    "library" -- original-id CSC only, relabelled by the library (IPREGEL_LAYOUT_DEGREE, the CSR
+    derived on the device): bench.py's graph."""
     import paper_2010_08781_b200 as ipr
     from inputs.gpu import config_graph_device
+    if order == "library":
+        g = config_graph_device(cfg, weighted=True, degree_order=False)
+        G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], None, None,
+                                         g["csc_w"], None, layout=ipr.LAYOUT_DEGREE))
+        return g, G
     g = config_graph_device(cfg, weighted=True, degree_order=order)
     G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
                                      g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
@@ -45,7 +53,7 @@ def check_counters(stats, want):
     np.testing.assert_array_equal(stats["messages"], np.asarray(want["messages"], np.uint64))
 
 
-@pytest.mark.parametrize("order", [True, False])
+@pytest.mark.parametrize("order", [True, False, "library"])
 @pytest.mark.parametrize("name", ["cfg0", "cfg1", "cfg2", "cfg3"])
 def test_config_vs_live_oracle(name, order):
     cfg = inputs.CONFIGS[name]
@@ -78,7 +86,7 @@ def test_config_vs_live_oracle(name, order):
     G.close()
 
 
-@pytest.mark.parametrize("order", [True, False])
+@pytest.mark.parametrize("order", [True, False, "library"])
 def test_cfg4_vs_golden(order):
     if not os.path.exists(GOLDEN4):
         pytest.skip("golden file missing")

@@ -1,5 +1,6 @@
 """cfg4 PageRank, element by element: all 67,108,864 values of the CUDA path (through the C ABI,
-bench.py's launch configuration: degree-ordered layout, pull, k = 10; and the original layout)
+bench.py's launch configuration: the library's degree relabel, pull, k = 10; the fixture's
+degree-ordered layout and the original layout)
 against the oracle's full vector (Fig. 8), computed in the background by
 tests/golden/cfg4_pagerank_full.py (started by tests/conftest.py when this file is collected).
 
@@ -45,16 +46,22 @@ def oracle_cfg4():
     return np.load(out + ".npy"), meta
 
 
-@pytest.mark.parametrize("order", [True, False], ids=["degree_ordered", "original"])
+@pytest.mark.parametrize("order", [True, False, "library"],
+                         ids=["degree_ordered", "original", "library_relabel"])
 def test_cfg4_pagerank_all_vertices(oracle_cfg4, order):
     import paper_2010_08781_b200 as ipr
     from inputs.gpu import config_graph_device
     want, meta = oracle_cfg4
     cfg = inputs.CONFIGS["cfg4"]
-    g = config_graph_device(cfg, weighted=False, degree_order=order)
-    G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
-                                     g["csr_idx"], None, None, g["vertex_ids"],
-                                     degree_ordered=order))
+    if order == "library":   # bench.py's graph: the library relabels the original-id CSC
+        g = config_graph_device(cfg, weighted=False, degree_order=False)
+        G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], None, None,
+                                         layout=ipr.LAYOUT_DEGREE))
+    else:
+        g = config_graph_device(cfg, weighted=False, degree_order=order)
+        G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"],
+                                         g["csr_off"], g["csr_idx"], None, None, g["vertex_ids"],
+                                         degree_ordered=order))
     G.run("pagerank", mode="pull", iterations=cfg.iterations, mass=True)
     v = G.values(host=True)
     s = G.stats()
