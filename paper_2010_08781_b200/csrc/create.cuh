@@ -87,14 +87,17 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     DeviceBuffers tmp;
     g_ctrace.mark("relabel begin", s);
     // 1. out-degrees and the degree order (stable: ties keep ascending ids)
-    uint32_t* deg = tmp.alloc<uint32_t>(n, s, true);
-    if (p.csr_off) {
-        k_degree_from_off<<<grid_for(n, 256), 256, 0, s>>>(p.csr_off, n, deg);
-    } else if (E) {
-        k_degree_hist<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(p.csc_idx, E,
-                                                                                   deg);
+    uint32_t* deg = p.pre_deg;   // counted window by window during the upload (init_partition)
+    if (!deg) {
+        deg = tmp.alloc<uint32_t>(n, s, true);
+        if (p.csr_off) {
+            k_degree_from_off<<<grid_for(n, 256), 256, 0, s>>>(p.csr_off, n, deg);
+        } else if (E) {
+            k_degree_hist<<<std::min<unsigned>(grid_for(E, 256), sm_grid(16)), 256, 0, s>>>(
+                p.csc_idx, E, deg);
+        }
+        LAUNCH_CHECK();
     }
-    LAUNCH_CHECK();
     int32_t* ids = tmp.alloc<int32_t>(n, s);
     k_degree_keys<<<grid_for(n, 256), 256, 0, s>>>(deg, n, ids);
     LAUNCH_CHECK();
@@ -214,6 +217,8 @@ void relabel_by_degree(ipregel_graph* g, Partition& p, const ipregel_graph_desc&
     p.csr_off = roff;
     CU(cudaStreamSynchronize(s));
     tmp.release();
+    p.pre_deg_mem.release();
+    p.pre_deg = nullptr;
     p.csc_off = off;
     p.csc_idx = idx;
     p.csc_w = w;
@@ -289,7 +294,31 @@ void init_partition(ipregel_graph* g, Partition& p, const ipregel_graph_desc& d)
         };
         g_ctrace.mark("uploads begin", cs);
         up(off_d, d.csc_offsets, (p.rows + 1) * 4);
-        up(idx_d, d.csc_indices, d.csc_edges * 4);
+        // the library relabel's out-degree histogram over the CSC sources (no CSR given, no
+        // validation pass to wait for) runs window by window as the indices land, while the rest
+        // uploads -- the GPU is otherwise idle until the structure is complete
+        const bool hist = d.layout == IPREGEL_LAYOUT_DEGREE && !d.csr_offsets && !d.validate &&
+                          idx_d && d.csc_edges >= (int64_t(1) << 24);
+        if (hist) {
+            p.pre_deg = p.pre_deg_mem.alloc<uint32_t>(g->n, s, true);
+            constexpr int kHistWindows = 8;
+            for (int c = 0; c < kHistWindows; ++c) {
+                const int64_t lo = d.csc_edges * c / kHistWindows;
+                const int64_t hi = d.csc_edges * (c + 1) / kHistWindows;
+                up((int32_t*)idx_d + lo, (const int32_t*)d.csc_indices + lo, (hi - lo) * 4);
+                cudaEvent_t e;
+                CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                CU(cudaEventRecord(e, cs));
+                compute_fence(s);
+                CU(cudaStreamWaitEvent(s, e, 0));
+                k_degree_hist<<<std::min<unsigned>(grid_for(hi - lo, 256), sm_grid(16)), 256, 0,
+                                s>>>((const int32_t*)idx_d + lo, hi - lo, p.pre_deg);
+                LAUNCH_CHECK();
+                p.up_hist.push_back(e);   // destroyed with the partition
+            }
+        } else {
+            up(idx_d, d.csc_indices, d.csc_edges * 4);
+        }
         up(roff_d, d.csr_offsets, (p.rows + 1) * 4);
         up(ridx_d, d.csr_indices, d.csr_edges * 4);
         CU(cudaEventRecord(p.up_idx, cs));
@@ -449,12 +478,16 @@ void destroy_graph(ipregel_graph* g) {
         for (cudaEvent_t e : {p.up_idx, p.up_w, p.up_all})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : p.up_wc) cudaEventDestroy(e);
+        for (cudaEvent_t e : p.up_hist) cudaEventDestroy(e);
         if (p.perm_done) cudaEventDestroy(p.perm_done);
         p.perm_done = nullptr;
         if (p.csr_done) cudaEventDestroy(p.csr_done);
         p.csr_done = nullptr;
         p.up_wc.clear();
+        p.up_hist.clear();
         p.pend.tmp.release();
+        p.pre_deg_mem.release();        // non-empty only after a failed create
+        p.relabel_csr.tmp.release();
         pinned_release(p.host_cnt);
         p.host_cnt = nullptr;
     }

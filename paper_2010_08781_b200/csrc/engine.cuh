@@ -317,12 +317,15 @@ struct Partition {
         int64_t edges = 0;
     } pend;
     std::vector<cudaEvent_t> up_wc;   // one per weight window (copy stream)
+    std::vector<cudaEvent_t> up_hist; // one per index window of the relabel's histogram
     cudaEvent_t perm_done = nullptr;  // the last window permuted (aux stream)
     // IPREGEL_LAYOUT_DEGREE: the CSR's indices / weights are built on the aux stream after create
     // returns; csr_off is ready.  wait_csr() orders the run stream after them (first use).
     cudaEvent_t csr_done = nullptr;
     bool csr_pending = false;
     RelabelCsr relabel_csr;           // its launch, deferred to after the tile plans
+    uint32_t* pre_deg = nullptr;      // its out-degree histogram, counted during the upload
+    DeviceBuffers pre_deg_mem;
     std::vector<int64_t> wc_bounds;
     AppState st[4];
     PullCounters* pull_cnt = nullptr;         // device

@@ -312,11 +312,19 @@ __global__ void k_degree_from_off(const int32_t* __restrict__ off, int64_t n,
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < n) deg[v] = (uint32_t)(off[v + 1] - off[v]);
 }
+// (CSC rows list their sources ascending, so a hot source recurs within a warp's 32 consecutive
+// edges: the lanes holding the same id add once, by their count)
 __global__ void k_degree_hist(const int32_t* __restrict__ idx, int64_t edges,
                               uint32_t* __restrict__ deg) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < edges;
-         e += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(deg + idx[e], 1u);
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); e0 < edges;
+         e0 += stride) {
+        const int64_t e = e0 + lane;
+        const int32_t u = e < edges ? idx[e] : -1;
+        const uint32_t same = __match_any_sync(kFull, u);
+        if (u >= 0 && lane == __ffs(same) - 1) atomicAdd(deg + u, (uint32_t)__popc(same));
+    }
 }
 // sort keys: ascending ~deg = descending degree; a stable sort keeps ties in id order
 __global__ void k_degree_keys(uint32_t* __restrict__ deg, int64_t n, int32_t* __restrict__ ids) {
