@@ -114,3 +114,37 @@ def test_cfg4_vs_golden(order):
                                                             np.uint32))
         check_counters(G.stats(), gold["apps"][app])
     G.close()
+
+
+def test_library_relabel_from_host_matches_device():
+    """bench.py's e2e create: the library relabel from pinned HOST memory without validation,
+    where the out-degree histogram runs window by window during the index upload (E >= 2^24),
+    builds the same graph as the relabel from device memory -- every app's values and counters
+    bit-identical (configs[2], 6.7e7 edges)."""
+    import torch
+
+    import paper_2010_08781_b200 as ipr
+    from inputs.gpu import config_graph_device
+    cfg = inputs.CONFIGS["cfg2"]
+    g = config_graph_device(cfg, weighted=True, degree_order=False)
+    assert g["e"] >= 1 << 24
+    host = {}
+    for k in ("csc_off", "csc_idx", "csc_w"):
+        h = torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True)
+        h.copy_(g[k])
+        host[k] = h.numpy()
+    Gd = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], None, None,
+                                      g["csc_w"], None, layout=ipr.LAYOUT_DEGREE))
+    Gh = ipr.Graph(ipr.full_partition(g["n"], g["e"], host["csc_off"], host["csc_idx"], None, None,
+                                      host["csc_w"], None, layout=ipr.LAYOUT_DEGREE),
+                   validate=False)
+    for app in ("pagerank", "cc", "sssp"):
+        mode = "pull" if app == "pagerank" else "auto"
+        Gd.run(app, mode=mode)
+        Gh.run(app, mode=mode)
+        np.testing.assert_array_equal(Gh.values(host=True), Gd.values(host=True))
+        sd, sh = Gd.stats(), Gh.stats()
+        np.testing.assert_array_equal(sh["changed"], sd["changed"])
+        np.testing.assert_array_equal(sh["messages"], sd["messages"])
+    Gd.close()
+    Gh.close()
