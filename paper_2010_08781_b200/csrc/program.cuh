@@ -323,14 +323,15 @@ template <> struct ProgAbsorb<int64_t, 2> {
 };
 
 template <class V>
-__device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
+__device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row, int32_t out_degree,
+                                            int32_t in_degree) {
     ProgCtx x;
     const int64_t v = A.vbase + row;
     x.id = A.ids ? (int64_t)A.ids[v] : v;
     x.num_vertices = A.n;
     x.superstep = A.superstep;
-    x.out_degree = A.out_off[row + 1] - A.out_off[row];
-    x.in_degree = A.in_off[row + 1] - A.in_off[row];
+    x.out_degree = out_degree;
+    x.in_degree = in_degree;
     x.wpar = (int32_t)(A.superstep & 1u);
     x.params = A.params;
     x.aggregate = A.aggregate;
@@ -338,6 +339,10 @@ __device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
     x.agg_acc = 0.0;
     x.agg_n = 0u;
     return x;
+}
+template <class V>
+__device__ __forceinline__ ProgCtx prog_ctx(const ProgArgs<V>& A, int64_t row) {
+    return prog_ctx(A, row, A.out_off[row + 1] - A.out_off[row], A.in_off[row + 1] - A.in_off[row]);
 }
 
 // ---- Fig. 2's IP_send_message and a Pregel aggregator ------------------------------------------
@@ -436,6 +441,28 @@ __device__ __forceinline__ typename P::V prog_p2p_in(const ProgArgs<typename P::
     return m;
 }
 
+// compute on one vertex whose value and degrees were loaded by the caller
+template <class P>
+__device__ __forceinline__ void prog_vertex_loaded(const ProgArgs<typename P::V>& A, int64_t row,
+                                                   typename P::V mailbox, typename P::V val,
+                                                   int32_t out_degree, int32_t in_degree,
+                                                   LaneCounters& c) {
+    using V = typename P::V;
+    using C = ProgComb<V, P::kCombiner>;
+    const ProgCtx x = prog_ctx(A, row, out_degree, in_degree);
+    mailbox = prog_p2p_in<P>(A, row, mailbox);
+    V msg = C::identity();
+    const unsigned f = P::compute(x, &val, mailbox, &msg);
+    A.value[row] = val;
+    if constexpr (P::kAggregates) {
+        if (x.agg_n) {
+            c.agg = c.agg_n ? agg_combine(A.agg_op, c.agg, x.agg_acc) : x.agg_acc;
+            c.agg_n = 1u;
+        }
+    }
+    prog_emit<P>(A, row, x, f, msg, c);
+}
+
 template <class P>
 __device__ __forceinline__ void prog_vertex(const ProgArgs<typename P::V>& A, int64_t row,
                                             typename P::V mailbox, LaneCounters& c) {
@@ -468,21 +495,37 @@ __global__ void __launch_bounds__(256) k_prog_init(ProgArgs<typename P::V> A,
     LaneCounters c{};
     // grid-stride (a few waves of CTAs): one counter flush per CTA, not per 256 rows -- with
     // every vertex broadcasting, 262K CTAs' same-address atomics cost more than the init itself
-    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.rows;
-         row += (int64_t)gridDim.x * blockDim.x) {
-        const ProgCtx x = prog_ctx(A, row);
-        V val = C::identity();
-        V msg = C::identity();
-        const unsigned f = P::init(x, &val, &msg);
-        A.value[row] = val;
-        A.mbox[row] = C::identity();
-        if constexpr (P::kAggregates) {
-            if (x.agg_n) {
-                c.agg = c.agg_n ? agg_combine(A.agg_op, c.agg, x.agg_acc) : x.agg_acc;
-                c.agg_n = 1u;
+    // kInitRows rows per thread, block-strided, their degrees loaded before any store
+    constexpr int kInitRows = 4;
+    for (int64_t blk = blockIdx.x; blk * blockDim.x * kInitRows < A.rows; blk += gridDim.x) {
+        const int64_t base = blk * blockDim.x * kInitRows + threadIdx.x;
+        int32_t od[kInitRows], id[kInitRows];
+#pragma unroll
+        for (int j = 0; j < kInitRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            if (row < A.rows) {
+                od[j] = A.out_off[row + 1] - A.out_off[row];
+                id[j] = A.in_off[row + 1] - A.in_off[row];
             }
         }
-        prog_emit<P, true>(A, row, x, f, msg, c);   // buffer 1 holds a previous run's values
+#pragma unroll
+        for (int j = 0; j < kInitRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            if (row >= A.rows) continue;
+            const ProgCtx x = prog_ctx(A, row, od[j], id[j]);
+            V val = C::identity();
+            V msg = C::identity();
+            const unsigned f = P::init(x, &val, &msg);
+            A.value[row] = val;
+            A.mbox[row] = C::identity();
+            if constexpr (P::kAggregates) {
+                if (x.agg_n) {
+                    c.agg = c.agg_n ? agg_combine(A.agg_op, c.agg, x.agg_acc) : x.agg_acc;
+                    c.agg_n = 1u;
+                }
+            }
+            prog_emit<P, true>(A, row, x, f, msg, c);   // buffer 1 holds a previous run's values
+        }
     }
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
@@ -594,6 +637,7 @@ k_prog_expand(PushAdj adj, const int32_t* __restrict__ e_id, const long long* __
 // recipient bits and skips them all when none has anything to do (the common case of a sparse
 // frontier), else processes them with lane l on rows base + 32 j + l (coalesced stores).
 constexpr int kProgApplyRows = 16;
+constexpr int kApplyBatch = 4;
 template <class P>
 __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
                                                     PullCounters* counters) {
@@ -620,32 +664,60 @@ __global__ void __launch_bounds__(256) k_prog_apply(ProgArgs<typename P::V> A,
         }
     }
     if (__any_sync(kFull, any)) {   // then every row of the warp, coalesced
-        for (int j = 0; j < kProgApplyRows; ++j) {
-            const int64_t row = base + 32 * j + lane;
-            uint32_t word = 0u;
-            if (row < A.rows) {
-                word = A.recv[row >> 5];
+        // the 16 recipient words of the warp's rows (lane j holds word j), then the rows in
+        // batches of kApplyBatch: flag bytes, mailboxes, values and degrees of a batch are loaded
+        // before any of its stores, so the batch's loads are in flight together
+        const int64_t w0 = base >> 5;
+        uint32_t words = 0u, words_p2p = 0u;
+        if (lane < kProgApplyRows && base + 32 * lane < A.rows) {
+            words = A.recv[w0 + lane];
+            if constexpr (P::kSends)
+                if (A.p2p_in_recv) words_p2p = A.p2p_in_recv[w0 + lane];
+        }
+#pragma unroll 1
+        for (int j0 = 0; j0 < kProgApplyRows; j0 += kApplyBatch) {
+            uint8_t fl[kApplyBatch];
+            bool run[kApplyBatch];
+            V m[kApplyBatch], val[kApplyBatch];
+            int32_t od[kApplyBatch], id[kApplyBatch];
+#pragma unroll
+            for (int b = 0; b < kApplyBatch; ++b) {
+                const int64_t row = base + 32 * (j0 + b) + lane;
+                const uint32_t word = __shfl_sync(kFull, words, j0 + b);
                 bool got = (word >> lane) & 1u;
                 if constexpr (P::kSends)
-                    if (A.p2p_in_recv) got = got || ((A.p2p_in_recv[row >> 5] >> lane) & 1u);
-                const uint8_t fl = A.flags[row];
-                if (got || (fl & 2u)) {
-                    const V m = A.mbox[row];
+                    got = got || ((__shfl_sync(kFull, words_p2p, j0 + b) >> lane) & 1u);
+                fl[b] = row < A.rows ? A.flags[row] : (uint8_t)0;
+                run[b] = row < A.rows && (got || (fl[b] & 2u));
+            }
+#pragma unroll
+            for (int b = 0; b < kApplyBatch; ++b) {
+                const int64_t row = base + 32 * (j0 + b) + lane;
+                if (run[b]) {
+                    m[b] = A.mbox[row];
+                    val[b] = A.value[row];
+                    od[b] = A.out_off[row + 1] - A.out_off[row];
+                    id[b] = A.in_off[row + 1] - A.in_off[row];
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < kApplyBatch; ++b) {
+                const int64_t row = base + 32 * (j0 + b) + lane;
+                if (run[b]) {
                     A.mbox[row] = C::identity();
-                    prog_vertex<P>(A, row, m, c);
-                } else if (fl) {
+                    prog_vertex_loaded<P>(A, row, m[b], val[b], od[b], id[b], c);
+                } else if (fl[b]) {
                     // halted and no messages: no broadcast.  The buffer written now holds a
                     // value only if the row broadcast two supersteps ago (bit 2)
-                    if (fl & 4u) {
+                    if (fl[b] & 4u) {
                         A.out_next[A.vbase + row] = C::identity();
                         A.peers.store(A.vbase + row, C::identity());
                     }
-                    A.flags[row] = (uint8_t)((fl & 1u) << 2);
+                    A.flags[row] = (uint8_t)((fl[b] & 1u) << 2);
                 }
             }
-            __syncwarp();   // every lane read the recipient word
-            if (lane == 0 && word) A.recv[row >> 5] = 0u;
         }
+        if (words) A.recv[w0 + lane] = 0u;   // lanes < 16: every lane has read them
     }
     flush_counters(c, s_cnt, counters);
     if constexpr (P::kSettled) flush_mkey(c.mkey, A.mkey_out);
@@ -668,15 +740,37 @@ __global__ void __launch_bounds__(256) k_prog_pull_apply(ProgArgs<typename P::V>
     for (int64_t blk = blockIdx.x; blk * blockDim.x * kProgPullRows < A.rows; blk += gridDim.x) {
         const int64_t base = blk * blockDim.x * kProgPullRows + threadIdx.x;
         V m[kProgPullRows];
+        if constexpr (sizeof(V) == 8) {
+            // 8-byte values: the values and degrees too (PageRank program 74.9 -> 74.0 ms at
+            // cfg4; with 4-byte values it measured slower: Hash-Min 16.1 -> 16.5, SSSP 13.4 -> 13.5)
+            V val[kProgPullRows];
+            int32_t od[kProgPullRows], id[kProgPullRows];
 #pragma unroll
-        for (int j = 0; j < kProgPullRows; ++j) {
-            const int64_t row = base + (int64_t)j * blockDim.x;
-            if (row < A.rows) m[j] = A.mbox[row];
-        }
+            for (int j = 0; j < kProgPullRows; ++j) {
+                const int64_t row = base + (int64_t)j * blockDim.x;
+                if (row < A.rows) {
+                    m[j] = A.mbox[row];
+                    val[j] = A.value[row];
+                    od[j] = A.out_off[row + 1] - A.out_off[row];
+                    id[j] = A.in_off[row + 1] - A.in_off[row];
+                }
+            }
 #pragma unroll
-        for (int j = 0; j < kProgPullRows; ++j) {
-            const int64_t row = base + (int64_t)j * blockDim.x;
-            if (row < A.rows) prog_vertex<P>(A, row, m[j], c);
+            for (int j = 0; j < kProgPullRows; ++j) {
+                const int64_t row = base + (int64_t)j * blockDim.x;
+                if (row < A.rows) prog_vertex_loaded<P>(A, row, m[j], val[j], od[j], id[j], c);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kProgPullRows; ++j) {
+                const int64_t row = base + (int64_t)j * blockDim.x;
+                if (row < A.rows) m[j] = A.mbox[row];
+            }
+#pragma unroll
+            for (int j = 0; j < kProgPullRows; ++j) {
+                const int64_t row = base + (int64_t)j * blockDim.x;
+                if (row < A.rows) prog_vertex<P>(A, row, m[j], c);
+            }
         }
     }
     __syncthreads();
