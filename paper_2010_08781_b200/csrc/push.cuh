@@ -24,8 +24,14 @@ constexpr int kScanThreads = 256;
 constexpr int kWordsPerThread = 4;
 constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;   // 32768 vertices per block
 constexpr int kListPerBlock = 2048;                             // list entries per scan block
-constexpr int kExpandThreads = 256;
-constexpr int kExpandItems = 2048;                               // edges per expand chunk
+#ifndef IPREGEL_EXPAND_THREADS
+#define IPREGEL_EXPAND_THREADS 256
+#endif
+#ifndef IPREGEL_EXPAND_ITEMS
+#define IPREGEL_EXPAND_ITEMS 512   // 2048: SSSP 11.85 ms, forced push 58.9; 1024: 11.45 / 41; 512: 11.32 / 34.5 (cfg4)
+#endif
+constexpr int kExpandThreads = IPREGEL_EXPAND_THREADS;
+constexpr int kExpandItems = IPREGEL_EXPAND_ITEMS;               // edges per expand chunk
 
 struct FrontierCounters {
     unsigned long long changed;   // vertices that broadcast (bits set)
