@@ -15,11 +15,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg4")
 ap.add_argument("--apps", default="cc,sssp,pagerank")
 ap.add_argument("--modes", default="auto")
+ap.add_argument("--relabel", action="store_true",
+                help="original-id CSC relabelled by the library (bench.py's graph)")
 a = ap.parse_args()
-g = config_graph_device(a.config, weighted=True, degree_order=True)
-G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
-                                 g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
-                                 degree_ordered=True))
+g = config_graph_device(a.config, weighted=True, degree_order=not a.relabel)
+if a.relabel:
+    G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], None, None,
+                                     g["csc_w"], None, layout=ipr.LAYOUT_DEGREE))
+else:
+    G = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
+                                     g["csr_idx"], g["csc_w"], g["csr_w"], g["vertex_ids"],
+                                     degree_ordered=True))
 for app in a.apps.split(","):
     for mode in a.modes.split(","):
         m = "pull" if app == "pagerank" and mode == "auto" else mode
