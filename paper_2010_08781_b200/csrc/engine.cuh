@@ -302,6 +302,7 @@ struct Partition {
     const int32_t* csr_idx = nullptr;
     const uint32_t* csr_w = nullptr;
     TilePlan plan_csc, plan_csr;
+    FlagPlan plan_flag;           // PageRank pull over the row-end-flagged CSC (pr_flag.cuh)
     PushAdj push_sssp, push_cc;   // out-edges of every source that land in the owned range
     bool push_view_ready = false;
     int64_t nondangling = 0;

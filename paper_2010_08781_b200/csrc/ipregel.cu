@@ -10,6 +10,7 @@
 // partitions, and the host reads the counters to decide termination ("every active vertex has
 // been processed and every outgoing message delivered").
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -29,6 +30,7 @@
 #include "../../include/ipregel.h"
 #include "common.cuh"
 #include "pull.cuh"
+#include "pr_flag.cuh"
 #include "push.cuh"
 #include "program.cuh"
 #include "setup.cuh"
@@ -37,6 +39,7 @@
 using namespace ipr;
 
 #include "engine.cuh"
+#include "pr_flag_host.cuh"
 #include "run_apps.cuh"
 #include "create.cuh"
 #include "run_programs.cuh"

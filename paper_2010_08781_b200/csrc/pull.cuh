@@ -226,6 +226,10 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
     int write_rank;
     int track;                                // to convergence: rank holds r_{s-1}; fold |dr|
     double* mass;                             // mass check: this superstep's [sum r, sum_nd r]
+    // k_pr_finish<., true>: sums by ordinal among rows with in-edges (pr_flag.cuh)
+    const double* __restrict__ sumc = nullptr;
+    const uint32_t* __restrict__ nzbits = nullptr;
+    const int32_t* __restrict__ nzpre = nullptr;
     const void* gather_base() const { return contrib_cur; }
     __device__ const T* gptr() const { return contrib_cur; }
     __device__ bool absorbed(int32_t) const { return false; }
@@ -885,8 +889,10 @@ constexpr int kPrFinishRows = IPREGEL_PR_FINISH_ROWS;
 // kMode: 0 general (runtime flags: to-convergence / mass-check runs), 1 broadcast only
 // (supersteps 1 .. k-1 of a fixed-k run), 2 rank only (superstep k).  The fixed-k variants fix
 // the flags at compile time: with them at run time the compiler versioned the row loop and the
-// kernel ran 2.3x the instructions (0.31 vs 0.16 ms at cfg4).
-template <int kMode>
+// kernel ran 2.3x the instructions (0.31 vs 0.16 ms at cfg4).  kCompact: the sums come from the
+// flagged superstep (pr_flag.cuh) by ordinal -- row v with in-edges has ordinal nzpre[v / 32] +
+// (rows with in-edges below v in its bitmap word); rows without in-edges sum to 0.
+template <int kMode, bool kCompact = false>
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
     __shared__ unsigned long long s_cnt[5];
@@ -905,7 +911,16 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
 #pragma unroll
     for (int j = 0; j < kPrFinishRows; ++j) {
         const int64_t row = base + (int64_t)j * blockDim.x;
-        sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+        if constexpr (kCompact) {
+            sum[j] = 0.0;
+            if (row < rows) {
+                const uint32_t w = op.nzbits[row >> 5];
+                const uint32_t bit = 1u << (row & 31);
+                if (w & bit) sum[j] = op.sumc[op.nzpre[row >> 5] + __popc(w & (bit - 1u))];
+            }
+        } else {
+            sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+        }
         deg[j] = row < rows && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
     }
 #pragma unroll

@@ -101,6 +101,10 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
         }
         return G.status;
     }
+    // the flagged plan is built (once per graph) before anything is captured
+    if (!push && k > 0 && g_pr_split && g_pr_flag)
+        for (auto& p : g->parts)
+            if (p.rows > 0) ensure_flag_plan(g, p);
     const unsigned long long launches0 = g_launches.load(std::memory_order_relaxed);
     if (graphable) {
         for (uint32_t i = 0; i <= 5 * (k + 1); ++i) ev(g, i);   // events exist before capture
@@ -182,7 +186,23 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.write_rank = write_rank;
                 op.track = track;
                 op.mass = mass_slot(step);
-                if (g_pr_split) {
+                if (g_pr_split && g_pr_flag) {
+                    // the flagged superstep (pr_flag.cuh): sums by ordinal, then Fig. 8's update
+                    launch_pr_flag(g, p, op.contrib_cur, s);
+                    T.rec(4 * (k + 1) + step);   // range kernel + fixup done (stats part_ms)
+                    op.sumc = p.plan_flag.sumc;
+                    op.nzbits = p.plan_flag.nzbits;
+                    op.nzpre = p.plan_flag.nzpre;
+                    const unsigned fg = grid_for(ceil_div(p.rows, kPrFinishRows), 256);
+                    if (track || mass || (broadcast && write_rank))
+                        k_pr_finish<0, true><<<fg, 256, 0, s>>>(op, p.rows,
+                                                                track ? p.pull_cnt : nullptr);
+                    else if (broadcast)
+                        k_pr_finish<1, true><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
+                    else
+                        k_pr_finish<2, true><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
+                    LAUNCH_CHECK();
+                } else if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
                     sop.sum_out = op.contrib_next;

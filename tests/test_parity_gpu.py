@@ -708,6 +708,49 @@ def test_pagerank_pull_bit_identical_random_bounds(exchange):
         Gp.close()
 
 
+@pytest.mark.parametrize("exchange", ["fused", "collective"])
+def test_pagerank_flagged_hub_rows_and_phantom_ends(exchange):
+    """The flagged PageRank superstep (pr_flag.cuh) where its bookkeeping is stretched: hub rows
+    of 300,000 and 140,000 in-edges (cut by more than 16 range boundaries: the warp-tree joins),
+    a run of 2,000-edge rows (chunks inside rows, rows cut by one boundary), runs of rows without
+    in-edges between rows of 1-3 in-edges (ordinals skip them; chunks with many ends), and
+    partitions whose first edge is off the 8192-edge range grid (phantom end at local -1), or
+    whose first rows have no in-edges -- equal to the oracle (Fig. 8), the mass invariant on the
+    GPU's sums, and bit-identical across partitionings."""
+    rng = np.random.default_rng(17)
+    n = 6000
+    deg = rng.integers(0, 4, n) * (rng.random(n) < 0.5)
+    deg[10] = 300000
+    deg[2500] = 140000
+    deg[4000:4100] = 2000
+    deg[5990:] = 0
+    dst = np.repeat(np.arange(n), deg)
+    src = rng.integers(0, n, len(dst))
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    o = oracle.pagerank(n, src, dst, k=10)
+    g = csr_csc(n, src, dst)
+    nd = int(np.count_nonzero(np.bincount(src, minlength=n)))
+    G1 = make_graph(g, weighted=False)
+    G1.run("pagerank", mode="pull", mass=True)
+    v1 = G1.values(host=True)
+    checkers.assert_pagerank_mass(G1.stats(), n, nd)
+    G1.close()
+    err = np.abs(v1 - o["values"])
+    assert err.max() <= PR_ABS
+    assert (err / np.abs(o["values"])).max() <= PR_REL
+    empty = np.flatnonzero(deg == 0)
+    cases = [[0, 11, n], [0, 2500, 2501, n], [0, 4050, n], [0, int(empty[3]), n],
+             [0, 10, 11, 3000, n]]
+    for _ in range(6):
+        cases.append([0] + sorted(rng.choice(np.arange(1, n), 3, replace=False).tolist()) + [n])
+    for bounds in cases:
+        Gp = make_graph(g, partitions=len(bounds) - 1, weighted=False, bounds=np.array(bounds))
+        Gp.run("pagerank", mode="pull", exchange=exchange)
+        np.testing.assert_array_equal(Gp.values(host=True), v1, err_msg=str(bounds))
+        Gp.close()
+
+
 @pytest.mark.parametrize("n,m", [(1, 0), (5, 0), (7, 3), (300, 40000)])
 def test_host_create_derived_csr_small_and_empty(n, m, monkeypatch):
     """The host-memory create pipeline (structure upload, derived CSR, weight windows permuted on

@@ -84,14 +84,16 @@ def test_paper_programs_equal_the_oracle(seed, mode, parts, exchange):
     G.close()
 
 
-def test_program_pagerank_pull_equals_builtin_bit_for_bit():
-    # same combine tree (pull.cuh ranges) and the same IEEE operations: identical doubles
+def test_program_pagerank_pull_equals_builtin():
+    # the same IEEE operations per term; the built-in sums each row with the flagged superstep's
+    # combine tree (pr_flag.cuh), the program with the range kernels' (pull.cuh): the two differ
+    # only by summation order, a few ulps after k = 10 supersteps
     n, src, dst, _ = graph(11, n=5000)
     G = make_graph(csr_csc(n, src, dst), weighted=False)
     G.run("pagerank", mode="pull")
     a = G.values(host=True)
     G.run_program(prog("pagerank"), params=[10], mode="pull")
-    np.testing.assert_array_equal(G.values(host=True), a)
+    np.testing.assert_allclose(G.values(host=True), a, rtol=1e-13, atol=0)
     G.close()
 
 
