@@ -24,8 +24,9 @@
 //  * sums are stored by ordinal (sumc); k_pr_finish maps rows to ordinals with a bitmap of the
 //    rows with in-edges plus a per-word prefix count, and rows without in-edges take sum 0;
 //  * a row cut by range boundaries leaves its partial in carry[] of every range it runs through
-//    and its last piece in head[]; k_pull_fixup joins them in a fixed order (as for the range
-//    kernels).
+//    and its last piece in head[]; k_flag_fixup joins them on the device in k_pull_fixup's fixed
+//    order.  Building the plan takes no host round trip (it runs inside the first PageRank run,
+//    which end-to-end callers time).
 //
 // Why (profiles/r02/README.md, tools/meta_lab.cu): the range kernel's time over the raw gather
 // stream went to its row logic -- CSC offset loads on the critical path and ~80 shuffles per chunk
@@ -46,7 +47,6 @@ struct FlagPlan {
     bool ready = false;
     int64_t edges = 0;
     int32_t rows = 0;
-    int32_t nnz = 0;             // rows with in-edges
     int64_t rphase = 0;          // (global edge index of local edge 0) mod kFlagRange
     int32_t num_ranges = 0;
     int32_t* fidx = nullptr;     // [edges] CSC indices, bit 31 set on each row's last edge
@@ -54,12 +54,11 @@ struct FlagPlan {
                                  // before the range); range 0 after a phantom end: (-1, 0)
     uint32_t* nzbits = nullptr;  // [ceil(rows / 32)] rows with in-edges
     int32_t* nzpre = nullptr;    // [ceil(rows / 32)] rows with in-edges before each word
-    double* sumc = nullptr;      // [nnz] combined sums by ordinal
+    double* sumc = nullptr;      // [rows + 1] combined sums by ordinal (ordinals < rows; + 1:
+                                 // k_pr_finish's slack slot)
     double* carry = nullptr;     // [num_ranges] partial of the row leaving the range
     double* head = nullptr;      // [num_ranges] last piece of the row entering the range
     int32_t* ctr = nullptr;      // range counter (zeroed before each launch)
-    int32_t num_groups = 0, num_short = 0;
-    int4* groups = nullptr;      // rows cut by range boundaries: (ordinal, a, b, 0)
 };
 
 // ---- build ---------------------------------------------------------------------------------
@@ -274,10 +273,56 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PRF_MINBLOCKS) k_pr_flag
     }
 }
 
-// k_pull_fixup's op for the flagged plan: rows by ordinal into sumc.
-struct PageRankCompactSum : SumF64, NotAbsorbing, NoAggregate {
-    double* __restrict__ sumc;
-    __device__ void finish(int32_t o, T sum, LaneCounters&) const { sumc[o] = sum; }
-};
+// Rows cut by range boundaries, joined on the device (no host pass over the plan): range b is
+// the last range of a row that started before it when rinfo[b] says "continuing" and range b + 1
+// does not continue the same row.  Its warp walks back over the boundaries a..b that carry the
+// row and folds carry[a - 1], carry[a], ..., carry[b - 1], head[b] in k_pull_fixup's fixed order
+// (spans <= kFixupShortSpan: a left fold; longer: lane-strided partials and the xor tree), which
+// depends on the ranges' global positions only.  One warp per range.
+__global__ void k_flag_fixup(const int2* __restrict__ rinfo, int32_t num_ranges,
+                             const double* __restrict__ carry, const double* __restrict__ head,
+                             double* __restrict__ sumc) {
+    using Op = SumF64;
+    const int lane = threadIdx.x & 31;
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= num_ranges) return;
+    const int2 info = rinfo[b];
+    if (!info.y) return;
+    if (b + 1 < num_ranges) {
+        const int2 nx = rinfo[b + 1];
+        if (nx.y && nx.x == info.x) return;   // the row runs on past range b
+    }
+    int64_t a = b;   // first boundary of the chain
+    for (;;) {
+        const int64_t j = a - 1 - lane;
+        bool ok = false;
+        if (j >= 1) {
+            const int2 r = rinfo[j];
+            ok = r.y && r.x == info.x;
+        }
+        const uint32_t brk = __ballot_sync(kFull, !ok);
+        if (brk) {
+            a -= __ffs(brk) - 1;
+            break;
+        }
+        a -= 32;
+    }
+    double acc;
+    if (b - a + 1 <= kFixupShortSpan) {
+        if (lane != 0) return;
+        acc = carry[a - 1];
+        for (int64_t t = a; t <= b - 1; ++t) acc = Op::combine(acc, carry[t]);
+    } else {
+        acc = Op::identity();
+        for (int64_t t = a - 1 + lane; t <= b - 1; t += 32) acc = Op::combine(acc, carry[t]);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = shfl_xor(acc, d);
+            acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
+        }
+        if (lane != 0) return;
+    }
+    sumc[info.x] = Op::combine(acc, head[b]);
+}
 
 }  // namespace ipr

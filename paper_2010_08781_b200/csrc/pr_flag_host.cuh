@@ -9,8 +9,9 @@ namespace {
 int g_pr_flag = getenv("IPREGEL_PR_FLAG") ? atoi(getenv("IPREGEL_PR_FLAG")) : 1;
 
 // Builds p.plan_flag on the graph's stream (library memory in p.graph_mem, reported by
-// ipregel_memory_footprint).  Device work: a copy of the CSC indices, one pass over the rows, a
-// scan, one binary search per range; the host groups the rows cut by range boundaries.
+// ipregel_memory_footprint), stream-ordered with no host synchronisation and no copy-engine
+// work: a kernel copy of the CSC indices, one pass over the rows, a scan, one binary search per
+// range.
 void ensure_flag_plan(ipregel_graph* g, Partition& p) {
     FlagPlan& F = p.plan_flag;
     if (F.ready) return;
@@ -22,12 +23,14 @@ void ensure_flag_plan(ipregel_graph* g, Partition& p) {
     const int64_t words = ceil_div(std::max<int64_t>(p.rows, 1), 32);
     F.nzbits = p.graph_mem.alloc<uint32_t>(words, s, true);
     F.nzpre = p.graph_mem.alloc<int32_t>(words + 1, s);   // [words]: the total
+    F.sumc = p.graph_mem.alloc<double>(p.rows + 1, s, true);
     DeviceBuffers tmp;
     int32_t* cnt = tmp.alloc<int32_t>(words + 1, s, true);
     if (F.edges > 0) {
         F.fidx = p.graph_mem.alloc<int32_t>(F.edges, s);
-        CU(cudaMemcpyAsync(F.fidx, p.csc_idx, (size_t)F.edges * sizeof(int32_t),
-                           cudaMemcpyDeviceToDevice, s));
+        // a kernel, not cudaMemcpyAsync: a copy-engine copy would queue behind create's
+        // host uploads still in flight (weights), see compute_fence in create.cuh
+        kernel_copy(F.fidx, p.csc_idx, (size_t)F.edges * sizeof(int32_t), s);
     }
     if (p.rows > 0) {
         k_flag_rows<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csc_off, p.rows, F.fidx, F.nzbits, cnt);
@@ -37,11 +40,6 @@ void ensure_flag_plan(ipregel_graph* g, Partition& p) {
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, F.nzpre, (int)(words + 1), s));
     void* t = tmp.alloc<char>((int64_t)tb, s);
     CU(cub::DeviceScan::ExclusiveSum(t, tb, cnt, F.nzpre, (int)(words + 1), s));
-    int32_t* h = static_cast<int32_t*>(g->pinned.get(16, 0));
-    kernel_copy(h, F.nzpre + words, sizeof(int32_t), s);
-    CU(cudaStreamSynchronize(s));
-    F.nnz = h[0];
-    F.sumc = p.graph_mem.alloc<double>(std::max<int32_t>(F.nnz, 1), s);
     const int32_t Q = F.num_ranges;
     if (Q > 0) {
         F.rinfo = p.graph_mem.alloc<int2>(Q, s);
@@ -51,33 +49,8 @@ void ensure_flag_plan(ipregel_graph* g, Partition& p) {
         k_flag_ranges<<<grid_for(Q, 256), 256, 0, s>>>(p.csc_off, F.rows, F.edges, F.rphase, Q,
                                                        F.nzbits, F.nzpre, F.rinfo);
         LAUNCH_CHECK();
-        // rows cut by range boundaries: consecutive boundaries carrying the same row form one
-        // group (ordinal, first boundary a, last boundary b) -- as build_plan
-        int2* hr = static_cast<int2*>(g->pinned.get((size_t)Q * sizeof(int2), 0));
-        kernel_copy(hr, F.rinfo, (size_t)Q * sizeof(int2), s);
-        CU(cudaStreamSynchronize(s));
-        std::vector<int4> groups;
-        for (int32_t b = 1; b < Q; ++b) {
-            if (!hr[b].y) continue;
-            if (!groups.empty() && groups.back().x == hr[b].x && groups.back().z == b - 1)
-                groups.back().z = b;
-            else
-                groups.push_back(make_int4(hr[b].x, b, b, 0));
-        }
-        std::stable_partition(groups.begin(), groups.end(),
-                              [](const int4& G) { return G.z - G.y + 1 <= kFixupShortSpan; });
-        F.num_groups = (int32_t)groups.size();
-        F.num_short = 0;
-        for (const int4& G : groups) F.num_short += (G.z - G.y + 1 <= kFixupShortSpan) ? 1 : 0;
-        if (F.num_groups) {
-            F.groups = p.graph_mem.alloc<int4>(F.num_groups, s);
-            int4* hg = static_cast<int4*>(g->pinned.get(groups.size() * sizeof(int4), 1));
-            memcpy(hg, groups.data(), groups.size() * sizeof(int4));
-            kernel_copy(F.groups, hg, groups.size() * sizeof(int4), s);
-            CU(cudaStreamSynchronize(s));
-        }
     }
-    tmp.release();
+    tmp.release();   // stream-ordered frees
     F.ready = true;
 }
 
@@ -120,13 +93,31 @@ void launch_pr_flag(ipregel_graph* g, Partition& p, const double* contrib_cur, c
     CU(cudaMemsetAsync(F.ctr, 0, sizeof(int32_t), s));
     k_pr_flag<<<pr_flag_grid(F.num_ranges), kPullThreads, 0, s>>>(A);
     LAUNCH_CHECK();
-    if (F.num_groups) {
-        PageRankCompactSum op;
-        op.sumc = F.sumc;
-        k_pull_fixup<PageRankCompactSum><<<fixup_grid(F.num_groups, F.num_short), 256, 0, s>>>(
-            op, F.groups, F.num_groups, F.num_short, F.carry, F.head, nullptr);
+    if (F.num_ranges > 1) {
+        k_flag_fixup<<<grid_for((int64_t)F.num_ranges * 32, 256), 256, 0, s>>>(
+            F.rinfo, F.num_ranges, F.carry, F.head, F.sumc);
         LAUNCH_CHECK();
     }
+}
+
+// Fig. 8's update after the flagged superstep (k_pr_finish<mode, true>): kRows rows per thread
+// (knob IPREGEL_PR_FINISH_ROWS_C: 4, 8 or 16; the ordinal lookup puts a second load in each
+// row's chain, so more rows per thread keep more of them in flight).
+int g_pr_finish_rows_c = getenv("IPREGEL_PR_FINISH_ROWS_C") ? atoi(getenv("IPREGEL_PR_FINISH_ROWS_C")) : 4;
+template <int kRows>
+void launch_pr_finish_rows(const PageRankPull& op, int64_t rows, PullCounters* cnt, int mode,
+                           cudaStream_t s) {
+    const unsigned fg = grid_for(ceil_div(rows, kRows), 256);
+    if (mode == 0) k_pr_finish<0, true, kRows><<<fg, 256, 0, s>>>(op, rows, cnt);
+    else if (mode == 1) k_pr_finish<1, true, kRows><<<fg, 256, 0, s>>>(op, rows, nullptr);
+    else k_pr_finish<2, true, kRows><<<fg, 256, 0, s>>>(op, rows, nullptr);
+    LAUNCH_CHECK();
+}
+void launch_pr_finish_compact(const PageRankPull& op, int64_t rows, PullCounters* cnt, int mode,
+                              cudaStream_t s) {
+    if (g_pr_finish_rows_c == 4) launch_pr_finish_rows<4>(op, rows, cnt, mode, s);
+    else if (g_pr_finish_rows_c == 16) launch_pr_finish_rows<16>(op, rows, cnt, mode, s);
+    else launch_pr_finish_rows<8>(op, rows, cnt, mode, s);
 }
 
 }  // namespace

@@ -892,7 +892,7 @@ constexpr int kPrFinishRows = IPREGEL_PR_FINISH_ROWS;
 // kernel ran 2.3x the instructions (0.31 vs 0.16 ms at cfg4).  kCompact: the sums come from the
 // flagged superstep (pr_flag.cuh) by ordinal -- row v with in-edges has ordinal nzpre[v / 32] +
 // (rows with in-edges below v in its bitmap word); rows without in-edges sum to 0.
-template <int kMode, bool kCompact = false>
+template <int kMode, bool kCompact = false, int kRows = kPrFinishRows>
 __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows,
                                                    PullCounters* counters) {
     __shared__ unsigned long long s_cnt[5];
@@ -904,27 +904,40 @@ __global__ void __launch_bounds__(256) k_pr_finish(PageRankPull op, int64_t rows
         op.mass = nullptr;
     }
     LaneCounters c{0u, 0u, 0u, 0ull};
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kPrFinishRows + threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kRows + threadIdx.x;
     const bool need_deg = op.broadcast || op.mass;
-    double sum[kPrFinishRows];
-    int32_t deg[kPrFinishRows];
+    double sum[kRows];
+    int32_t deg[kRows];
+    if constexpr (kCompact) {
+        // branch-free: every thread loads its words, then the sums at the ordinals (sumc holds
+        // nnz + 1 slots, so the ordinal of a row without in-edges -- at most nnz -- is in bounds)
+        uint32_t w[kRows];
+        int32_t pre[kRows];
 #pragma unroll
-    for (int j = 0; j < kPrFinishRows; ++j) {
-        const int64_t row = base + (int64_t)j * blockDim.x;
-        if constexpr (kCompact) {
-            sum[j] = 0.0;
-            if (row < rows) {
-                const uint32_t w = op.nzbits[row >> 5];
-                const uint32_t bit = 1u << (row & 31);
-                if (w & bit) sum[j] = op.sumc[op.nzpre[row >> 5] + __popc(w & (bit - 1u))];
-            }
-        } else {
-            sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+        for (int j = 0; j < kRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            const int64_t rr = row < rows ? row : 0;
+            w[j] = op.nzbits[rr >> 5];
+            pre[j] = op.nzpre[rr >> 5];
+            deg[j] = row < rows && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
         }
-        deg[j] = row < rows && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            const uint32_t bit = 1u << (row & 31);
+            const double v = op.sumc[pre[j] + __popc(w[j] & (bit - 1u))];
+            sum[j] = (row < rows && (w[j] & bit)) ? v : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+            const int64_t row = base + (int64_t)j * blockDim.x;
+            sum[j] = row < rows ? op.contrib_next[op.vbase + row] : 0.0;
+            deg[j] = row < rows && need_deg ? op.out_off[row + 1] - op.out_off[row] : 0;
+        }
     }
 #pragma unroll
-    for (int j = 0; j < kPrFinishRows; ++j) {
+    for (int j = 0; j < kRows; ++j) {
         const int64_t row = base + (int64_t)j * blockDim.x;
         if (row < rows) op.finish_deg((int32_t)row, sum[j], deg[j], c);
     }

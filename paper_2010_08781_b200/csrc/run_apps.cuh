@@ -193,15 +193,9 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                     op.sumc = p.plan_flag.sumc;
                     op.nzbits = p.plan_flag.nzbits;
                     op.nzpre = p.plan_flag.nzpre;
-                    const unsigned fg = grid_for(ceil_div(p.rows, kPrFinishRows), 256);
-                    if (track || mass || (broadcast && write_rank))
-                        k_pr_finish<0, true><<<fg, 256, 0, s>>>(op, p.rows,
-                                                                track ? p.pull_cnt : nullptr);
-                    else if (broadcast)
-                        k_pr_finish<1, true><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
-                    else
-                        k_pr_finish<2, true><<<fg, 256, 0, s>>>(op, p.rows, nullptr);
-                    LAUNCH_CHECK();
+                    launch_pr_finish_compact(op, p.rows, track ? p.pull_cnt : nullptr,
+                                             track || mass || (broadcast && write_rank) ? 0
+                                                 : (broadcast ? 1 : 2), s);
                 } else if (g_pr_split) {
                     PageRankSum sop;
                     sop.contrib_cur = op.contrib_cur;
