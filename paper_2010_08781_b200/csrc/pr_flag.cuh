@@ -24,8 +24,8 @@
 //  * sums are stored by ordinal (sumc); k_pr_finish maps rows to ordinals with a bitmap of the
 //    rows with in-edges plus a per-word prefix count, and rows without in-edges take sum 0;
 //  * a row cut by range boundaries leaves its partial in carry[] of every range it runs through
-//    and its last piece in head[]; k_flag_fixup joins them on the device in k_pull_fixup's fixed
-//    order.  Building the plan takes no host round trip (it runs inside the first PageRank run,
+//    and its last piece in head[]; k_flag_fixup joins them in k_pull_fixup's fixed order (the
+//    groups found on the device by k_flag_groups when the plan is built).  Building the plan takes no host round trip (it runs inside the first PageRank run,
 //    which end-to-end callers time).
 //
 // Why (profiles/r02/README.md, tools/meta_lab.cu): the range kernel's time over the raw gather
@@ -59,6 +59,9 @@ struct FlagPlan {
     double* carry = nullptr;     // [num_ranges] partial of the row leaving the range
     double* head = nullptr;      // [num_ranges] last piece of the row entering the range
     int32_t* ctr = nullptr;      // range counter (zeroed before each launch)
+    int4* gshort = nullptr;      // rows cut by range boundaries (ordinal, a, b, 0): spans <= 16
+    int4* glong = nullptr;       //   and longer spans (hub rows), [num_ranges] each
+    int32_t* gcount = nullptr;   // [2] their counts (device)
 };
 
 // ---- build ---------------------------------------------------------------------------------
@@ -273,18 +276,18 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PRF_MINBLOCKS) k_pr_flag
     }
 }
 
-// Rows cut by range boundaries, joined on the device (no host pass over the plan): range b is
-// the last range of a row that started before it when rinfo[b] says "continuing" and range b + 1
-// does not continue the same row.  Its warp walks back over the boundaries a..b that carry the
-// row and folds carry[a - 1], carry[a], ..., carry[b - 1], head[b] in k_pull_fixup's fixed order
-// (spans <= kFixupShortSpan: a left fold; longer: lane-strided partials and the xor tree), which
-// depends on the ranges' global positions only.  One warp per range.
-__global__ void k_flag_fixup(const int2* __restrict__ rinfo, int32_t num_ranges,
-                             const double* __restrict__ carry, const double* __restrict__ head,
-                             double* __restrict__ sumc) {
-    using Op = SumF64;
-    const int lane = threadIdx.x & 31;
-    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Rows cut by range boundaries.  Range b is the last range of a row that started before it when
+// rinfo[b] says "continuing" and range b + 1 does not continue the same row; the row's pieces are
+// carry[a - 1], carry[a], ..., carry[b - 1], head[b] for the boundaries a..b that carry it.  The
+// groups (ordinal, a, b) are found once, on the device, when the plan is built (k_flag_groups:
+// short spans and long ones in two lists, in any order) and joined every superstep by
+// k_flag_fixup in k_pull_fixup's fixed order -- spans <= kFixupShortSpan by one thread (a left
+// fold), longer ones by one warp (lane-strided partials, the xor tree) -- which depends on the
+// ranges' global positions only.
+__global__ void k_flag_groups(const int2* __restrict__ rinfo, int32_t num_ranges,
+                              int4* __restrict__ gshort, int4* __restrict__ glong,
+                              int32_t* __restrict__ counts) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= num_ranges) return;
     const int2 info = rinfo[b];
     if (!info.y) return;
@@ -292,37 +295,44 @@ __global__ void k_flag_fixup(const int2* __restrict__ rinfo, int32_t num_ranges,
         const int2 nx = rinfo[b + 1];
         if (nx.y && nx.x == info.x) return;   // the row runs on past range b
     }
-    int64_t a = b;   // first boundary of the chain
-    for (;;) {
-        const int64_t j = a - 1 - lane;
-        bool ok = false;
-        if (j >= 1) {
-            const int2 r = rinfo[j];
-            ok = r.y && r.x == info.x;
-        }
-        const uint32_t brk = __ballot_sync(kFull, !ok);
-        if (brk) {
-            a -= __ffs(brk) - 1;
-            break;
-        }
-        a -= 32;
+    int64_t a = b;
+    while (a - 1 >= 1) {
+        const int2 r = rinfo[a - 1];
+        if (!(r.y && r.x == info.x)) break;
+        --a;
     }
-    double acc;
-    if (b - a + 1 <= kFixupShortSpan) {
-        if (lane != 0) return;
-        acc = carry[a - 1];
-        for (int64_t t = a; t <= b - 1; ++t) acc = Op::combine(acc, carry[t]);
-    } else {
-        acc = Op::identity();
-        for (int64_t t = a - 1 + lane; t <= b - 1; t += 32) acc = Op::combine(acc, carry[t]);
+    const int4 G = make_int4(info.x, (int32_t)a, (int32_t)b, 0);
+    if (b - a + 1 <= kFixupShortSpan) gshort[atomicAdd(&counts[0], 1)] = G;
+    else glong[atomicAdd(&counts[1], 1)] = G;
+}
+
+// Fixed grid, grid-stride over the device-side counts: first every thread takes short groups,
+// then every warp takes long ones.
+__global__ void k_flag_fixup(const int4* __restrict__ gshort, const int4* __restrict__ glong,
+                             const int32_t* __restrict__ counts, const double* __restrict__ carry,
+                             const double* __restrict__ head, double* __restrict__ sumc) {
+    using Op = SumF64;
+    const int lane = threadIdx.x & 31;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int32_t ns = counts[0], nl = counts[1];
+    for (int64_t i = tid; i < ns; i += nthreads) {
+        const int4 G = gshort[i];
+        double acc = carry[G.y - 1];
+        for (int32_t t = G.y; t <= G.z - 1; ++t) acc = Op::combine(acc, carry[t]);
+        sumc[G.x] = Op::combine(acc, head[G.z]);
+    }
+    for (int64_t w = tid >> 5; w < nl; w += nthreads >> 5) {
+        const int4 G = glong[w];
+        double acc = Op::identity();
+        for (int32_t t = G.y - 1 + lane; t <= G.z - 1; t += 32) acc = Op::combine(acc, carry[t]);
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const double o = shfl_xor(acc, d);
             acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
         }
-        if (lane != 0) return;
+        if (lane == 0) sumc[G.x] = Op::combine(acc, head[G.z]);
     }
-    sumc[info.x] = Op::combine(acc, head[b]);
 }
 
 }  // namespace ipr

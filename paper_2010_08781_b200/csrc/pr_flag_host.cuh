@@ -49,6 +49,11 @@ void ensure_flag_plan(ipregel_graph* g, Partition& p) {
         k_flag_ranges<<<grid_for(Q, 256), 256, 0, s>>>(p.csc_off, F.rows, F.edges, F.rphase, Q,
                                                        F.nzbits, F.nzpre, F.rinfo);
         LAUNCH_CHECK();
+        F.gshort = p.graph_mem.alloc<int4>(Q, s);
+        F.glong = p.graph_mem.alloc<int4>(Q, s);
+        F.gcount = p.graph_mem.alloc<int32_t>(2, s, true);
+        k_flag_groups<<<grid_for(Q, 256), 256, 0, s>>>(F.rinfo, Q, F.gshort, F.glong, F.gcount);
+        LAUNCH_CHECK();
     }
     tmp.release();   // stream-ordered frees
     F.ready = true;
@@ -94,8 +99,10 @@ void launch_pr_flag(ipregel_graph* g, Partition& p, const double* contrib_cur, c
     k_pr_flag<<<pr_flag_grid(F.num_ranges), kPullThreads, 0, s>>>(A);
     LAUNCH_CHECK();
     if (F.num_ranges > 1) {
-        k_flag_fixup<<<grid_for((int64_t)F.num_ranges * 32, 256), 256, 0, s>>>(
-            F.rinfo, F.num_ranges, F.carry, F.head, F.sumc);
+        // groups <= num_ranges / 1 (short) or num_ranges / 17 (long): a fixed grid strides them
+        const unsigned fg = std::max<unsigned>(
+            1, std::min<unsigned>(grid_for(F.num_ranges, 256), sm_grid(4)));
+        k_flag_fixup<<<fg, 256, 0, s>>>(F.gshort, F.glong, F.gcount, F.carry, F.head, F.sumc);
         LAUNCH_CHECK();
     }
 }

@@ -18,7 +18,9 @@ FIXTURE = ("cub::", "DeviceRadixSort", "DeviceSegmentedRadixSort", "(anonymous n
            # graph create (outside every timed superstep): relabel, derived CSR, plans
            "k_transpose", "k_degree_", "k_relabel_", "k_gather_u32", "k_iota_u32", "k_run_",
            "k_invert_perm", "k_plan_", "k_chunk_", "k_unpack_w", "k_count_nondangling",
-           "k_validate", "k_copy_words", "k_noop")
+           "k_validate", "k_copy_words", "k_noop",
+           # the flagged PageRank plan, built once per graph before its first PageRank run
+           "k_flag_rows", "k_flag_ranges")
 
 FULL_METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -28,6 +30,10 @@ FULL_METRICS = [
     "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "lts__t_requests_srcunit_tex_op_read.sum",
+    "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
