@@ -13,7 +13,9 @@ messages of superstep s-1) per second of device time, whole job (all ranks).  Th
 (7.5 GB per adjacency array) are larger than L2, so no flush is needed between steps.
 
 Extra keys: roofline (dominant kernel: the PageRank pull gather, algorithmic bytes per launch
-12E + 16N over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs), cpu_baseline
+12E + 24N over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs; frac_16N on
+12E + 16N; request_bound: its L1 -> L2 gather requests against one request per SM per clock, the
+limit it actually meets), cpu_baseline
 (the oracle on a bounded sample, rank 0, N=1), e2e (host buffers through the C ABI, copies
 inside the timed region), clocks (nvidia-smi sampled during the timed region), gpu_launches.
 """
@@ -121,6 +123,28 @@ def ncu_traffic():
             return float(json.load(f)["dram_bytes_per_launch"])
     except Exception:
         return None
+
+
+def request_bound(range_ms, clocks, sms):
+    """The limit the PageRank range kernel meets (profiles/r02/prf_ncu_full_s38.json): its
+    L1 -> L2 read requests (one per distinct 128-byte line per warp gather, ncu
+    lts__t_requests_srcunit_tex_op_read) against one request per SM per SM clock -- ncu shows the
+    L1 -> XBAR request path 89 % busy and the L2 tag lookups 84 %, DRAM at 42 %."""
+    p = os.path.join(ROOT, "profiles", "r02", "prf_ncu_full_s38.json")
+    try:
+        with open(p) as f:
+            caps = json.load(f)
+        req = next(float(k["metrics"]["lts__t_requests_srcunit_tex_op_read.sum"]["value"])
+                   for k in caps if k["kernel"].startswith("k_pr_flag"))
+    except Exception:
+        return None
+    mhz = (clocks or {}).get("sm_mhz") or 0
+    if not mhz or not range_ms:
+        return None
+    cap = sms * mhz * 1e6 * range_ms * 1e-3
+    return {"requests_per_launch": req, "source": "profiles/r02/prf_ncu_full_s38.json",
+            "limit": "1 L1->L2 request per SM per clock", "sm_mhz": mhz,
+            "frac": req / cap}
 
 
 def device_info(device):
@@ -413,8 +437,8 @@ def main():
         mb16 = 12.0 * e + 16.0 * n if world == 1 else np.mean(mb) - 8.0 * (n / world)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(),
-                "kernel": "PageRank gather superstep: k_pull_ranges<PageRankSum> + "
-                          "k_pull_fixup + k_pr_finish (Fig. 8 update)",
+                "kernel": "PageRank gather superstep: k_pr_flag + k_flag_fixup + "
+                          "k_pr_finish (Fig. 8 update)",
                 "bytes_per_launch": float(np.mean(mb)),
                 "model": "SURVEY.md 8(d): 12 B/edge (4 B index + 8 B gathered f64 outbox) + "
                          "24 B/vertex (CSC offset, out-degree, rank, next outbox)",
@@ -441,9 +465,13 @@ def main():
               "state_bytes_per_vertex": round(sb / (n / world), 2),
               "note": "vertex state is Theta(N) (single-slot mailboxes, PAPER.md:205-211, "
                       ":476-480); library graph bytes: the relabelled CSC and the derived CSR "
-                      "(IPREGEL_LAYOUT_DEGREE) plus the range plans; the user's arrays are "
-                      "borrowed"}
+                      "(IPREGEL_LAYOUT_DEGREE), the range plans, and PageRank's row-end-flagged "
+                      "copy of the CSC indices (4 B per edge, pr_flag.cuh); the user's arrays "
+                      "are borrowed"}
 
+    if roof is not None:
+        roof["request_bound"] = request_bound(roof["range_kernel_ms"], clk.summary(),
+                                              device_info(local)["sms"])
     # e2e: host buffers through the C ABI, H2D of the graph + D2H of every result in the region
     e2e = None
     G.close()   # its device state goes back to the pool for the e2e graphs
