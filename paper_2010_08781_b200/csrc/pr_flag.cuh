@@ -59,6 +59,8 @@ struct FlagPlan {
     double* carry = nullptr;     // [num_ranges] partial of the row leaving the range
     double* head = nullptr;      // [num_ranges] last piece of the row entering the range
     int32_t* ctr = nullptr;      // range counter (zeroed before each launch)
+    int2* rowdeg = nullptr;      // [rows] by ordinal: (row, out-degree) of each row with in-edges
+                                 // (the fused update, k_pr_flag<true>)
     int4* gshort = nullptr;      // rows cut by range boundaries (ordinal, a, b, 0): spans <= 16
     int4* glong = nullptr;       //   and longer spans (hub rows), [num_ranges] each
     int32_t* gcount = nullptr;   // [2] their counts (device)
@@ -124,7 +126,36 @@ struct FlagArgs {
     int gather_policy;
     uint32_t ghot, gtotal;
     int32_t l1hot;
+    // k_pr_flag<true>: Fig. 8's update in the epilogue (broadcasting supersteps of a fixed-k run)
+    const int2* rowdeg;
+    double* contrib_next;        // the next outbox replica (global ids)
+    PeerSlots<double> peers;     // fused exchange: the other replicas
+    int64_t vbase;
+    double ratio;
 };
+
+// Fig. 8's update of the row with ordinal o and combined sum `sum` (broadcasting superstep): the
+// same IEEE operations as PageRankPull::finish_deg, so the result is bit-identical to the split
+// path (k_pr_finish).
+__device__ __forceinline__ void flag_update(const FlagArgs& A, int32_t o, double sum) {
+    const int2 rd = A.rowdeg[o];
+    const double r = __dadd_rn(A.ratio, __dmul_rn(0.85, sum));
+    const double x = rd.y > 0 ? __ddiv_rn(r, (double)rd.y) : 0.0;
+    A.contrib_next[A.vbase + rd.x] = x;
+    A.peers.store(A.vbase + rd.x, x);
+}
+
+// Per row with in-edges: its (row, out-degree) at its ordinal.
+__global__ void k_flag_rowdeg(const int32_t* __restrict__ in_off, const int32_t* __restrict__ out_off,
+                              int64_t rows, const uint32_t* __restrict__ nzbits,
+                              const int32_t* __restrict__ nzpre, int2* __restrict__ rowdeg) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    if (in_off[r + 1] == in_off[r]) return;
+    const uint32_t w = nzbits[r >> 5];
+    const int32_t o = nzpre[r >> 5] + __popc(w & ((1u << (r & 31)) - 1u));
+    rowdeg[o] = make_int2((int32_t)r, out_off[r + 1] - out_off[r]);
+}
 
 #ifndef IPREGEL_PRF_MINBLOCKS
 #define IPREGEL_PRF_MINBLOCKS 3
@@ -159,6 +190,7 @@ __device__ __forceinline__ void flag_gather(const FlagArgs& A, const int32_t (&r
     }
 }
 
+template <bool kFuse>
 __global__ void __launch_bounds__(kPullThreads, IPREGEL_PRF_MINBLOCKS) k_pr_flag(FlagArgs A) {
     using Op = SumF64;
     __shared__ __align__(16) double s_w[kWarpsPerCta][kChunk];
@@ -178,7 +210,10 @@ __global__ void __launch_bounds__(kPullThreads, IPREGEL_PRF_MINBLOCKS) k_pr_flag
         const int32_t hord = info.y ? info.x : INT_MIN;   // its piece here goes to head[q]
         auto emit = [&](int32_t o, double v) {
             if (o == hord) A.head[q] = v;
-            else if (o >= 0) A.sumc[o] = v;
+            else if (o >= 0) {
+                if constexpr (kFuse) flag_update(A, o, v);
+                else A.sumc[o] = v;
+            }
         };
         int32_t I[4];
         double G[4];
@@ -308,9 +343,11 @@ __global__ void k_flag_groups(const int2* __restrict__ rinfo, int32_t num_ranges
 
 // Fixed grid, grid-stride over the device-side counts: first every thread takes short groups,
 // then every warp takes long ones.
+template <bool kFuse>
 __global__ void k_flag_fixup(const int4* __restrict__ gshort, const int4* __restrict__ glong,
                              const int32_t* __restrict__ counts, const double* __restrict__ carry,
-                             const double* __restrict__ head, double* __restrict__ sumc) {
+                             const double* __restrict__ head, double* __restrict__ sumc,
+                             FlagArgs A) {
     using Op = SumF64;
     const int lane = threadIdx.x & 31;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -320,7 +357,9 @@ __global__ void k_flag_fixup(const int4* __restrict__ gshort, const int4* __rest
         const int4 G = gshort[i];
         double acc = carry[G.y - 1];
         for (int32_t t = G.y; t <= G.z - 1; ++t) acc = Op::combine(acc, carry[t]);
-        sumc[G.x] = Op::combine(acc, head[G.z]);
+        acc = Op::combine(acc, head[G.z]);
+        if constexpr (kFuse) flag_update(A, G.x, acc);
+        else sumc[G.x] = acc;
     }
     for (int64_t w = tid >> 5; w < nl; w += nthreads >> 5) {
         const int4 G = glong[w];
@@ -331,7 +370,11 @@ __global__ void k_flag_fixup(const int4* __restrict__ gshort, const int4* __rest
             const double o = shfl_xor(acc, d);
             acc = (lane & d) ? Op::combine(o, acc) : Op::combine(acc, o);
         }
-        if (lane == 0) sumc[G.x] = Op::combine(acc, head[G.z]);
+        if (lane == 0) {
+            acc = Op::combine(acc, head[G.z]);
+            if constexpr (kFuse) flag_update(A, G.x, acc);
+            else sumc[G.x] = acc;
+        }
     }
 }
 

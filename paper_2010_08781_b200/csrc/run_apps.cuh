@@ -186,7 +186,14 @@ ipregel_status run_pagerank(ipregel_graph* g, uint32_t max_steps, const ipregel_
                 op.write_rank = write_rank;
                 op.track = track;
                 op.mass = mass_slot(step);
-                if (g_pr_split && g_pr_flag) {
+                if (g_pr_split && g_pr_flag && g_pr_fuse && step >= 3 && broadcast &&
+                    !write_rank && !track && !mass) {
+                    // the flagged superstep with Fig. 8's update in its epilogue (the outbox
+                    // entries of rows without in-edges were written by supersteps 1 and 2)
+                    launch_pr_flag(g, p, op.contrib_cur, s, true, op.contrib_next, op.peers,
+                                   ratio);
+                    T.rec(4 * (k + 1) + step);   // no separate update pass
+                } else if (g_pr_split && g_pr_flag) {
                     // the flagged superstep (pr_flag.cuh): sums by ordinal, then Fig. 8's update
                     launch_pr_flag(g, p, op.contrib_cur, s);
                     T.rec(4 * (k + 1) + step);   // range kernel + fixup done (stats part_ms)
