@@ -55,10 +55,12 @@ void ensure_flag_plan(ipregel_graph* g, Partition& p) {
         k_flag_ranges<<<grid_for(Q, 256), 256, 0, s>>>(p.csc_off, F.rows, F.edges, F.rphase, Q,
                                                        F.nzbits, F.nzpre, F.rinfo);
         LAUNCH_CHECK();
-        F.rowdeg = p.graph_mem.alloc<int2>(std::max<int64_t>(p.rows, 1), s);
-        k_flag_rowdeg<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csc_off, p.csr_off, p.rows,
-                                                             F.nzbits, F.nzpre, F.rowdeg);
-        LAUNCH_CHECK();
+        if (g_pr_fuse) {   // only the fused update reads it
+            F.rowdeg = p.graph_mem.alloc<int2>(std::max<int64_t>(p.rows, 1), s);
+            k_flag_rowdeg<<<grid_for(p.rows, 256), 256, 0, s>>>(p.csc_off, p.csr_off, p.rows,
+                                                                 F.nzbits, F.nzpre, F.rowdeg);
+            LAUNCH_CHECK();
+        }
         F.gshort = p.graph_mem.alloc<int4>(Q, s);
         F.glong = p.graph_mem.alloc<int4>(Q, s);
         F.gcount = p.graph_mem.alloc<int32_t>(2, s, true);

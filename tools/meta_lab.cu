@@ -454,18 +454,30 @@ __global__ void __launch_bounds__(256, kMB) k_meta4(const int32_t* __restrict__ 
 }
 
 // v9/v10: index-bit row-end flags (bit 31 of the CSC index), gathers kAhead chunks ahead
-template <int kBlk, int kAhead>
-__global__ void __launch_bounds__(256, 3) k_flag(const int32_t* __restrict__ idx,
+__device__ __forceinline__ double ld_cold(const double* base, int32_t u, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+        : "=d"(r) : "l"(base + u), "l"(pol));
+    return r;
+}
+template <int kBlk, int kAhead, int kThreads = 256, int kMinB = 3, int kH = 0>
+__global__ void __launch_bounds__(kThreads, kMinB) k_flag(const int32_t* __restrict__ idx,
                                                  const int32_t* __restrict__ ord, int64_t E,
                                                  int64_t nch, const double* __restrict__ vals,
                                                  double* __restrict__ sumc, double* carry_out,
                                                  int* ctr, uint32_t gtotal, int order,
                                                  int64_t nblk) {
-    __shared__ __align__(16) double s_w[8][128];
+    extern __shared__ __align__(16) double s_dyn[];
+    double* s_hot = s_dyn;                       // [kH]
+    double* s_wall = s_dyn + kH;                 // [warps][128]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double* sw = s_w[wid];
+    double* sw = s_wall + wid * 128;
     const uint64_t pol = pol_first();
     const uint64_t gp = pol_range(vals, 64u << 20, gtotal);
+    if (kH > 0) {
+        for (int i = threadIdx.x; i < kH; i += kThreads) s_hot[i] = vals[i];
+        __syncthreads();
+    }
     for (;;) {
         int t = lane == 0 ? atomicAdd(ctr, 1) : 0;
         t = __shfl_sync(kFull, t, 0);
@@ -485,7 +497,8 @@ __global__ void __launch_bounds__(256, 3) k_flag(const int32_t* __restrict__ idx
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int32_t u = r[k] & 0x7fffffff;
-                gg[k] = u != 0x7fffffff ? ld_valp(vals, u, gp) : 0.0;
+                if (kH > 0) gg[k] = u < kH ? s_hot[u] : (u != 0x7fffffff ? ld_cold(vals, u, gp) : 0.0);
+                else gg[k] = u != 0x7fffffff ? ld_valp(vals, u, gp) : 0.0;
                 ff[k] = __ballot_sync(kFull, r[k] < 0);
             }
         };
@@ -620,6 +633,13 @@ float run_meta_lab(int variant, const int32_t* idx, const uint4* mask, const int
     const int64_t nch = (E + kChunk - 1) / kChunk;
     const int64_t nblk = (nch + kBlk - 1) / kBlk;
     const int grid = 148 * ctas_per_sm;
+    static bool attr = false;
+    if (!attr) {
+        attr = true;
+        cudaFuncSetAttribute(k_flag<kBlk, 1, 768, 1, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 24 * 1024);
+        cudaFuncSetAttribute(k_flag<kBlk, 1, 768, 1, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8 + 24 * 1024);
+        cudaFuncSetAttribute(k_flag<kBlk, 1, 768, 1, 25088>, cudaFuncAttributeMaxDynamicSharedMemorySize, 25088 * 8 + 24 * 1024);
+    }
     const uint32_t gtotal = (uint32_t)(n_vals * 8);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -642,17 +662,25 @@ float run_meta_lab(int variant, const int32_t* idx, const uint4* mask, const int
         else if (variant == 6)
             k_meta4<kBlk, 3, 2><<<grid, 256>>>(idx, mask, ord, E, nch, vals, sumc, carry, ctr,
                                                gtotal, order, nblk);
+        else if (variant == 13)
+            k_flag<kBlk, 1, 768, 1, 8192><<<148, 768, 8192 * 8 + 24 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal, order, nblk);
+        else if (variant == 14)
+            k_flag<kBlk, 1, 768, 1, 16384><<<148, 768, 16384 * 8 + 24 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal, order, nblk);
+        else if (variant == 15)
+            k_flag<kBlk, 1, 768, 1, 25088><<<148, 768, 25088 * 8 + 24 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal, order, nblk);
+        else if (variant == 16)
+            k_flag<kBlk, 1, 768, 1, 0><<<148, 768, 24 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal, order, nblk);
         else if (variant == 9)
-            k_flag<kBlk, 1><<<grid, 256>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
+            k_flag<kBlk, 1><<<grid, 256, 8 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
                                            order, nblk);
         else if (variant == 10)
-            k_flag<kBlk, 2><<<grid, 256>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
+            k_flag<kBlk, 2><<<grid, 256, 8 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
                                            order, nblk);
         else if (variant == 11)
-            k_flag<32, 2><<<grid, 256>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
+            k_flag<32, 2><<<grid, 256, 8 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
                                          order, (nch + 31) / 32);
         else if (variant == 12)
-            k_flag<128, 2><<<grid, 256>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
+            k_flag<128, 2><<<grid, 256, 8 * 1024>>>(idx, ord, E, nch, vals, sumc, carry, ctr, gtotal,
                                           order, (nch + 127) / 128);
         else if (variant == 8)
             k_meta4<kBlk, 3, 3><<<grid, 256>>>(idx, mask, ord, E, nch, vals, sumc, carry, ctr,
