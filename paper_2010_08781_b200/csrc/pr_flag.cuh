@@ -25,13 +25,18 @@
 //    rows with in-edges plus a per-word prefix count, and rows without in-edges take sum 0;
 //  * a row cut by range boundaries leaves its partial in carry[] of every range it runs through
 //    and its last piece in head[]; k_flag_fixup joins them in k_pull_fixup's fixed order (the
-//    groups found on the device by k_flag_groups when the plan is built).  Building the plan takes no host round trip (it runs inside the first PageRank run,
-//    which end-to-end callers time).
+//    groups found on the device by k_flag_groups when the plan is built).  Building the plan
+//    takes no host round trip (it runs inside the first PageRank run, which end-to-end callers
+//    time).
+//
+// The kernel runs at ~0.95 of its gather-request limit (one L1 -> L2 request per SM per clock;
+// ncu: request path 89 % busy, L2 tag lookups 84 %, DRAM 42 %; profiles/r02/prf_ncu_full_s38.json).
 //
 // Why (profiles/r02/README.md, tools/meta_lab.cu): the range kernel's time over the raw gather
 // stream went to its row logic -- CSC offset loads on the critical path and ~80 shuffles per chunk
 // with several row ends (the L1 data pipe also serves the gathers).  Measured on the cfg4 CSC
-// without range joins: raw stream 5.56 ms, offsets-driven bookkeeping 6.3-6.5 ms, this scheme 5.9-6.0.
+// without range joins: raw stream 5.56 ms, offsets-driven bookkeeping 6.3-6.5 ms, this scheme
+// 5.9-6.0.
 #pragma once
 #include "pull.cuh"
 
