@@ -359,6 +359,10 @@ def main():
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
     if use_comm:
+        # a standalone `--comm` run (no torchrun) is a world of one on this host
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                     ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29541")):
+            os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     g, part, bounds = build_graph_device(args.config, rank, world)
     comm = ipr.Comm.from_process_group(local) if use_comm else None
