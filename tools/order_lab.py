@@ -43,7 +43,7 @@ def stable_order(keys_major, keys_minor=None):
     return idx[o2]
 
 
-def requests(old_of_new, tag):
+def requests(old_of_new, tag, shift=4, hot=8192):
     new_of_old = torch.empty(n, dtype=torch.int64, device="cuda")
     new_of_old[old_of_new] = torch.arange(n, device="cuda")
     ns = new_of_old[src.long()]
@@ -53,8 +53,8 @@ def requests(old_of_new, tag):
     key = torch.sort(key).values
     s_sorted = key & ((1 << 26) - 1)
     del key
-    line = s_sorted >> 4
-    cold = s_sorted >= 8192
+    line = s_sorted >> shift
+    cold = s_sorted >= hot
     # change points inside each 32-edge group among cold sources
     pos = torch.arange(E, device="cuda")
     first_in_group = (pos % 32) == 0
@@ -71,6 +71,7 @@ def requests(old_of_new, tag):
 deg_key = -outdeg
 o0 = stable_order(deg_key)
 r0 = requests(o0, "degree order (ties by original id)")
+requests(o0, "degree order, u32 values (32 per line, 16384 in L1)", shift=5, hot=16384)
 # first destination of every source under order 0
 new0 = torch.empty(n, dtype=torch.int64, device="cuda")
 new0[o0] = torch.arange(n, device="cuda")
