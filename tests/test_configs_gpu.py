@@ -148,3 +148,30 @@ def test_library_relabel_from_host_matches_device():
         np.testing.assert_array_equal(sh["messages"], sd["messages"])
     Gd.close()
     Gh.close()
+
+
+@pytest.mark.parametrize("parts", [2, 5])
+def test_cfg3_pagerank_partitions_bit_identical(parts):
+    """configs[3] (1.17e8 edges, degree-ordered layout) split into 2 / 5 edge-balanced destination
+    partitions (loopback; both exchanges): every PageRank value bit-identical to the one-partition
+    run -- the flagged superstep's ranges sit on the global 8192-edge grid and every partition
+    whose first edge is off that grid starts with a phantom end (pr_flag.cuh)."""
+    import paper_2010_08781_b200 as ipr
+    from inputs.gpu import config_graph_device
+    cfg = inputs.CONFIGS["cfg3"]
+    g = config_graph_device(cfg, weighted=False, degree_order=True)
+    G1 = ipr.Graph(ipr.full_partition(g["n"], g["e"], g["csc_off"], g["csc_idx"], g["csr_off"],
+                                      g["csr_idx"], vertex_ids=g["vertex_ids"],
+                                      degree_ordered=True))
+    G1.run("pagerank", mode="pull", iterations=cfg.iterations)
+    v1 = G1.values(host=True)
+    G1.close()
+    bounds = ipr.edge_balanced_bounds(g["csc_off"].cpu().numpy(), parts,
+                                      g["csr_off"].cpu().numpy())
+    for exchange in ("fused", "collective"):
+        ps = ipr.split_partitions(g["n"], g["e"], bounds, g["csc_off"], g["csc_idx"], g["csr_off"],
+                                  g["csr_idx"], vertex_ids=g["vertex_ids"], degree_ordered=True)
+        Gp = ipr.Graph(ps)
+        Gp.run("pagerank", mode="pull", iterations=cfg.iterations, exchange=exchange)
+        np.testing.assert_array_equal(Gp.values(host=True), v1, err_msg=exchange)
+        Gp.close()
