@@ -249,8 +249,10 @@ struct PageRankPull : SumF64, NotAbsorbing, NoAggregate {
             c.dmax = d > c.dmax ? d : c.dmax;
         }
         if (write_rank) rank[row] = r;
-        if (broadcast) {
-            const double x = deg > 0 ? __ddiv_rn(r, (double)deg) : 0.0;
+        if (broadcast && deg > 0) {
+            // a vertex without out-edges is never gathered (it is nobody's in-neighbour): its
+            // outbox slot is left as it is
+            const double x = __ddiv_rn(r, (double)deg);
             contrib_next[vbase + row] = x;
             peers.store(vbase + row, x);
         }
