@@ -284,6 +284,13 @@ static ipregel_status create_common(const ipregel_graph_desc* descs, int np, ipr
         build_plans(g);
         g_ctrace.mark("plans built", g->stream);
         for (auto& p : g->parts) launch_relabel_csr(g, p);
+        // a graph the library relabelled (IPREGEL_LAYOUT_DEGREE) gets PageRank's flagged plan
+        // here, on the run stream while the CSR sorts on the aux stream: its allocations then
+        // come in the same order every time (a create / run / destroy loop keeps a settled
+        // device pool; built lazily in the first run they met the CSR sort's asynchronous frees
+        // in varying order, and some end-to-end steps paid for pool growth: 650-1040 vs 483 ms)
+        for (auto& p : g->parts)
+            if (p.csr_pending && p.rows > 0 && g_pr_flag && g_pr_split) ensure_flag_plan(g, p);
         for (auto& p : g->parts) finish_uploads(g, p);
         CU(cudaStreamSynchronize(g->stream));
         g_ctrace.mark("create end", g->stream);
