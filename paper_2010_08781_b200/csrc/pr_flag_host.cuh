@@ -1,6 +1,7 @@
 // paper_2010_08781_b200/csrc/pr_flag_host.cuh -- host side of the flagged PageRank superstep
-// (pr_flag.cuh): the per-partition plan, built once before a graph's first PageRank pull run, and
-// the launch.  Part of the single translation unit ipregel.cu (after engine.cuh).
+// (pr_flag.cuh): the per-partition plan -- built at create for graphs the library relabelled,
+// else before a graph's first PageRank pull run -- and the launch.  Part of the single
+// translation unit ipregel.cu (after engine.cuh).
 #pragma once
 
 namespace {
