@@ -273,7 +273,9 @@ ipregel_status ipregel_graph_create_partitioned(const ipregel_graph_desc* descs,
                                                 ipregel_graph** out);
 void ipregel_graph_destroy(ipregel_graph* graph);
 
-/* Device bytes held by the handle: graph-side (copies, tile plans) and vertex state (values,
+/* Device bytes held by the handle: graph-side (copies, tile plans, and once PageRank's pull has
+ * run -- or at create for IPREGEL_LAYOUT_DEGREE graphs -- its row-end-flagged copy of the CSC
+ * indices, 4 B per edge, with per-row bookkeeping) and vertex state (values,
  * mailboxes/outboxes, frontier).  The vertex state is Theta(N), independent of E
  * (PAPER.md:205-211, :476-480). */
 ipregel_status ipregel_memory_footprint(ipregel_graph* graph, uint64_t* graph_bytes,
